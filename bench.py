@@ -1,0 +1,452 @@
+#!/usr/bin/env python
+"""Benchmark: batched P-GVIMP on B200 (BASELINE.json metric
+"factor-expectation evals/s and time-to-converge per plan").
+
+Workload (BASELINE configs[4], "C5"): independent point2d plans, N=1000
+intervals (1001 knots), T=10 s, Smolyak k_q=3 (41 sigma points), the C2
+narrow-gap map (two boxes, 281 x 281 cells at 0.05), start 0, goal
+(10,10,0,0) + U(-0.5,0.5)^2 on position from default_rng(2411_03416),
+collision r=0.2 sigma=8, q_c=1, sigma_b=1e-3, the C1 optimizer settings
+(kl_bound=10, beta_max=0.5). --plans plans per GPU (weak scaling: each rank
+runs its own shard of independent plans, no data-path collective).
+
+One step = one Algorithm-1 iteration of every plan on the rank: the whole
+bisection step-size search (GBP marginals + proximal update + KL per probe),
+the factor stage at the accepted state, and cost/convergence control.
+value = factor-expectation evaluations (plan x interior knot, Q sigma points
+each) completed per second, all ranks. Inputs are resident in HBM; the
+working set (~4 GB at 4096 plans) is far larger than L2, so no L2 flush is
+needed between steps.
+
+Also reported: e2e (the same through the C ABI from pinned host buffers),
+time-to-converge of the C1 plan, roofline of the dominant kernel, a CPU
+baseline of the reference on this host.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+N_INTERVALS = 1000
+T_TOTAL = 10.0
+K_Q = 3
+SEED = 2411_03416
+
+
+def c2_map(P):
+    from paper_2411_03416_b200.sdf import Box
+    return P.rasterize([Box(center=np.array([5.0, 1.2]), halfextents=np.array([0.3, 3.4])),
+                        Box(center=np.array([5.0, 8.8]), halfextents=np.array([0.3, 3.4]))],
+                       bounds=[[-2, 12], [-2, 12]], cell_size=0.05)
+
+
+def c5_goals(total: int) -> np.ndarray:
+    rng = np.random.default_rng(SEED)
+    g = np.tile(np.array([10.0, 10.0, 0.0, 0.0]), (total, 1))
+    g[:, :2] += rng.uniform(-0.5, 0.5, size=(total, 2))
+    return g
+
+
+def c5_cfg(P, max_iters):
+    return P.OptimizerConfig(k_q=K_Q, kl_bound=10.0, beta_max=0.5, max_iters=max_iters)
+
+
+def build_problem(P, goals):
+    """Shared prior precision; per-plan info / prior mean / initial mean.
+    The anchored prior mean is affine in the goal, so plan b's mean is the
+    base mean plus n precomputed unit responses (setup only, not timed)."""
+    K, n = N_INTERVALS + 1, 4
+    sys_ltv = P.point_robot_lti(2)(N_INTERVALS, T_TOTAL / N_INTERVALS)
+    base_goal = np.array([10.0, 10.0, 0.0, 0.0])
+    prior = P.assemble_prior(sys_ltv, np.zeros(4), base_goal, 1.0, 1e-3)
+    anchor = np.eye(n) / 1e-3 ** 2
+    resp = np.zeros((n, K, n))
+    for j in range(n):
+        eta = np.zeros((K, n))
+        eta[-1] = anchor[:, j]
+        resp[j] = P.gbp_mean_solve(prior.prec, eta.reshape(-1)).reshape(K, n)
+    dg = goals - base_goal
+    B = len(goals)
+    info = np.repeat(prior.info.reshape(1, K, n), B, axis=0)
+    info[:, -1, :] += dg @ anchor.T
+    pmean = prior.mean.reshape(1, K, n) + np.einsum("bj,jkn->bkn", dg, resp)
+    a = np.linspace(0.0, 1.0, K).reshape(1, K, 1)
+    init = a * goals[:, None, :]
+    return prior, info, pmean, init
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.path = os.path.join(REPO, "gpurun_out", f"clocks_r{index}.csv")
+
+    def __enter__(self):
+        os.makedirs(os.path.dirname(self.path), exist_ok=True)
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), "--query-gpu=clocks.sm,clocks.max.sm,"
+                 "clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+                 "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_power_cap", "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except OSError:
+            self.proc = None
+        time.sleep(0.3)
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            self.proc.wait()
+
+    def summary(self):
+        rows = []
+        try:
+            for line in open(self.path):
+                parts = [p.strip() for p in line.split(",")]
+                if len(parts) >= 7 and parts[0].isdigit():
+                    rows.append(parts)
+        except OSError:
+            pass
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = sorted(int(r[0]) for r in rows)
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({nm for r in rows for nm, v in zip(names, r[3:7]) if v.lower() == "active"})
+        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": int(rows[0][1]), "reasons": reasons,
+                "samples": len(rows)}
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(REPO, "MEASURED_PEAKS.json")) as fh:
+            return json.load(fh)
+    except OSError:
+        return {"hbm_gbs": 6650.0, "fallback": True}
+
+
+def cpu_baseline_reference(steps_iters: int = 1):
+    """The reference (oracle/_ref, built from /root/reference sources) on one
+    C5 plan, single process, for `steps_iters` iterations of run_pgvimp
+    (threads=1). Returns factor evals/s and the sample description."""
+    ref = os.path.join(REPO, "oracle", "_ref")
+    code = f"""
+import sys, time, json, numpy as np
+sys.path.insert(0, {ref!r})
+import gvplan
+from gvplan.sdf import Box
+from gvplan import optimizer as O
+sdf = gvplan.rasterize([Box(center=np.array([5.0,1.2]), halfextents=np.array([0.3,3.4])),
+                        Box(center=np.array([5.0,8.8]), halfextents=np.array([0.3,3.4]))],
+                       bounds=[[-2,12],[-2,12]], cell_size=0.05)
+env = O.Environment(sdf=sdf, model=gvplan.CollisionModel(0.2, 8.0))
+rng = np.random.default_rng({SEED})
+goal = np.array([10.0,10.0,0,0]); goal[:2] += rng.uniform(-0.5,0.5,size=(1,2))[0]
+sys_ltv = gvplan.point_robot_lti(2)({N_INTERVALS}, {T_TOTAL}/{N_INTERVALS})
+prior = gvplan.assemble_prior(sys_ltv, np.zeros(4), goal, 1.0, 1e-3)
+cfg = gvplan.OptimizerConfig(k_q=3, kl_bound=10.0, beta_max=0.5, max_iters={steps_iters}, threads=1)
+t0 = time.perf_counter()
+res = gvplan.run_pgvimp(sys_ltv, env, cfg, np.zeros(4), goal, 1.0, 1e-3, prior=prior)
+dt = time.perf_counter() - t0
+print(json.dumps({{"seconds": dt, "iterations": res.iterations, "ext": gvplan.HAVE_EXTENSION}}))
+"""
+    env = dict(os.environ, OMP_NUM_THREADS="1", OPENBLAS_NUM_THREADS="1", MKL_NUM_THREADS="1")
+    out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env, timeout=900)
+    if out.returncode != 0:
+        return None, out.stderr[-500:]
+    r = json.loads(out.stdout.strip().splitlines()[-1])
+    # factor evals: the initial factor stage + one per iteration (optimizer.py:338-357)
+    evals = (N_INTERVALS - 1) * (r["iterations"] + 1)
+    return {"value": evals / r["seconds"], "unit": "factor-evals/s", "cores": 1, "kind": "reference",
+            "sample": f"1 C5 plan (N={N_INTERVALS}, k_q=3) x {r['iterations']} run_pgvimp iteration(s) "
+                      f"incl. initial marginals+factor stage, gvplan from oracle/_ref "
+                      f"(Cython kernel: {r['ext']}), threads=1, {r['seconds']:.2f} s"}, None
+
+
+def run_reference_arm(args):
+    """--impl reference: the reference's CPU implementation of the path on
+    all host cores (one plan per process), rank 0 only."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import multiprocessing as mp
+
+    lanes = len(os.sched_getaffinity(0))
+    total_steps = args.warmup + args.steps
+    ref = os.path.join(REPO, "oracle", "_ref")
+    if not os.path.isdir(os.path.join(ref, "gvplan")):
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built (run oracle/build_ref.sh)"}))
+        return
+    ctx = mp.get_context("spawn")
+    with ctx.Pool(lanes, initializer=_ref_worker_init, initargs=(ref,)) as pool:
+        pool.map(_ref_worker_warm, range(lanes))  # prior assembly per worker, untimed
+        times = []
+        evals = 0
+        for step in range(total_steps):
+            t0 = time.perf_counter()
+            res = pool.map(_ref_worker_step, [(step, w) for w in range(lanes)])
+            dt = time.perf_counter() - t0
+            if step >= args.warmup:
+                times.append(dt)
+                evals += sum(res)
+    wall = sum(times)
+    value = evals / wall
+    line = {"metric": "factor-expectation evals/s", "value": value, "unit": "factor-evals/s",
+            "impl": "reference", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * wall / len(times), "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"C5 sample: {lanes} independent point2d plans (one per host core) x 1 "
+                                   f"run_pgvimp iteration per step, N={N_INTERVALS}, k_q=3, C2 map",
+                       "plans_per_step": lanes, "N": N_INTERVALS, "k_q": K_Q},
+            "cpu_baseline": {"value": value, "unit": "factor-evals/s", "cores": lanes, "kind": "reference",
+                             "sample": f"{lanes} plans x 1 iteration per step, multiprocessing, gvplan from oracle/_ref"},
+            "e2e": {"value": value, "unit": "factor-evals/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+
+
+_REF = {}
+
+
+def _ref_worker_init(ref):
+    os.environ["OMP_NUM_THREADS"] = "1"
+    sys.path.insert(0, ref)
+
+
+def _ref_worker_warm(w):
+    import gvplan
+    from gvplan import optimizer as O
+    from gvplan.sdf import Box
+    sdf = gvplan.rasterize([Box(center=np.array([5.0, 1.2]), halfextents=np.array([0.3, 3.4])),
+                            Box(center=np.array([5.0, 8.8]), halfextents=np.array([0.3, 3.4]))],
+                           bounds=[[-2, 12], [-2, 12]], cell_size=0.05)
+    goal = c5_goals(w + 1)[w]
+    sys_ltv = gvplan.point_robot_lti(2)(N_INTERVALS, T_TOTAL / N_INTERVALS)
+    _REF.update(env=O.Environment(sdf=sdf, model=gvplan.CollisionModel(0.2, 8.0)), goal=goal, sys=sys_ltv,
+                prior=gvplan.assemble_prior(sys_ltv, np.zeros(4), goal, 1.0, 1e-3), gvplan=gvplan)
+    return w
+
+
+def _ref_worker_step(arg):
+    g = _REF["gvplan"]
+    cfg = g.OptimizerConfig(k_q=K_Q, kl_bound=10.0, beta_max=0.5, max_iters=1, threads=1)
+    res = g.run_pgvimp(_REF["sys"], _REF["env"], cfg, np.zeros(4), _REF["goal"], 1.0, 1e-3, prior=_REF["prior"])
+    return (N_INTERVALS - 1) * res.iterations
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--plans", type=int, default=4096, help="plans per GPU")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-c1", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference_arm(args)
+
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    import paper_2411_03416_b200 as P
+    from paper_2411_03416_b200 import _native
+
+    _native.load().gvp_device_count()
+    # the library's runtime follows the device torch made current for this rank
+    B = args.plans
+    goals = c5_goals(B * world)[rank * B:(rank + 1) * B]
+    prior, info, pmean, init = build_problem(P, goals)
+    K, n = N_INTERVALS + 1, 4
+    F = K - 2
+    sdf = c2_map(P)
+    model = P.CollisionModel(0.2, 8.0)
+    rule = P.smolyak_rule(K_Q, n)
+    max_iters = args.warmup + 2 * args.steps + 4
+    eng = P.PlanBatch(B, K, n, sdf, model, rule, c5_cfg(P, max_iters), shared_prior=True)
+
+    # problem resident in HBM (plan-minor torch tensors), loaded device-to-device
+    from paper_2411_03416_b200.engine import to_plan_minor
+    dev = torch.device("cuda", local)
+    t_kd = torch.from_numpy(np.ascontiguousarray(prior.prec.diag_stack)).to(dev)
+    t_ko = torch.from_numpy(np.ascontiguousarray(prior.prec.off_stack)).to(dev)
+    t_info = torch.from_numpy(to_plan_minor(info)).to(dev)
+    t_pm = torch.from_numpy(to_plan_minor(pmean)).to(dev)
+    t_m0 = torch.from_numpy(to_plan_minor(init)).to(dev)
+    torch.cuda.synchronize()
+
+    def load_device():
+        eng.load_device(t_kd.data_ptr(), t_ko.data_ptr(), t_info.data_ptr(), t_pm.data_ptr(), t_m0.data_ptr())
+
+    stream = torch.cuda.ExternalStream(eng.stream_ptr(), device=dev)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def sum_over_ranks(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        return float(t.item())
+
+    # ---------------- timed region: K steps, inputs resident in HBM
+    load_device()
+    eng.step(args.warmup, sync=True)
+    it_before = eng.summary()["iterations"].astype(np.int64)
+    launches_before = eng.launches()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        barrier()
+        torch.cuda.synchronize()
+        ev0.record(stream)
+        eng.step(args.steps)
+        ev1.record(stream)
+        ev1.synchronize()
+        torch.cuda.synchronize()
+        barrier()
+    ms = ev0.elapsed_time(ev1)
+    launches = eng.launches() - launches_before
+    it_after = eng.summary()["iterations"].astype(np.int64)
+    evals = float((it_after - it_before).sum() * F)
+    ms_max = max_over_ranks(ms)
+    evals_all = sum_over_ranks(evals)
+    value = evals_all / (ms_max / 1e3)
+
+    # ---------------- per-kernel device times (events around each kernel)
+    kms = eng.step_profiled(args.steps)
+    it_prof = eng.summary()["iterations"].astype(np.int64)
+    plans_prof = float((it_prof - it_after).sum())
+    # ---------------- e2e: through the C ABI from pinned host buffers
+    pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()  # noqa: E731
+    h_kd, h_ko = pin(prior.prec.diag_stack), pin(prior.prec.off_stack)
+    h_info, h_pm, h_m0 = pin(to_plan_minor(info)), pin(to_plan_minor(pmean)), pin(to_plan_minor(init))
+    h_rec = torch.empty((max_iters, B, 8), dtype=torch.float64).pin_memory().numpy()
+    h2d = h_kd.nbytes + h_ko.nbytes + h_info.nbytes + h_pm.nbytes + h_m0.nbytes
+    barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t_wall = time.perf_counter()
+    e0.record(stream)
+    eng.load(h_kd, h_ko, info, pmean, init) if False else \
+        eng.lib.gvp_engine_load(eng.handle, _native.ptr(h_kd), _native.ptr(h_ko), _native.ptr(h_info),
+                                _native.ptr(h_pm), _native.ptr(h_m0))
+    eng.step(args.steps)
+    eng.lib.gvp_engine_get_records(eng.handle, _native.ptr(h_rec))
+    e1.record(stream)
+    e1.synchronize()
+    e2e_ms = max_over_ranks(max(e0.elapsed_time(e1), (time.perf_counter() - t_wall) * 1e3))
+    d2h = h_rec.nbytes
+    e2e_evals = sum_over_ranks(float(np.isfinite(h_rec[:, :, 0]).sum() * F))
+    e2e_value = e2e_evals / (e2e_ms / 1e3)
+
+    result = None
+    if rank == 0:
+        peaks = measured_peaks()
+        hbm = float(peaks.get("hbm_gbs", 6650.0))
+        steps_prof = max(args.steps, 1)
+        sel_ms = kms[0] / steps_prof
+        fac_ms = kms[1] / steps_prof
+        ctl_ms = kms[2] / steps_prof
+        # algorithmic bytes per launch:
+        #  select_step: per plan per knot, read mu, Lambda (diag+off), info, g_mu, G_diag, prior
+        #  mean (64 doubles) + write mu', Lambda', Sigma_ii, Sigma_i,i+1 (68 doubles); the
+        #  shared prior precision once per launch.
+        sel_bytes = B * K * 132 * 8 + K * 32 * 8
+        #  factor stage: 8 (n^2 + 3n + 1) = 232 B per factor
+        fac_bytes = B * F * 232
+        dominant = "select_step" if sel_ms >= fac_ms else "factor_grads"
+        if dominant == "select_step":
+            ach = sel_bytes / (sel_ms / 1e3) / 1e9
+        else:
+            ach = fac_bytes / (fac_ms / 1e3) / 1e9
+        fac_ach = fac_bytes / (fac_ms / 1e3) / 1e9 if fac_ms > 0 else None
+        result = {
+            "metric": "factor-expectation evals/s",
+            "value": value,
+            "unit": "factor-evals/s",
+            "n_gpus": world,
+            "steps": args.steps,
+            "warmup": args.warmup,
+            "ms_per_step": ms_max / args.steps,
+            "higher_is_better": True,
+            "scaling": "weak",
+            "vs_baseline": None,
+            "dtype": "f64",
+            "data": "synthetic",
+            "config": {"workload": f"C5 batched sweep: {B} independent point2d plans per GPU, N={N_INTERVALS} "
+                                   f"(1001 knots), k_q=3 (41 sigma points), C2 narrow-gap map 281x281, "
+                                   "C1 optimizer settings; step = one full P-GVIMP iteration "
+                                   "(bisection step selection + factor stage + control)",
+                       "plans_per_gpu": B, "plans_total": B * world, "N": N_INTERVALS, "k_q": K_Q,
+                       "sigma_points": int(rule.npoints), "parallelism": f"plan-sharded x{world}",
+                       "l2": "working set > L2 (no flush needed)"},
+            "sigma_point_evals_per_s": value * rule.npoints,
+            "plan_iterations_per_s": value / F,
+            "gpu_launches": int(launches),
+            "kernel_ms_per_step": {"select_step": sel_ms, "factor_grads": fac_ms, "control": ctl_ms},
+            "roofline": {"kernel": dominant, "bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s",
+                         "frac": ach / hbm, "traffic": None,
+                         "peak_source": "MEASURED_PEAKS.json hbm_gbs" + (" (fallback)" if peaks.get("fallback") else ""),
+                         "factor_grads_achieved_gbs": fac_ach,
+                         "factor_grads_frac": (fac_ach / hbm) if fac_ach else None},
+            "e2e": {"value": e2e_value, "unit": "factor-evals/s", "h2d_bytes_per_step": h2d // max(args.steps, 1),
+                    "d2h_bytes_per_step": d2h // max(args.steps, 1),
+                    "what": "gvp_engine_load from pinned host + steps + records D2H, one C-ABI call chain"},
+            "clocks": clk.summary(),
+        }
+    # ---------------- time-to-converge of one plan (C1 pinned), rank 0
+    if rank == 0 and not args.no_c1:
+        sdf1 = P.rasterize([P.sdf.Disc(center=np.array([1.1, 0.55]), radius=0.45)], bounds=[[-2, 4], [-2, 4]],
+                           cell_size=0.05)
+        env1 = P.Environment(sdf1, P.CollisionModel(0.2, 8.0))
+        sys1 = P.point_robot_lti(2)(50, 3.0 / 50)
+        cfg1 = P.OptimizerConfig(k_q=3, kl_bound=10.0, beta_max=0.5, max_iters=600)
+        pr1 = P.assemble_prior(sys1, np.zeros(4), np.array([2.0, 1.5, 0, 0]), 1.0, 1e-3)
+        P.run_pgvimp(sys1, env1, cfg1, np.zeros(4), np.array([2.0, 1.5, 0, 0]), 1.0, 1e-3, prior=pr1)  # warm
+        t0 = time.perf_counter()
+        r1 = P.run_pgvimp(sys1, env1, cfg1, np.zeros(4), np.array([2.0, 1.5, 0, 0]), 1.0, 1e-3, prior=pr1)
+        c1_ms = (time.perf_counter() - t0) * 1e3
+        result["time_to_converge"] = {"config": "C1 pinned: point2d N=50, k_q=3, kl_bound=10, beta_max=0.5",
+                                      "ms": c1_ms, "iterations": r1.iterations, "converged": r1.converged,
+                                      "reference_iterations": 94}
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cb, err = cpu_baseline_reference(1)
+        result["cpu_baseline"] = cb if cb else {"value": None, "error": err}
+    if rank == 0:
+        print(json.dumps(result))
+    eng.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,218 @@
+/*
+ * gvp_b200 — C ABI of the B200-native P-GVIMP engine (libgvp_b200.so).
+ *
+ * Plain C: pointers, sizes, status codes. No torch or CUDA-runtime types
+ * leak through the signatures except an opaque stream handle (void*) on the
+ * *_dev entry points; 0 means the library's own stream.
+ *
+ * Two families of entry points:
+ *
+ *  1. Drop-in host entry points (gvp_factor_expectations, gvp_gbp_marginals,
+ *     ...). Host pointers, blocking, one plan. Each one replaces one function
+ *     of the reference package `gvplan` (/root/reference/pkg/src/gvplan) and
+ *     keeps its argument meaning; the reference location is cited on each.
+ *     Block-tridiagonal matrices are passed stacked: diag (nblocks, n, n),
+ *     off (nblocks-1, n, n), C order — the reference's lists of blocks
+ *     (blocktri.py:48-66) stacked with np.stack.
+ *
+ *  2. The batched engine (gvp_engine_*): B independent plans resident in HBM,
+ *     the whole Algorithm-1 loop (optimizer.py:299-401) on device. Batched
+ *     arrays are "plan-minor": element e of knot i of plan b is at
+ *     [(i * E + e) * B + b] (E = n*n for blocks, n for vectors), so a warp of
+ *     consecutive plans reads 256 contiguous bytes per element. For B = 1
+ *     this is exactly the stacked layout of family 1.
+ *
+ * Status codes map to the reference's exceptions.
+ */
+#ifndef GVP_B200_H
+#define GVP_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ------------------------------------------------------------ status codes */
+#define GVP_OK 0
+#define GVP_ERR_NOT_SPD 1          /* NotPositiveDefiniteError (blocktri.py:20); where = knot */
+#define GVP_ERR_NONFINITE 2        /* FactorEvaluationError (factors.py:34-37); where = factor index */
+#define GVP_ERR_NO_FEASIBLE_STEP 3 /* RuntimeError "no feasible step size" (optimizer.py:217-221) */
+#define GVP_ERR_SQRT 4             /* gaussian_sqrt needed its eigh root (quadrature.py:178-181) */
+#define GVP_ERR_ARG -1             /* bad argument (ValueError) */
+#define GVP_ERR_UNSUPPORTED -2     /* block size n outside 1..8, or grid ndim not 2/3 */
+#define GVP_ERR_CUDA -3            /* CUDA runtime failure; see gvp_last_error() */
+#define GVP_ERR_NO_DEVICE -4       /* no CUDA device visible */
+
+/* "where" sub-codes for GVP_ERR_NOT_SPD raised by the step machinery */
+#define GVP_WHERE_MEAN_SOLVE_BIAS (1 << 30) /* pivot failed in the proximal mean solve */
+
+/* Human-readable description of the last error on this thread. */
+const char* gvp_last_error(void);
+/* Library version string. */
+const char* gvp_version(void);
+/* Number of visible CUDA devices (0 if none); never fails. */
+int gvp_device_count(void);
+
+/* ------------------------------------------------- 1. drop-in host entry points */
+
+/* Hinge-collision quadrature moments of every factor.
+ * Replaces gvplan._kernels.factor_expectations (_kernels.pyx:132-177; numpy
+ * twin _kernels_py.py:16-53). means (nfac, n), chols (nfac, n, n) (any square
+ * root; the full n x n product L xi is formed like _kernels.pyx:107-112),
+ * points (npts, n), weights (npts), grid of shape grid_shape[0..grid_ndim-1]
+ * = (ny, nx) or (nz, ny, nx), x fastest. pos_dim is accepted and, like the
+ * compiled reference kernel, the grid's ndim decides the position dims.
+ * Outputs e0 (nfac), e1 (nfac, n), e2 (nfac, n, n), *oob = number of
+ * border-clamped sigma points. */
+int gvp_factor_expectations(const double* means, const double* chols, int64_t nfac, int32_t n,
+                            const double* points, const double* weights, int64_t npts,
+                            const double* grid, int32_t grid_ndim, const int64_t* grid_shape,
+                            const double* origin, double cell_size, double radius_eps,
+                            double sigma_obs, int32_t pos_dim, double* e0, double* e1,
+                            double* e2, int64_t* oob);
+
+/* Fused factor stage of one plan: per interior knot i = 1..nblocks-2, the
+ * Cholesky root of covs[i] (with the 1e-10 jitter retry of
+ * quadrature.py:164-177), the quadrature moments, and the moment-form
+ * gradients of factors.py:95-104. Replaces the body of
+ * gvplan.factors.evaluate_all_factors (factors.py:167-225) after the marginal
+ * extraction. mean (nblocks, n), covs (nblocks, n, n). Outputs e_psi
+ * (nblocks-2, clamped at 0 like factors.py:218-224), g_mu (nblocks-2, n),
+ * g_sigma (nblocks-2, n, n), *oob. On GVP_ERR_NONFINITE *where is the
+ * factor_index (= knot) of the first bad factor. */
+int gvp_evaluate_factors(const double* mean, const double* covs, int64_t nblocks, int32_t n,
+                         const double* points, const double* weights, int64_t npts,
+                         const double* grid, int32_t grid_ndim, const int64_t* grid_shape,
+                         const double* origin, double cell_size, double radius_eps,
+                         double sigma_obs, double* e_psi, double* g_mu, double* g_sigma,
+                         int64_t* oob, int64_t* where);
+
+/* Marginal covariance blocks of an SPD block-tridiagonal precision by exact
+ * chain GBP. Replaces gvplan.gbp.gbp_marginals (gbp.py:43-80). covs (nblocks,
+ * n, n), crosses (nblocks-1, n, n). GVP_ERR_NOT_SPD: *where = knot whose
+ * belief precision failed. */
+int gvp_gbp_marginals(const double* diag, const double* off, int64_t nblocks, int32_t n,
+                      double* covs, double* crosses, int64_t* where);
+
+/* Solve Lambda mu = eta. Replaces gvplan.gbp.gbp_mean_solve (gbp.py:83-106).
+ * GVP_ERR_NOT_SPD: *where = pivot block. */
+int gvp_gbp_mean_solve(const double* diag, const double* off, const double* info,
+                       int64_t nblocks, int32_t n, double* out, int64_t* where);
+
+/* log det by forward Schur pivots. Replaces
+ * gvplan.blocktri.logdet_block_tridiag (blocktri.py:151-174). */
+int gvp_logdet_block_tridiag(const double* diag, const double* off, int64_t nblocks, int32_t n,
+                             double* out, int64_t* where);
+
+/* One closed-form KL-proximal step. Replaces gvplan.optimizer.proximal_update
+ * (optimizer.py:129-161). cur (mean, diag, off), prior (kdiag, koff, info),
+ * gradients (g_mu, gdiag, goff). Outputs the next mean/diag/off (precision
+ * symmetrised, not SPD-checked). GVP_ERR_NOT_SPD from the mean solve:
+ * *where = pivot block. */
+int gvp_proximal_update(const double* mean, const double* diag, const double* off,
+                        const double* kdiag, const double* koff, const double* info,
+                        const double* g_mu, const double* gdiag, const double* goff,
+                        int64_t nblocks, int32_t n, double beta, double temp,
+                        double* out_mean, double* out_diag, double* out_off, int64_t* where);
+
+/* Largest feasible beta by bisection, whole search on device. Replaces
+ * gvplan.optimizer.select_step_size (optimizer.py:188-231) including its
+ * probe (proximal_update + gbp_marginals + kl_joint). Outputs beta, kl and
+ * the accepted state with its marginals. probe_log (optional, may be NULL):
+ * up to max_probes rows of (beta, feasible, kl); *nprobes = rows written. */
+int gvp_select_step_size(const double* mean, const double* diag, const double* off,
+                         const double* kdiag, const double* koff, const double* info,
+                         const double* g_mu, const double* gdiag, const double* goff,
+                         int64_t nblocks, int32_t n, double temp, double kl_bound,
+                         double beta_min, double beta_max, double* beta, double* kl,
+                         double* out_mean, double* out_diag, double* out_off, double* covs,
+                         double* crosses, double* probe_log, int32_t max_probes,
+                         int32_t* nprobes, int64_t* where);
+
+/* -------------------------------------------------------- 2. batched engine */
+
+typedef struct gvp_plan_config {
+  double kl_bound;       /* OptimizerConfig (optimizer.py:72-87) */
+  double beta_min;
+  double beta_max;
+  double temp_low;
+  double temp_high;
+  double collision_tol;  /* < 0 -> 1e-4 * N (optimizer.py:316-318) */
+  double tol_mean;
+  double tol_cost;
+  double init_cov_scale;
+  int32_t max_iters;
+  int32_t spec_lanes;    /* candidate betas evaluated concurrently per plan (1 = plain bisection) */
+} gvp_plan_config;
+
+typedef struct gvp_engine gvp_engine;
+
+/* nplans independent plans of nknots = N+1 knots, state size n, sharing one
+ * SDF (grid values on host, copied once) and one quadrature rule. If
+ * shared_prior != 0 every plan uses the same prior precision (one copy,
+ * L2-resident); info and prior mean stay per plan. */
+int gvp_engine_create(gvp_engine** out, int32_t nplans, int64_t nknots, int32_t n,
+                      int32_t shared_prior, const double* grid, int32_t grid_ndim,
+                      const int64_t* grid_shape, const double* origin, double cell_size,
+                      double radius_eps, double sigma_obs, const double* points,
+                      const double* weights, int64_t npts, const gvp_plan_config* cfg);
+void gvp_engine_destroy(gvp_engine* e);
+
+/* Upload the problem (host pointers, plan-minor layout): prior precision
+ * kdiag/koff (one plan's blocks if shared_prior), info and prior mean
+ * (nknots, n, nplans), initial joint mean (nknots, n, nplans). Resets all
+ * per-plan state (initial_state, optimizer.py:280-296). */
+int gvp_engine_load(gvp_engine* e, const double* kdiag, const double* koff, const double* info,
+                    const double* prior_mean, const double* init_mean);
+/* Same, from device pointers (no host traffic). */
+int gvp_engine_load_dev(gvp_engine* e, const double* kdiag, const double* koff,
+                        const double* info, const double* prior_mean, const double* init_mean);
+
+/* Run up to `iters` more iterations of Algorithm 1 for every active plan
+ * (asynchronous on the engine stream unless sync != 0). */
+int gvp_engine_step(gvp_engine* e, int32_t iters, int32_t sync);
+/* Same as gvp_engine_step but kernel by kernel with CUDA events on the
+ * engine stream; adds the device time of each kernel over the iterations to
+ * ms[0..2] = {select_step, factor_grads, control} (synchronous). */
+int gvp_engine_step_profiled(gvp_engine* e, int32_t iters, double* ms);
+/* The engine's cudaStream_t (as void*), for events/interop. */
+void* gvp_engine_stream(gvp_engine* e);
+/* Block until the engine stream is idle. */
+int gvp_engine_sync(gvp_engine* e);
+/* Number of plans still active (not converged, not failed, below max_iters). */
+int gvp_engine_active(gvp_engine* e, int32_t* nactive);
+
+/* Copy results to host (plan-minor layouts):
+ * mean (nknots, n, B); diag (nknots, n, n, B); off (nknots-1, n, n, B);
+ * covs like diag; crosses like off; any pointer may be NULL. */
+int gvp_engine_get_state(gvp_engine* e, double* mean, double* diag, double* off, double* covs,
+                         double* crosses);
+/* Per-plan summary: converged, iterations, switch_iteration (-1 = none),
+ * status, where (each int32[B]). */
+int gvp_engine_get_summary(gvp_engine* e, int32_t* converged, int32_t* iterations,
+                           int32_t* switch_iteration, int32_t* status, int32_t* where);
+/* Per-iteration records (max_iters, B, GVP_NREC): beta, temperature,
+ * prior_cost, collision_cost, entropy_cost, total_cost, kl_step, mean_shift
+ * (optimizer.py:366-379); rows past a plan's last iteration are NaN. */
+#define GVP_NREC 8
+int gvp_engine_get_records(gvp_engine* e, double* records);
+/* Device pointers of the resident state, for zero-copy consumers. */
+int gvp_engine_device_state(gvp_engine* e, double** mean, double** diag, double** off,
+                            double** covs, double** crosses);
+/* Launch counters: kernels launched by this engine since create. */
+int64_t gvp_engine_launches(gvp_engine* e);
+
+/* ------------------------------------------------ batched device kernels (tests) */
+/* All pointers device memory, plan-minor layout with nplans plans, async on
+ * `stream` (a cudaStream_t; NULL = legacy default stream). */
+int gvp_gbp_marginals_dev(int32_t nplans, int64_t nblocks, int32_t n, const double* diag,
+                          const double* off, double* covs, double* crosses, double* logdet,
+                          int32_t* status, int32_t* where, double* scratch, void* stream);
+/* scratch size in doubles for gvp_gbp_marginals_dev / gvp_select_step_dev */
+int64_t gvp_chain_scratch_doubles(int32_t nplans, int64_t nblocks, int32_t n, int32_t lanes);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GVP_B200_H */

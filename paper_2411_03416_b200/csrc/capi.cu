@@ -1,0 +1,500 @@
+// C ABI of libgvp_b200: drop-in host entry points and the batched engine.
+// See include/gvp_b200.h for the contract of every function.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <climits>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "gvp_internal.cuh"
+
+namespace gvp {
+
+static thread_local std::string g_err;
+void set_error(const std::string& msg) { g_err = msg; }
+int cuda_fail(cudaError_t err, const char* what) {
+  g_err = std::string("CUDA error ") + cudaGetErrorString(err) + " in " + what;
+  return err == cudaErrorNoDevice || err == cudaErrorInsufficientDriver ? GVP_ERR_NO_DEVICE
+                                                                        : GVP_ERR_CUDA;
+}
+
+// plan-minor views over a batch of B plans
+static View pview(const double* p, int64_t E, int64_t B) { return View{p, E * B, B, 1}; }
+static MutView pmview(double* p, int64_t E, int64_t B) { return MutView{p, E * B, B, 1}; }
+// a view shared by all plans (one copy)
+static View sview(const double* p, int64_t E) { return View{p, E, 1, 0}; }
+
+// --------------------------------------------------------------- device arena
+// grow-only device buffers reused across drop-in calls (one per slot)
+struct Arena {
+  std::vector<void*> ptr;
+  std::vector<size_t> cap;
+  template <class T>
+  int get(int slot, size_t count, T** out) {
+    if ((int)ptr.size() <= slot) {
+      ptr.resize(slot + 1, nullptr);
+      cap.resize(slot + 1, 0);
+    }
+    const size_t bytes = std::max<size_t>(count * sizeof(T), 16);
+    if (cap[slot] < bytes) {
+      if (ptr[slot]) cudaFree(ptr[slot]);
+      ptr[slot] = nullptr;
+      cap[slot] = 0;
+      GVP_CUDA(cudaMalloc(&ptr[slot], bytes));
+      cap[slot] = bytes;
+    }
+    *out = static_cast<T*>(ptr[slot]);
+    return GVP_OK;
+  }
+};
+
+struct Context {
+  std::mutex mu;
+  cudaStream_t stream = nullptr;
+  Arena arena;
+  Field field;
+  Rule rule;
+  int init() {
+    if (stream) return GVP_OK;
+    int ndev = 0;
+    cudaError_t e = cudaGetDeviceCount(&ndev);
+    if (e != cudaSuccess || ndev == 0) {
+      set_error("no CUDA device visible");
+      return GVP_ERR_NO_DEVICE;
+    }
+    GVP_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+    return GVP_OK;
+  }
+};
+static Context& ctx() {
+  static Context* c = new Context();  // leaked on purpose: no teardown-order issues at exit
+  return *c;
+}
+
+#define GVP_TRY(expr)          \
+  do {                         \
+    int _r = (expr);           \
+    if (_r != GVP_OK) return _r; \
+  } while (0)
+
+template <class T>
+static int h2d(T* dst, const T* src, size_t count, cudaStream_t s) {
+  if (count) GVP_CUDA(cudaMemcpyAsync(dst, src, count * sizeof(T), cudaMemcpyHostToDevice, s));
+  return GVP_OK;
+}
+template <class T>
+static int d2h(T* dst, const T* src, size_t count, cudaStream_t s) {
+  if (count) GVP_CUDA(cudaMemcpyAsync(dst, src, count * sizeof(T), cudaMemcpyDeviceToHost, s));
+  return GVP_OK;
+}
+
+static int check_n(int n) {
+  if (n < 1 || n > 8) {
+    set_error("block size n must be in 1..8");
+    return GVP_ERR_UNSUPPORTED;
+  }
+  return GVP_OK;
+}
+
+}  // namespace gvp
+
+using namespace gvp;
+
+// =================================================================== misc
+extern "C" const char* gvp_last_error(void) { return g_err.c_str(); }
+extern "C" const char* gvp_version(void) { return "gvp_b200 0.1.0 (sm_100a)"; }
+extern "C" int gvp_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+
+// =================================================================== drop-in host API
+extern "C" int gvp_factor_expectations(const double* means, const double* chols, int64_t nfac,
+                                       int32_t n, const double* points, const double* weights,
+                                       int64_t npts, const double* grid, int32_t grid_ndim,
+                                       const int64_t* grid_shape, const double* origin,
+                                       double cell_size, double radius_eps, double sigma_obs,
+                                       int32_t pos_dim, double* e0, double* e1, double* e2,
+                                       int64_t* oob) {
+  (void)pos_dim;  // like _kernels.pyx:142, the grid's ndim decides
+  Context& C = ctx();
+  std::lock_guard<std::mutex> lock(C.mu);
+  GVP_TRY(C.init());
+  GVP_TRY(check_n(n));
+  if (nfac < 0 || npts < 0) return set_error("negative size"), GVP_ERR_ARG;
+  cudaStream_t s = C.stream;
+  GVP_TRY(C.field.build(grid, grid_ndim, grid_shape, origin, cell_size, s));
+  GVP_TRY(C.rule.build(points, weights, npts, n, grid_ndim, s));
+  double *d_means, *d_chols, *d_e0, *d_e1, *d_e2;
+  unsigned long long* d_oob;
+  GVP_TRY(C.arena.get(0, nfac * n, &d_means));
+  GVP_TRY(C.arena.get(1, nfac * n * n, &d_chols));
+  GVP_TRY(C.arena.get(2, nfac, &d_e0));
+  GVP_TRY(C.arena.get(3, nfac * n, &d_e1));
+  GVP_TRY(C.arena.get(4, nfac * n * n, &d_e2));
+  GVP_TRY(C.arena.get(5, 1, &d_oob));
+  GVP_TRY(h2d(d_means, means, nfac * n, s));
+  GVP_TRY(h2d(d_chols, chols, nfac * n * n, s));
+  GVP_CUDA(cudaMemsetAsync(d_oob, 0, sizeof(unsigned long long), s));
+  GVP_TRY(launch_factor_moments(nfac, n, d_means, d_chols, C.rule.dev, C.field.dev, radius_eps,
+                                sigma_obs, d_e0, d_e1, d_e2, d_oob, s));
+  unsigned long long h_oob = 0;
+  GVP_TRY(d2h(e0, d_e0, nfac, s));
+  GVP_TRY(d2h(e1, d_e1, nfac * n, s));
+  GVP_TRY(d2h(e2, d_e2, nfac * n * n, s));
+  GVP_TRY(d2h(&h_oob, d_oob, 1, s));
+  GVP_CUDA(cudaStreamSynchronize(s));
+  *oob = (int64_t)h_oob;
+  return GVP_OK;
+}
+
+extern "C" int gvp_evaluate_factors(const double* mean, const double* covs, int64_t nblocks,
+                                    int32_t n, const double* points, const double* weights,
+                                    int64_t npts, const double* grid, int32_t grid_ndim,
+                                    const int64_t* grid_shape, const double* origin,
+                                    double cell_size, double radius_eps, double sigma_obs,
+                                    double* e_psi, double* g_mu, double* g_sigma, int64_t* oob,
+                                    int64_t* where) {
+  Context& C = ctx();
+  std::lock_guard<std::mutex> lock(C.mu);
+  GVP_TRY(C.init());
+  GVP_TRY(check_n(n));
+  if (n < grid_ndim) return set_error("state dim below grid dim"), GVP_ERR_ARG;
+  cudaStream_t s = C.stream;
+  const int64_t K = nblocks, F = std::max<int64_t>(K - 2, 0);
+  *oob = 0;
+  *where = -1;
+  if (F == 0) return GVP_OK;
+  GVP_TRY(C.field.build(grid, grid_ndim, grid_shape, origin, cell_size, s));
+  GVP_TRY(C.rule.build(points, weights, npts, n, grid_ndim, s));
+  double *d_mean, *d_covs, *d_epsi, *d_gmu, *d_gd;
+  unsigned long long* d_oob;
+  int* d_st;
+  GVP_TRY(C.arena.get(0, K * n, &d_mean));
+  GVP_TRY(C.arena.get(1, K * n * n, &d_covs));
+  GVP_TRY(C.arena.get(2, F, &d_epsi));
+  GVP_TRY(C.arena.get(3, K * n, &d_gmu));
+  GVP_TRY(C.arena.get(4, K * n * n, &d_gd));
+  GVP_TRY(C.arena.get(5, 1, &d_oob));
+  GVP_TRY(C.arena.get(6, 2, &d_st));
+  GVP_TRY(h2d(d_mean, mean, K * n, s));
+  GVP_TRY(h2d(d_covs, covs, K * n * n, s));
+  GVP_CUDA(cudaMemsetAsync(d_oob, 0, sizeof(unsigned long long), s));
+  const int init_st[2] = {0, INT_MAX};
+  GVP_TRY(h2d(d_st, init_st, 2, s));
+  FactorOut fo{pmview(d_epsi, 1, 1), pmview(d_gmu, n, 1), pmview(d_gd, n * n, 1), d_oob, d_st,
+               d_st + 1};
+  GVP_TRY(launch_factor_grads(1, K, n, pview(d_mean, n, 1), pview(d_covs, n * n, 1),
+                              C.rule.dev, C.field.dev, radius_eps, sigma_obs, fo, nullptr, s));
+  int st[2];
+  unsigned long long h_oob;
+  GVP_TRY(d2h(st, d_st, 2, s));
+  GVP_TRY(d2h(&h_oob, d_oob, 1, s));
+  GVP_TRY(d2h(e_psi, d_epsi, F, s));
+  GVP_TRY(d2h(g_mu, d_gmu + n, F * n, s));
+  GVP_TRY(d2h(g_sigma, d_gd + n * n, F * n * n, s));
+  GVP_CUDA(cudaStreamSynchronize(s));
+  *oob = (int64_t)h_oob;
+  if (st[0] != GVP_OK) {
+    *where = st[1];
+    set_error(st[0] == GVP_ERR_SQRT ? "covariance needs the eigendecomposition root"
+                                    : "non-finite expectation");
+    return st[0];
+  }
+  return GVP_OK;
+}
+
+namespace {
+struct ChainBufs {
+  double *diag, *off, *scr;
+  int* st;
+};
+int upload_bt(Context& C, const double* diag, const double* off, int64_t K, int n, ChainBufs& b,
+              int scr_lanes = 1) {
+  cudaStream_t s = C.stream;
+  GVP_TRY(C.arena.get(10, K * n * n, &b.diag));
+  GVP_TRY(C.arena.get(11, std::max<int64_t>(K - 1, 1) * n * n, &b.off));
+  GVP_TRY(C.arena.get(12, (size_t)chain_scratch_doubles(1, K, n, scr_lanes), &b.scr));
+  GVP_TRY(C.arena.get(13, 4, &b.st));
+  GVP_TRY(h2d(b.diag, diag, K * n * n, s));
+  GVP_TRY(h2d(b.off, off, (K - 1) * n * n, s));
+  return GVP_OK;
+}
+int fetch_status(Context& C, const int* d_st, int64_t* where) {
+  int st[2];
+  GVP_TRY(d2h(st, d_st, 2, C.stream));
+  GVP_CUDA(cudaStreamSynchronize(C.stream));
+  if (where) *where = st[1];
+  return st[0];
+}
+}  // namespace
+
+extern "C" int gvp_gbp_marginals(const double* diag, const double* off, int64_t nblocks,
+                                 int32_t n, double* covs, double* crosses, int64_t* where) {
+  Context& C = ctx();
+  std::lock_guard<std::mutex> lock(C.mu);
+  GVP_TRY(C.init());
+  GVP_TRY(check_n(n));
+  if (nblocks < 1) return set_error("need at least one block"), GVP_ERR_ARG;
+  const int64_t K = nblocks;
+  ChainBufs b;
+  GVP_TRY(upload_bt(C, diag, off, K, n, b));
+  double *d_cov, *d_cr;
+  GVP_TRY(C.arena.get(14, K * n * n, &d_cov));
+  GVP_TRY(C.arena.get(15, std::max<int64_t>(K - 1, 1) * n * n, &d_cr));
+  GVP_TRY(launch_marginals(1, K, n, pview(b.diag, n * n, 1), pview(b.off, n * n, 1),
+                           pmview(d_cov, n * n, 1), pmview(d_cr, n * n, 1), nullptr, b.st,
+                           b.st + 1, b.scr, nullptr, C.stream));
+  const int st = fetch_status(C, b.st, where);
+  if (st != GVP_OK) {
+    set_error("belief precision at knot " + std::to_string(*where) + " is not positive definite");
+    return st;
+  }
+  GVP_TRY(d2h(covs, d_cov, K * n * n, C.stream));
+  GVP_TRY(d2h(crosses, d_cr, (K - 1) * n * n, C.stream));
+  GVP_CUDA(cudaStreamSynchronize(C.stream));
+  return GVP_OK;
+}
+
+extern "C" int gvp_gbp_mean_solve(const double* diag, const double* off, const double* info,
+                                  int64_t nblocks, int32_t n, double* out, int64_t* where) {
+  Context& C = ctx();
+  std::lock_guard<std::mutex> lock(C.mu);
+  GVP_TRY(C.init());
+  GVP_TRY(check_n(n));
+  if (nblocks < 1) return set_error("need at least one block"), GVP_ERR_ARG;
+  const int64_t K = nblocks;
+  ChainBufs b;
+  GVP_TRY(upload_bt(C, diag, off, K, n, b));
+  double *d_eta, *d_out;
+  GVP_TRY(C.arena.get(14, K * n, &d_eta));
+  GVP_TRY(C.arena.get(15, K * n, &d_out));
+  GVP_TRY(h2d(d_eta, info, K * n, C.stream));
+  GVP_TRY(launch_mean_solve(1, K, n, pview(b.diag, n * n, 1), pview(b.off, n * n, 1),
+                            pview(d_eta, n, 1), pmview(d_out, n, 1), b.st, b.st + 1, b.scr,
+                            C.stream));
+  const int st = fetch_status(C, b.st, where);
+  if (st != GVP_OK) {
+    set_error("pivot block " + std::to_string(*where) + " is not positive definite");
+    return st;
+  }
+  GVP_TRY(d2h(out, d_out, K * n, C.stream));
+  GVP_CUDA(cudaStreamSynchronize(C.stream));
+  return GVP_OK;
+}
+
+extern "C" int gvp_logdet_block_tridiag(const double* diag, const double* off, int64_t nblocks,
+                                        int32_t n, double* out, int64_t* where) {
+  Context& C = ctx();
+  std::lock_guard<std::mutex> lock(C.mu);
+  GVP_TRY(C.init());
+  GVP_TRY(check_n(n));
+  if (nblocks < 1) return set_error("need at least one block"), GVP_ERR_ARG;
+  const int64_t K = nblocks;
+  ChainBufs b;
+  GVP_TRY(upload_bt(C, diag, off, K, n, b));
+  double* d_out;
+  GVP_TRY(C.arena.get(14, 1, &d_out));
+  GVP_TRY(launch_logdet_fwd(1, K, n, pview(b.diag, n * n, 1), pview(b.off, n * n, 1), d_out, b.st,
+                            b.st + 1, b.scr, C.stream));
+  const int st = fetch_status(C, b.st, where);
+  if (st != GVP_OK) {
+    set_error("pivot block " + std::to_string(*where) + " is not positive definite");
+    return st;
+  }
+  GVP_TRY(d2h(out, d_out, 1, C.stream));
+  GVP_CUDA(cudaStreamSynchronize(C.stream));
+  return GVP_OK;
+}
+
+namespace {
+// uploads of one plan's step problem; returns device StepProblem
+struct StepBufs {
+  double *mean, *diag, *off, *kdiag, *koff, *info, *gmu, *gdiag, *goff, *scr;
+  double *omean, *odiag, *ooff, *covs, *crosses, *scal;  // scal: beta, kl, ld_next, shift, temp, ld_cur, beta_fixed
+  double* plog;
+  int *st, *np;
+};
+int upload_step(Context& C, const double* mean, const double* diag, const double* off,
+                const double* kdiag, const double* koff, const double* info, const double* g_mu,
+                const double* gdiag, const double* goff, int64_t K, int n, int max_probes,
+                StepBufs& b, StepProblem& pb) {
+  cudaStream_t s = C.stream;
+  const int64_t B2 = (int64_t)n * n, K1 = std::max<int64_t>(K - 1, 1);
+  GVP_TRY(C.arena.get(20, K * n, &b.mean));
+  GVP_TRY(C.arena.get(21, K * B2, &b.diag));
+  GVP_TRY(C.arena.get(22, K1 * B2, &b.off));
+  GVP_TRY(C.arena.get(23, K * B2, &b.kdiag));
+  GVP_TRY(C.arena.get(24, K1 * B2, &b.koff));
+  GVP_TRY(C.arena.get(25, K * n, &b.info));
+  GVP_TRY(C.arena.get(26, K * n, &b.gmu));
+  GVP_TRY(C.arena.get(27, K * B2, &b.gdiag));
+  GVP_TRY(C.arena.get(28, K1 * B2, &b.goff));
+  GVP_TRY(C.arena.get(29, (size_t)chain_scratch_doubles(1, K, n, 1), &b.scr));
+  GVP_TRY(C.arena.get(30, K * n, &b.omean));
+  GVP_TRY(C.arena.get(31, K * B2, &b.odiag));
+  GVP_TRY(C.arena.get(32, K1 * B2, &b.ooff));
+  GVP_TRY(C.arena.get(33, K * B2, &b.covs));
+  GVP_TRY(C.arena.get(34, K1 * B2, &b.crosses));
+  GVP_TRY(C.arena.get(35, 16, &b.scal));
+  GVP_TRY(C.arena.get(36, std::max(max_probes, 1) * 3, &b.plog));
+  GVP_TRY(C.arena.get(37, 4, &b.st));
+  b.np = b.st + 2;
+  GVP_TRY(h2d(b.mean, mean, K * n, s));
+  GVP_TRY(h2d(b.diag, diag, K * B2, s));
+  GVP_TRY(h2d(b.off, off, (K - 1) * B2, s));
+  GVP_TRY(h2d(b.kdiag, kdiag, K * B2, s));
+  GVP_TRY(h2d(b.koff, koff, (K - 1) * B2, s));
+  GVP_TRY(h2d(b.info, info, K * n, s));
+  GVP_TRY(h2d(b.gmu, g_mu, K * n, s));
+  GVP_TRY(h2d(b.gdiag, gdiag, K * B2, s));
+  if (goff) GVP_TRY(h2d(b.goff, goff, (K - 1) * B2, s));
+  pb = StepProblem{pview(b.mean, n, 1),  pview(b.diag, B2, 1), pview(b.off, B2, 1),
+                   pview(b.kdiag, B2, 1), pview(b.koff, B2, 1), pview(b.info, n, 1),
+                   pview(b.gmu, n, 1),   pview(b.gdiag, B2, 1), pview(b.goff, B2, 1),
+                   goff != nullptr,      pview(b.mean, n, 1),   false};
+  return GVP_OK;
+}
+}  // namespace
+
+extern "C" int gvp_proximal_update(const double* mean, const double* diag, const double* off,
+                                   const double* kdiag, const double* koff, const double* info,
+                                   const double* g_mu, const double* gdiag, const double* goff,
+                                   int64_t nblocks, int32_t n, double beta, double temp,
+                                   double* out_mean, double* out_diag, double* out_off,
+                                   int64_t* where) {
+  if (!(beta > 0)) return set_error("beta must be positive"), GVP_ERR_ARG;
+  Context& C = ctx();
+  std::lock_guard<std::mutex> lock(C.mu);
+  GVP_TRY(C.init());
+  GVP_TRY(check_n(n));
+  const int64_t K = nblocks, B2 = (int64_t)n * n;
+  StepBufs b;
+  StepProblem pb;
+  GVP_TRY(upload_step(C, mean, diag, off, kdiag, koff, info, g_mu, gdiag, goff, K, n, 0, b, pb));
+  const double sc[2] = {temp, beta};
+  GVP_TRY(h2d(b.scal + 4, sc, 2, C.stream));
+  StepParams pr{b.scal + 4, nullptr, 0, 0, 0, 1, true, b.scal + 5};
+  StepOut out{pmview(b.omean, n, 1), pmview(b.odiag, B2, 1), pmview(b.ooff, B2, 1),
+              pmview(b.covs, B2, 1), pmview(b.crosses, B2, 1), nullptr, nullptr, nullptr,
+              nullptr, nullptr, nullptr, 0, nullptr, b.st, b.st + 1};
+  GVP_TRY(launch_select_step(1, K, n, pb, pr, out, b.scr, nullptr, C.stream));
+  const int st = fetch_status(C, b.st, where);
+  if (st != GVP_OK) {
+    set_error("pivot block " + std::to_string(*where) + " is not positive definite");
+    return st;
+  }
+  GVP_TRY(d2h(out_mean, b.omean, K * n, C.stream));
+  GVP_TRY(d2h(out_diag, b.odiag, K * B2, C.stream));
+  GVP_TRY(d2h(out_off, b.ooff, (K - 1) * B2, C.stream));
+  GVP_CUDA(cudaStreamSynchronize(C.stream));
+  return GVP_OK;
+}
+
+extern "C" int gvp_select_step_size(const double* mean, const double* diag, const double* off,
+                                    const double* kdiag, const double* koff, const double* info,
+                                    const double* g_mu, const double* gdiag, const double* goff,
+                                    int64_t nblocks, int32_t n, double temp, double kl_bound,
+                                    double beta_min, double beta_max, double* beta, double* kl,
+                                    double* out_mean, double* out_diag, double* out_off,
+                                    double* covs, double* crosses, double* probe_log,
+                                    int32_t max_probes, int32_t* nprobes, int64_t* where) {
+  Context& C = ctx();
+  std::lock_guard<std::mutex> lock(C.mu);
+  GVP_TRY(C.init());
+  GVP_TRY(check_n(n));
+  const int64_t K = nblocks, B2 = (int64_t)n * n;
+  StepBufs b;
+  StepProblem pb;
+  GVP_TRY(upload_step(C, mean, diag, off, kdiag, koff, info, g_mu, gdiag, goff, K, n,
+                      probe_log ? max_probes : 0, b, pb));
+  cudaStream_t s = C.stream;
+  // log det of the current precision, from the same backward Schur pivots the
+  // probes use for the candidate (consistent KL)
+  GVP_TRY(launch_marginals(1, K, n, pb.diag, pb.off, pmview(b.covs, B2, 1),
+                           pmview(b.crosses, B2, 1), b.scal + 5, b.st, b.st + 1, b.scr, nullptr,
+                           s));
+  int64_t w0 = -1;
+  int st = fetch_status(C, b.st, &w0);
+  if (st != GVP_OK) {
+    if (where) *where = w0;
+    set_error("current precision is not positive definite at knot " + std::to_string(w0));
+    return st;
+  }
+  GVP_TRY(h2d(b.scal + 4, &temp, 1, s));
+  StepParams pr{b.scal + 4, b.scal + 5, kl_bound, beta_min, beta_max, 1, false, nullptr};
+  StepOut out{pmview(b.omean, n, 1),
+              pmview(b.odiag, B2, 1),
+              pmview(b.ooff, B2, 1),
+              pmview(b.covs, B2, 1),
+              pmview(b.crosses, B2, 1),
+              b.scal + 0,
+              b.scal + 1,
+              b.scal + 2,
+              b.scal + 3,
+              nullptr,
+              probe_log ? b.plog : nullptr,
+              max_probes,
+              b.np,
+              b.st,
+              b.st + 1};
+  GVP_TRY(launch_select_step(1, K, n, pb, pr, out, b.scr, nullptr, s));
+  int stw[3];
+  GVP_TRY(d2h(stw, b.st, 3, s));
+  GVP_CUDA(cudaStreamSynchronize(s));
+  if (nprobes) *nprobes = stw[2];
+  if (probe_log && stw[2] > 0)
+    GVP_TRY(d2h(probe_log, b.plog, (size_t)std::min(stw[2], max_probes) * 3, s));
+  if (stw[0] != GVP_OK) {
+    if (where) *where = stw[1];
+    GVP_CUDA(cudaStreamSynchronize(s));
+    if (stw[0] == GVP_ERR_NO_FEASIBLE_STEP) {
+      char msg[160];
+      std::snprintf(msg, sizeof msg, "no feasible step size at beta_min=%g (KL bound %g)", beta_min,
+                    kl_bound);
+      set_error(msg);
+    } else {
+      set_error("pivot block " + std::to_string(stw[1] & ~GVP_WHERE_MEAN_SOLVE_BIAS) +
+                " is not positive definite");
+    }
+    return stw[0];
+  }
+  double sc[2];
+  GVP_TRY(d2h(sc, b.scal, 2, s));
+  GVP_TRY(d2h(out_mean, b.omean, K * n, s));
+  GVP_TRY(d2h(out_diag, b.odiag, K * B2, s));
+  GVP_TRY(d2h(out_off, b.ooff, (K - 1) * B2, s));
+  GVP_TRY(d2h(covs, b.covs, K * B2, s));
+  GVP_TRY(d2h(crosses, b.crosses, (K - 1) * B2, s));
+  GVP_CUDA(cudaStreamSynchronize(s));
+  *beta = sc[0];
+  *kl = sc[1];
+  if (where) *where = -1;
+  return GVP_OK;
+}
+
+// =================================================================== batched device kernels
+extern "C" int64_t gvp_chain_scratch_doubles(int32_t nplans, int64_t nblocks, int32_t n,
+                                             int32_t lanes) {
+  return chain_scratch_doubles(nplans, nblocks, n, lanes);
+}
+
+extern "C" int gvp_gbp_marginals_dev(int32_t nplans, int64_t nblocks, int32_t n,
+                                     const double* diag, const double* off, double* covs,
+                                     double* crosses, double* logdet, int32_t* status,
+                                     int32_t* where, double* scratch, void* stream) {
+  GVP_TRY(check_n(n));
+  const int64_t B2 = (int64_t)n * n;
+  return launch_marginals(nplans, nblocks, n, pview(diag, B2, nplans), pview(off, B2, nplans),
+                          pmview(covs, B2, nplans), pmview(crosses, B2, nplans), logdet, status,
+                          where, scratch, nullptr, (cudaStream_t)stream);
+}

@@ -1,0 +1,474 @@
+// Batched P-GVIMP engine: Algorithm 1 (optimizer.py:299-401) for B
+// independent plans, all state resident in HBM, no host round trip inside an
+// iteration. One iteration = 3 kernels on the engine stream:
+//
+//   select_step_kernel   bisection + in-place commit of (mu, Lambda) and the
+//                        accepted marginals, KL, log det, prior cost
+//   factor_grads_kernel  collision factors at the accepted state (the cache
+//                        the next iteration's step uses, optimizer.py:354-360)
+//   control_kernel       cost_breakdown (optimizer.py:238-277), the record,
+//                        convergence and temperature switch (optimizer.py:381-398)
+//
+// The iteration is captured once into a CUDA graph and replayed.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <climits>
+#include <cmath>
+#include <vector>
+
+#include "gvp_internal.cuh"
+
+using namespace gvp;
+
+namespace {
+constexpr double kLog2Pi = 1.8378770664093453;  // log(2 pi), optimizer.py:38
+
+struct PlanState {
+  // per-plan scalars (device)
+  double *temp, *logdet, *beta, *kl, *shift, *prior_cost, *prev_total, *prev_temp, *total;
+  int *active, *status, *where, *converged, *iters, *switch_it, *switched, *fstatus, *fwhere;
+  unsigned long long* oob;
+  int* nactive;
+};
+
+__global__ void init_plans_kernel(int B, PlanState ps, double temp_low) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= B) return;
+  ps.temp[b] = temp_low;
+  ps.prev_total[b] = NAN;  // NaN encodes python None
+  ps.prev_temp[b] = NAN;
+  ps.active[b] = 1;
+  ps.status[b] = 0;
+  ps.where[b] = -1;
+  ps.converged[b] = 0;
+  ps.iters[b] = 0;
+  ps.switch_it[b] = -1;
+  ps.switched[b] = 0;
+  ps.fstatus[b] = 0;
+  ps.fwhere[b] = INT_MAX;
+  ps.oob[b] = 0;
+}
+
+// initial_state (optimizer.py:280-296): Lambda_0 = K^{-1} / init_cov_scale
+__global__ void init_prec_kernel(int64_t count_diag, int64_t count_off, const double* kd,
+                                 const double* ko, int64_t ksp_diag, int64_t ksp_off, double* d,
+                                 double* o, int B, double inv_scale) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  // count_* = number of (knot, entry) pairs; plans interleaved
+  if (t < count_diag * B) {
+    const int64_t b = t % B, e = t / B;
+    d[t] = kd[ksp_diag ? t : e] * inv_scale;
+  } else if (t < (count_diag + count_off) * B) {
+    const int64_t u = t - count_diag * B;
+    const int64_t b = u % B, e = u / B;
+    (void)b;
+    o[u] = ko[ksp_off ? u : e] * inv_scale;
+  }
+}
+
+__global__ void control_kernel(int B, int64_t F, int n64dim, const double* __restrict__ epsi,
+                               PlanState ps, double* __restrict__ records, int max_iters,
+                               double temp_high, double tol_mean, double tol_cost, double ctol) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= B) return;
+  if (!ps.active[b]) return;
+  if (ps.status[b] != 0 || ps.fstatus[b] != 0) {  // a kernel failed this plan
+    if (ps.status[b] == 0) {
+      ps.status[b] = ps.fstatus[b];
+      ps.where[b] = ps.fwhere[b];
+    }
+    ps.active[b] = 0;
+    return;
+  }
+  const int it = ps.iters[b] + 1;
+  double coll = 0.0;  // sum(f.e_psi), ascending factor order (optimizer.py:274)
+  for (int64_t f = 0; f < F; ++f) coll += epsi[f * B + b];
+  const double temp = ps.temp[b];
+  const double dim = (double)n64dim;
+  const double entropy = 0.5 * (dim * (kLog2Pi + 1.0) - ps.logdet[b]);  // optimizer.py:234-235
+  const double ent_cost = -temp * entropy;
+  const double prior = ps.prior_cost[b];
+  const double total = prior + coll + ent_cost;
+  const double shift = ps.shift[b];
+  double* rec = records + ((int64_t)(it - 1) * B + b) * GVP_NREC;
+  rec[0] = ps.beta[b];
+  rec[1] = temp;
+  rec[2] = prior;
+  rec[3] = coll;
+  rec[4] = ent_cost;
+  rec[5] = total;
+  rec[6] = ps.kl[b];
+  rec[7] = shift;
+  ps.iters[b] = it;
+  ps.total[b] = total;
+  const double prev_temp = ps.prev_temp[b], prev_total = ps.prev_total[b];
+  const bool same_temp = !isnan(prev_temp) && prev_temp == temp;
+  const double change = !isnan(prev_total) ? fabs(total - prev_total) : INFINITY;
+  if (same_temp && shift < tol_mean && change < tol_cost) {
+    ps.converged[b] = 1;
+    ps.active[b] = 0;
+    return;
+  }
+  ps.prev_total[b] = (same_temp || isnan(prev_temp)) ? total : NAN;
+  ps.prev_temp[b] = temp;
+  if (!ps.switched[b] && coll < ctol && temp != temp_high) {
+    ps.temp[b] = temp_high;
+    ps.switched[b] = 1;
+    ps.switch_it[b] = it;
+    ps.prev_total[b] = NAN;
+  }
+  if (it >= max_iters) {
+    ps.active[b] = 0;
+    return;
+  }
+  atomicAdd(ps.nactive, 1);
+}
+
+__global__ void fill_kernel(double* p, int64_t count, double v) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < count) p[t] = v;
+}
+
+__global__ void count_active_kernel(int B, const int* active, int* out) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b < B && active[b]) atomicAdd(out, 1);
+}
+}  // namespace
+
+struct gvp_engine {
+  int B = 0;
+  int64_t K = 0;
+  int n = 0;
+  bool shared_prior = false;
+  cudaStream_t stream = nullptr;
+  Field field;
+  Rule rule;
+  double radius_eps = 0, sigma_obs = 0;
+  gvp_plan_config cfg{};
+  // resident state (plan-minor)
+  double *mean = nullptr, *diag = nullptr, *off = nullptr, *covs = nullptr, *crosses = nullptr;
+  double *kdiag = nullptr, *koff = nullptr, *info = nullptr, *pmean = nullptr;
+  double *gmu = nullptr, *gdiag = nullptr, *epsi = nullptr, *scratch = nullptr;
+  double* records = nullptr;
+  double* scal = nullptr;
+  int* ints = nullptr;
+  unsigned long long* oob = nullptr;
+  PlanState ps{};
+  cudaGraphExec_t graph = nullptr;
+  int iters_launched = 0;
+  int64_t launches = 0;
+  std::vector<void*> allocs;
+
+  template <class T>
+  int alloc(T** p, size_t count) {
+    void* q = nullptr;
+    GVP_CUDA(cudaMalloc(&q, std::max<size_t>(count, 1) * sizeof(T)));
+    allocs.push_back(q);
+    *p = static_cast<T*>(q);
+    return GVP_OK;
+  }
+  ~gvp_engine() {
+    if (graph) cudaGraphExecDestroy(graph);
+    for (void* p : allocs) cudaFree(p);
+    if (stream) cudaStreamDestroy(stream);
+  }
+
+  int64_t B2() const { return (int64_t)n * n; }
+  View v(const double* p, int64_t E) const { return View{p, E * B, B, 1}; }
+  MutView mv(double* p, int64_t E) const { return MutView{p, E * B, B, 1}; }
+  View kv(const double* p) const {
+    return shared_prior ? View{p, B2(), 1, 0} : View{p, B2() * B, B, 1};
+  }
+
+  int factors() {
+    FactorOut fo{mv(epsi, 1), mv(gmu, n), mv(gdiag, B2()), ps.oob, ps.fstatus, ps.fwhere};
+    launches += (K > 2);
+    return launch_factor_grads(B, K, n, v(mean, n), v(covs, B2()), rule.dev, field.dev,
+                               radius_eps, sigma_obs, fo, ps.active, stream);
+  }
+
+  int iteration_body() {
+    StepProblem pb{v(mean, n),  v(diag, B2()), v(off, B2()), kv(kdiag),   kv(koff),
+                   v(info, n),  v(gmu, n),     v(gdiag, B2()), v(gdiag, B2()), false,
+                   v(pmean, n), true};
+    StepParams pr{ps.temp, ps.logdet, cfg.kl_bound, cfg.beta_min, cfg.beta_max,
+                  std::max(1, cfg.spec_lanes), false, nullptr};
+    StepOut out{mv(mean, n),     mv(diag, B2()), mv(off, B2()), mv(covs, B2()),
+                mv(crosses, B2()), ps.beta,      ps.kl,         ps.logdet,
+                ps.shift,        ps.prior_cost,  nullptr,       0,
+                nullptr,         ps.status,      ps.where};
+    int r = launch_select_step(B, K, n, pb, pr, out, scratch, ps.active, stream);
+    if (r) return r;
+    ++launches;
+    r = factors();
+    if (r) return r;
+    const double ctol = cfg.collision_tol >= 0 ? cfg.collision_tol : 1e-4 * (double)(K - 1);
+    control_kernel<<<(B + 127) / 128, 128, 0, stream>>>(
+        B, std::max<int64_t>(K - 2, 0), (int)(K * n), epsi, ps, records, cfg.max_iters,
+        cfg.temp_high, cfg.tol_mean, cfg.tol_cost, ctol);
+    ++launches;
+    GVP_CUDA(cudaGetLastError());
+    return GVP_OK;
+  }
+};
+
+extern "C" int gvp_engine_create(gvp_engine** out, int32_t nplans, int64_t nknots, int32_t n,
+                                 int32_t shared_prior, const double* grid, int32_t grid_ndim,
+                                 const int64_t* grid_shape, const double* origin,
+                                 double cell_size, double radius_eps, double sigma_obs,
+                                 const double* points, const double* weights, int64_t npts,
+                                 const gvp_plan_config* cfg) {
+  *out = nullptr;
+  if (nplans < 1 || nknots < 2 || n < 1 || n > 8 || !cfg) {
+    set_error("bad engine dimensions");
+    return GVP_ERR_ARG;
+  }
+  if (cfg->max_iters < 1 || !(cfg->kl_bound > 0) || !(0 < cfg->beta_min && cfg->beta_min < cfg->beta_max)) {
+    set_error("invalid optimizer config (optimizer.py:89-99)");
+    return GVP_ERR_ARG;
+  }
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+    cudaGetLastError();
+    set_error("no CUDA device visible");
+    return GVP_ERR_NO_DEVICE;
+  }
+  auto* e = new gvp_engine();
+  e->B = nplans;
+  e->K = nknots;
+  e->n = n;
+  e->shared_prior = shared_prior != 0;
+  e->cfg = *cfg;
+  e->radius_eps = radius_eps;
+  e->sigma_obs = sigma_obs;
+  int r = GVP_OK;
+  auto fail = [&](int code) {
+    delete e;
+    return code;
+  };
+  if (cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking) != cudaSuccess)
+    return fail(cuda_fail(cudaGetLastError(), "cudaStreamCreate"));
+  if ((r = e->field.build(grid, grid_ndim, grid_shape, origin, cell_size, e->stream))) return fail(r);
+  if (grid_ndim > n) return set_error("grid dim exceeds state dim"), fail(GVP_ERR_ARG);
+  if ((r = e->rule.build(points, weights, npts, n, grid_ndim, e->stream))) return fail(r);
+  const int64_t B = nplans, K = nknots, B2 = (int64_t)n * n;
+  const int64_t kb = e->shared_prior ? 1 : B;
+  if ((r = e->alloc(&e->mean, K * n * B)) || (r = e->alloc(&e->diag, K * B2 * B)) ||
+      (r = e->alloc(&e->off, (K - 1) * B2 * B)) || (r = e->alloc(&e->covs, K * B2 * B)) ||
+      (r = e->alloc(&e->crosses, (K - 1) * B2 * B)) || (r = e->alloc(&e->kdiag, K * B2 * kb)) ||
+      (r = e->alloc(&e->koff, (K - 1) * B2 * kb)) || (r = e->alloc(&e->info, K * n * B)) ||
+      (r = e->alloc(&e->pmean, K * n * B)) || (r = e->alloc(&e->gmu, K * n * B)) ||
+      (r = e->alloc(&e->gdiag, K * B2 * B)) ||
+      (r = e->alloc(&e->epsi, std::max<int64_t>(K - 2, 1) * B)) ||
+      (r = e->alloc(&e->scratch, (size_t)chain_scratch_doubles(nplans, K, n, std::max(1, cfg->spec_lanes)))) ||
+      (r = e->alloc(&e->records, (size_t)cfg->max_iters * B * GVP_NREC)) ||
+      (r = e->alloc(&e->scal, 9 * B)) || (r = e->alloc(&e->ints, 10 * B + 1)) ||
+      (r = e->alloc(&e->oob, B)))
+    return fail(r);
+  PlanState& ps = e->ps;
+  double* s = e->scal;
+  ps.temp = s; ps.logdet = s + B; ps.beta = s + 2 * B; ps.kl = s + 3 * B; ps.shift = s + 4 * B;
+  ps.prior_cost = s + 5 * B; ps.prev_total = s + 6 * B; ps.prev_temp = s + 7 * B; ps.total = s + 8 * B;
+  int* q = e->ints;
+  ps.active = q; ps.status = q + B; ps.where = q + 2 * B; ps.converged = q + 3 * B;
+  ps.iters = q + 4 * B; ps.switch_it = q + 5 * B; ps.switched = q + 6 * B; ps.fstatus = q + 7 * B;
+  ps.fwhere = q + 8 * B; ps.nactive = q + 10 * B;
+  ps.oob = e->oob;
+  *out = e;
+  return GVP_OK;
+}
+
+extern "C" void gvp_engine_destroy(gvp_engine* e) { delete e; }
+
+static int engine_reset(gvp_engine* e) {
+  const int64_t B = e->B, K = e->K, B2 = e->B2();
+  cudaStream_t s = e->stream;
+  // knots 0 and K-1 carry no factor: their gradient blocks stay zero
+  GVP_CUDA(cudaMemsetAsync(e->gmu, 0, K * e->n * B * sizeof(double), s));
+  GVP_CUDA(cudaMemsetAsync(e->gdiag, 0, K * B2 * B * sizeof(double), s));
+  {
+    const int64_t cnt = (int64_t)e->cfg.max_iters * B * GVP_NREC;
+    fill_kernel<<<(unsigned)((cnt + 255) / 256), 256, 0, s>>>(e->records, cnt, NAN);
+  }
+  init_plans_kernel<<<(unsigned)((B + 127) / 128), 128, 0, s>>>((int)B, e->ps, e->cfg.temp_low);
+  const int64_t cd = K * B2, co = (K - 1) * B2;
+  const int64_t tot = (cd + co) * B;
+  init_prec_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(
+      cd, co, e->kdiag, e->koff, e->shared_prior ? 0 : 1, e->shared_prior ? 0 : 1, e->diag,
+      e->off, (int)B, 1.0 / e->cfg.init_cov_scale);
+  GVP_CUDA(cudaGetLastError());
+  // result.marginals = gbp_marginals(cur.prec) (optimizer.py:329) + log det
+  int r = launch_marginals((int)B, K, e->n, e->v(e->diag, B2), e->v(e->off, B2),
+                           e->mv(e->covs, B2), e->mv(e->crosses, B2), e->ps.logdet, e->ps.status,
+                           e->ps.where, e->scratch, nullptr, s);
+  if (r) return r;
+  // first factor sweep (optimizer.py:338-344)
+  if ((r = e->factors())) return r;
+  e->launches += 3;
+  e->iters_launched = 0;
+  if (e->graph) {
+    cudaGraphExecDestroy(e->graph);
+    e->graph = nullptr;
+  }
+  return GVP_OK;
+}
+
+extern "C" int gvp_engine_load(gvp_engine* e, const double* kdiag, const double* koff,
+                               const double* info, const double* prior_mean,
+                               const double* init_mean) {
+  const int64_t B = e->B, K = e->K, B2 = e->B2(), kb = e->shared_prior ? 1 : B;
+  cudaStream_t s = e->stream;
+  GVP_CUDA(cudaMemcpyAsync(e->kdiag, kdiag, K * B2 * kb * sizeof(double), cudaMemcpyHostToDevice, s));
+  GVP_CUDA(cudaMemcpyAsync(e->koff, koff, (K - 1) * B2 * kb * sizeof(double), cudaMemcpyHostToDevice, s));
+  GVP_CUDA(cudaMemcpyAsync(e->info, info, K * e->n * B * sizeof(double), cudaMemcpyHostToDevice, s));
+  GVP_CUDA(cudaMemcpyAsync(e->pmean, prior_mean, K * e->n * B * sizeof(double), cudaMemcpyHostToDevice, s));
+  GVP_CUDA(cudaMemcpyAsync(e->mean, init_mean, K * e->n * B * sizeof(double), cudaMemcpyHostToDevice, s));
+  return engine_reset(e);
+}
+
+extern "C" int gvp_engine_load_dev(gvp_engine* e, const double* kdiag, const double* koff,
+                                   const double* info, const double* prior_mean,
+                                   const double* init_mean) {
+  const int64_t B = e->B, K = e->K, B2 = e->B2(), kb = e->shared_prior ? 1 : B;
+  cudaStream_t s = e->stream;
+  GVP_CUDA(cudaMemcpyAsync(e->kdiag, kdiag, K * B2 * kb * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  GVP_CUDA(cudaMemcpyAsync(e->koff, koff, (K - 1) * B2 * kb * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  GVP_CUDA(cudaMemcpyAsync(e->info, info, K * e->n * B * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  GVP_CUDA(cudaMemcpyAsync(e->pmean, prior_mean, K * e->n * B * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  GVP_CUDA(cudaMemcpyAsync(e->mean, init_mean, K * e->n * B * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  return engine_reset(e);
+}
+
+extern "C" int gvp_engine_step(gvp_engine* e, int32_t iters, int32_t sync) {
+  cudaStream_t s = e->stream;
+  for (int k = 0; k < iters && e->iters_launched < e->cfg.max_iters; ++k) {
+    if (!e->graph) {
+      cudaGraph_t g;
+      GVP_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+      const int64_t before = e->launches;
+      int r = e->iteration_body();
+      cudaError_t ce = cudaStreamEndCapture(s, &g);
+      if (r) return r;
+      if (ce != cudaSuccess) return cuda_fail(ce, "cudaStreamEndCapture");
+      GVP_CUDA(cudaGraphInstantiate(&e->graph, g, 0));
+      cudaGraphDestroy(g);
+      e->launches = before;  // counted per replay below
+    }
+    GVP_CUDA(cudaGraphLaunch(e->graph, s));
+    e->launches += 2 + (e->K > 2);
+    ++e->iters_launched;
+  }
+  if (sync) GVP_CUDA(cudaStreamSynchronize(s));
+  return GVP_OK;
+}
+
+// Same iterations as gvp_engine_step, launched kernel by kernel (no graph)
+// with CUDA events around each kernel on the engine stream; accumulates the
+// per-kernel device time (ms) over the iterations into ms[0..2] =
+// {select_step, factor_grads, control}.
+extern "C" int gvp_engine_step_profiled(gvp_engine* e, int32_t iters, double* ms) {
+  cudaStream_t s = e->stream;
+  cudaEvent_t ev[4];
+  for (auto& x : ev) GVP_CUDA(cudaEventCreate(&x));
+  double acc[3] = {0, 0, 0};
+  for (int k = 0; k < iters && e->iters_launched < e->cfg.max_iters; ++k) {
+    StepProblem pb{e->v(e->mean, e->n), e->v(e->diag, e->B2()), e->v(e->off, e->B2()),
+                   e->kv(e->kdiag),     e->kv(e->koff),         e->v(e->info, e->n),
+                   e->v(e->gmu, e->n),  e->v(e->gdiag, e->B2()), e->v(e->gdiag, e->B2()),
+                   false,               e->v(e->pmean, e->n),   true};
+    StepParams pr{e->ps.temp, e->ps.logdet, e->cfg.kl_bound, e->cfg.beta_min, e->cfg.beta_max,
+                  std::max(1, e->cfg.spec_lanes), false, nullptr};
+    StepOut out{e->mv(e->mean, e->n),      e->mv(e->diag, e->B2()), e->mv(e->off, e->B2()),
+                e->mv(e->covs, e->B2()),   e->mv(e->crosses, e->B2()), e->ps.beta,
+                e->ps.kl,                  e->ps.logdet,            e->ps.shift,
+                e->ps.prior_cost,          nullptr,                 0,
+                nullptr,                   e->ps.status,            e->ps.where};
+    GVP_CUDA(cudaEventRecord(ev[0], s));
+    int r = launch_select_step(e->B, e->K, e->n, pb, pr, out, e->scratch, e->ps.active, s);
+    if (r) return r;
+    GVP_CUDA(cudaEventRecord(ev[1], s));
+    if ((r = e->factors())) return r;
+    GVP_CUDA(cudaEventRecord(ev[2], s));
+    const double ctol = e->cfg.collision_tol >= 0 ? e->cfg.collision_tol : 1e-4 * (double)(e->K - 1);
+    control_kernel<<<(e->B + 127) / 128, 128, 0, s>>>(
+        e->B, std::max<int64_t>(e->K - 2, 0), (int)(e->K * e->n), e->epsi, e->ps, e->records,
+        e->cfg.max_iters, e->cfg.temp_high, e->cfg.tol_mean, e->cfg.tol_cost, ctol);
+    GVP_CUDA(cudaGetLastError());
+    GVP_CUDA(cudaEventRecord(ev[3], s));
+    GVP_CUDA(cudaEventSynchronize(ev[3]));
+    for (int j = 0; j < 3; ++j) {
+      float t = 0.f;
+      GVP_CUDA(cudaEventElapsedTime(&t, ev[j], ev[j + 1]));
+      acc[j] += t;
+    }
+    e->launches += 2;  // select + control (factors() counted itself)
+    ++e->iters_launched;
+  }
+  for (auto& x : ev) cudaEventDestroy(x);
+  for (int j = 0; j < 3; ++j) ms[j] = acc[j];
+  return GVP_OK;
+}
+
+extern "C" void* gvp_engine_stream(gvp_engine* e) { return (void*)e->stream; }
+
+extern "C" int gvp_engine_sync(gvp_engine* e) {
+  GVP_CUDA(cudaStreamSynchronize(e->stream));
+  return GVP_OK;
+}
+
+extern "C" int gvp_engine_active(gvp_engine* e, int32_t* nactive) {
+  GVP_CUDA(cudaMemsetAsync(e->ps.nactive, 0, sizeof(int), e->stream));
+  count_active_kernel<<<(e->B + 127) / 128, 128, 0, e->stream>>>(e->B, e->ps.active, e->ps.nactive);
+  GVP_CUDA(cudaGetLastError());
+  GVP_CUDA(cudaMemcpyAsync(nactive, e->ps.nactive, sizeof(int), cudaMemcpyDeviceToHost, e->stream));
+  GVP_CUDA(cudaStreamSynchronize(e->stream));
+  if (e->iters_launched >= e->cfg.max_iters) *nactive = 0;
+  return GVP_OK;
+}
+
+extern "C" int gvp_engine_get_state(gvp_engine* e, double* mean, double* diag, double* off,
+                                    double* covs, double* crosses) {
+  const int64_t B = e->B, K = e->K, B2 = e->B2();
+  cudaStream_t s = e->stream;
+  if (mean) GVP_CUDA(cudaMemcpyAsync(mean, e->mean, K * e->n * B * 8, cudaMemcpyDeviceToHost, s));
+  if (diag) GVP_CUDA(cudaMemcpyAsync(diag, e->diag, K * B2 * B * 8, cudaMemcpyDeviceToHost, s));
+  if (off) GVP_CUDA(cudaMemcpyAsync(off, e->off, (K - 1) * B2 * B * 8, cudaMemcpyDeviceToHost, s));
+  if (covs) GVP_CUDA(cudaMemcpyAsync(covs, e->covs, K * B2 * B * 8, cudaMemcpyDeviceToHost, s));
+  if (crosses) GVP_CUDA(cudaMemcpyAsync(crosses, e->crosses, (K - 1) * B2 * B * 8, cudaMemcpyDeviceToHost, s));
+  GVP_CUDA(cudaStreamSynchronize(s));
+  return GVP_OK;
+}
+
+extern "C" int gvp_engine_get_summary(gvp_engine* e, int32_t* converged, int32_t* iterations,
+                                      int32_t* switch_iteration, int32_t* status, int32_t* where) {
+  cudaStream_t s = e->stream;
+  const size_t bytes = e->B * sizeof(int);
+  if (converged) GVP_CUDA(cudaMemcpyAsync(converged, e->ps.converged, bytes, cudaMemcpyDeviceToHost, s));
+  if (iterations) GVP_CUDA(cudaMemcpyAsync(iterations, e->ps.iters, bytes, cudaMemcpyDeviceToHost, s));
+  if (switch_iteration) GVP_CUDA(cudaMemcpyAsync(switch_iteration, e->ps.switch_it, bytes, cudaMemcpyDeviceToHost, s));
+  if (status) GVP_CUDA(cudaMemcpyAsync(status, e->ps.status, bytes, cudaMemcpyDeviceToHost, s));
+  if (where) GVP_CUDA(cudaMemcpyAsync(where, e->ps.where, bytes, cudaMemcpyDeviceToHost, s));
+  GVP_CUDA(cudaStreamSynchronize(s));
+  return GVP_OK;
+}
+
+extern "C" int gvp_engine_get_records(gvp_engine* e, double* records) {
+  GVP_CUDA(cudaMemcpyAsync(records, e->records, (size_t)e->cfg.max_iters * e->B * GVP_NREC * 8,
+                           cudaMemcpyDeviceToHost, e->stream));
+  GVP_CUDA(cudaStreamSynchronize(e->stream));
+  return GVP_OK;
+}
+
+extern "C" int gvp_engine_device_state(gvp_engine* e, double** mean, double** diag, double** off,
+                                       double** covs, double** crosses) {
+  if (mean) *mean = e->mean;
+  if (diag) *diag = e->diag;
+  if (off) *off = e->off;
+  if (covs) *covs = e->covs;
+  if (crosses) *crosses = e->crosses;
+  return GVP_OK;
+}
+
+extern "C" int64_t gvp_engine_launches(gvp_engine* e) { return e->launches; }
+

@@ -1,0 +1,507 @@
+// Kernel (a): collision-factor quadrature on B200.
+//
+// Two kernels, both one thread per (plan, factor), plan index fastest so a
+// warp's loads of a knot's mean/covariance are 256 B contiguous:
+//
+//  * factor_moments_kernel — the reference's exact contract
+//    (_kernels.pyx:93-177): given (means, chols) produce e0/e1/e2 and the OOB
+//    count. It loops over every sigma point in ascending order and uses
+//    explicitly rounded fp64 ops (__dmul_rn/__dadd_rn, no FMA contraction) in
+//    the reference's evaluation order, so it reproduces the compiled
+//    reference (gcc -O3 on x86-64, no FMA) bit for bit.
+//
+//  * factor_grads_kernel — the fused engine kernel (factors.py:167-225 after
+//    marginal extraction): Cholesky of the knot covariance in registers, hinge
+//    potential evaluated once per distinct position projection of the rule
+//    (13 of 41 points at k_q=3, 57 of 385 at k_q=5), moments
+//    contracted with per-projection weight tensors, moment-form gradients via
+//    the triangular inverse (g_mu = L^{-T} E1, g_S = sym(-e0/2 P^{-1} +
+//    L^{-T} E2 L^{-1}/2)). Writes straight into the joint-gradient layout.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <vector>
+
+#include "gvp_internal.cuh"
+
+namespace gvp {
+
+// ======================================================================= Field
+Field::~Field() {
+  if (d_corners) cudaFree(d_corners);
+}
+
+int Field::build(const double* grid, int ndim, const int64_t* shape, const double* origin,
+                 double cell, cudaStream_t s) {
+  if (ndim != 2 && ndim != 3) {
+    set_error("grid must be 2D or 3D");
+    return GVP_ERR_UNSUPPORTED;
+  }
+  FieldDev f{};
+  f.ndim = ndim;
+  f.nz = ndim == 3 ? shape[0] : 1;
+  f.ny = shape[ndim - 2];
+  f.nx = shape[ndim - 1];
+  if (f.nx < 2 || f.ny < 2 || (ndim == 3 && f.nz < 2)) {
+    set_error("grid needs at least 2 nodes per axis");
+    return GVP_ERR_ARG;
+  }
+  f.ox = origin[0];
+  f.oy = origin[1];
+  f.oz = ndim == 3 ? origin[2] : 0.0;
+  f.cell = cell;
+  std::vector<double> packed;
+  if (ndim == 2) {
+    // corner-packed cells: (iy, ix) -> {g[iy][ix], g[iy][ix+1], g[iy+1][ix], g[iy+1][ix+1]}
+    const int64_t cy = f.ny - 1, cx = f.nx - 1;
+    packed.resize((size_t)(cy * cx * 4));
+    for (int64_t iy = 0; iy < cy; ++iy)
+      for (int64_t ix = 0; ix < cx; ++ix) {
+        double* c = &packed[(size_t)((iy * cx + ix) * 4)];
+        const double* r0 = grid + iy * f.nx + ix;
+        const double* r1 = r0 + f.nx;
+        c[0] = r0[0];
+        c[1] = r0[1];
+        c[2] = r1[0];
+        c[3] = r1[1];
+      }
+  } else {
+    // x-pair packed rows: (iz, iy, ix) -> {g[iz][iy][ix], g[iz][iy][ix+1]}
+    const int64_t cx = f.nx - 1;
+    packed.resize((size_t)(f.nz * f.ny * cx * 2));
+    for (int64_t iz = 0; iz < f.nz; ++iz)
+      for (int64_t iy = 0; iy < f.ny; ++iy)
+        for (int64_t ix = 0; ix < cx; ++ix) {
+          double* c = &packed[(size_t)(((iz * f.ny + iy) * cx + ix) * 2)];
+          const double* g = grid + (iz * f.ny + iy) * f.nx + ix;
+          c[0] = g[0];
+          c[1] = g[1];
+        }
+  }
+  const int64_t nbytes = (int64_t)(packed.size() * sizeof(double));
+  if (nbytes > bytes) {
+    if (d_corners) cudaFree(d_corners);
+    d_corners = nullptr;
+    GVP_CUDA(cudaMalloc(&d_corners, nbytes));
+    bytes = nbytes;
+  }
+  GVP_CUDA(cudaMemcpyAsync(d_corners, packed.data(), nbytes, cudaMemcpyHostToDevice, s));
+  GVP_CUDA(cudaStreamSynchronize(s));
+  f.corners = d_corners;
+  dev = f;
+  return GVP_OK;
+}
+
+// ======================================================================= Rule
+Rule::~Rule() {
+  if (d_buf) cudaFree(d_buf);
+  if (d_cnt) cudaFree(d_cnt);
+}
+
+int Rule::build(const double* points, const double* weights, int64_t npts, int n, int P,
+                cudaStream_t s) {
+  if (P > n) P = n;
+  // group points by the exact bit pattern of their first P coordinates
+  std::map<std::vector<uint64_t>, int64_t> key_to_proj;
+  std::vector<int64_t> order;  // first point of each projection, in order of appearance
+  std::vector<int64_t> proj_of(npts);
+  for (int64_t l = 0; l < npts; ++l) {
+    std::vector<uint64_t> key(P);
+    for (int k = 0; k < P; ++k) std::memcpy(&key[k], &points[l * n + k], sizeof(double));
+    auto it = key_to_proj.find(key);
+    if (it == key_to_proj.end()) {
+      const int64_t j = (int64_t)order.size();
+      key_to_proj.emplace(key, j);
+      order.push_back(l);
+      proj_of[l] = j;
+    } else {
+      proj_of[l] = it->second;
+    }
+  }
+  const int64_t nproj = (int64_t)order.size();
+  const int T = n * (n + 1) / 2;
+  const int M = 1 + n + T;
+  std::vector<double> proj((size_t)(nproj * P)), mom((size_t)(nproj * M), 0.0);
+  std::vector<int> cnt((size_t)nproj, 0);
+  for (int64_t j = 0; j < nproj; ++j)
+    for (int k = 0; k < P; ++k) proj[j * P + k] = points[order[j] * n + k];
+  for (int64_t l = 0; l < npts; ++l) {  // ascending point order within each group
+    const int64_t j = proj_of[l];
+    const double w = weights[l];
+    const double* x = points + l * n;
+    double* m = &mom[(size_t)(j * M)];
+    m[0] += w;
+    for (int r = 0; r < n; ++r) m[1 + r] += w * x[r];
+    for (int r = 0; r < n; ++r)
+      for (int c = 0; c <= r; ++c) m[1 + n + r * (r + 1) / 2 + c] += w * x[r] * x[c];
+    cnt[j] += 1;
+  }
+  const int64_t nd = npts * n + npts + nproj * P + nproj * M;
+  if (d_buf) cudaFree(d_buf);
+  if (d_cnt) cudaFree(d_cnt);
+  d_buf = nullptr;
+  d_cnt = nullptr;
+  GVP_CUDA(cudaMalloc(&d_buf, std::max<int64_t>(nd, 1) * sizeof(double)));
+  GVP_CUDA(cudaMalloc(&d_cnt, std::max<int64_t>(nproj, 1) * sizeof(int)));
+  double* p = d_buf;
+  GVP_CUDA(cudaMemcpyAsync(p, points, npts * n * sizeof(double), cudaMemcpyHostToDevice, s));
+  GVP_CUDA(cudaMemcpyAsync(p + npts * n, weights, npts * sizeof(double), cudaMemcpyHostToDevice, s));
+  GVP_CUDA(cudaMemcpyAsync(p + npts * n + npts, proj.data(), nproj * P * sizeof(double),
+                           cudaMemcpyHostToDevice, s));
+  GVP_CUDA(cudaMemcpyAsync(p + npts * n + npts + nproj * P, mom.data(), nproj * M * sizeof(double),
+                           cudaMemcpyHostToDevice, s));
+  GVP_CUDA(cudaMemcpyAsync(d_cnt, cnt.data(), nproj * sizeof(int), cudaMemcpyHostToDevice, s));
+  GVP_CUDA(cudaStreamSynchronize(s));
+  dev.n = n;
+  dev.P = P;
+  dev.npts = npts;
+  dev.nproj = nproj;
+  dev.points = p;
+  dev.weights = p + npts * n;
+  dev.proj = p + npts * n + npts;
+  dev.mom = p + npts * n + npts + nproj * P;
+  dev.cnt = d_cnt;
+  return GVP_OK;
+}
+
+// ============================================================ interpolation
+// Border-clamped bilinear interpolation with the reference's operation order
+// (_kernels.pyx:18-45). EXACT=true uses explicitly rounded ops (no FMA) so
+// the result equals gcc's x86-64 evaluation of the Cython kernel.
+template <bool EXACT>
+GVP_DEV double fmul(double a, double b) { return EXACT ? __dmul_rn(a, b) : a * b; }
+template <bool EXACT>
+GVP_DEV double fadd(double a, double b) { return EXACT ? __dadd_rn(a, b) : a + b; }
+template <bool EXACT>
+GVP_DEV double fsub(double a, double b) { return EXACT ? __dsub_rn(a, b) : a - b; }
+
+GVP_DEV double clamp_axis(double u, double top, bool& out) {
+  if (u < 0.0) {
+    out = true;
+    return 0.0;
+  }
+  if (u > top) {
+    out = true;
+    return top;
+  }
+  return u;
+}
+
+template <bool EXACT>
+GVP_DEV double interp2(const FieldDev& F, double px, double py, bool& out) {
+  double u = __ddiv_rn(__dsub_rn(px, F.ox), F.cell);
+  double v = __ddiv_rn(__dsub_rn(py, F.oy), F.cell);
+  out = false;
+  u = clamp_axis(u, (double)(F.nx - 1), out);
+  v = clamp_axis(v, (double)(F.ny - 1), out);
+  int64_t ix = (int64_t)floor(u);
+  int64_t iy = (int64_t)floor(v);
+  if (ix > F.nx - 2) ix = F.nx - 2;
+  if (iy > F.ny - 2) iy = F.ny - 2;
+  const double fx = fsub<EXACT>(u, (double)ix);
+  const double fy = fsub<EXACT>(v, (double)iy);
+  // one 32 B sector: {g00, g01, g10, g11}
+  const double2* c = reinterpret_cast<const double2*>(F.corners + (iy * (F.nx - 1) + ix) * 4);
+  const double2 a = __ldg(c);
+  const double2 b = __ldg(c + 1);
+  const double gx = fsub<EXACT>(1.0, fx), gy = fsub<EXACT>(1.0, fy);
+  double r = fmul<EXACT>(fmul<EXACT>(a.x, gx), gy);
+  r = fadd<EXACT>(r, fmul<EXACT>(fmul<EXACT>(a.y, fx), gy));
+  r = fadd<EXACT>(r, fmul<EXACT>(fmul<EXACT>(b.x, gx), fy));
+  r = fadd<EXACT>(r, fmul<EXACT>(fmul<EXACT>(b.y, fx), fy));
+  return r;
+}
+
+// trilinear (_kernels.pyx:48-90): two bilinear planes combined in z
+template <bool EXACT>
+GVP_DEV double interp3(const FieldDev& F, double px, double py, double pz, bool& out) {
+  double u = __ddiv_rn(__dsub_rn(px, F.ox), F.cell);
+  double v = __ddiv_rn(__dsub_rn(py, F.oy), F.cell);
+  double w = __ddiv_rn(__dsub_rn(pz, F.oz), F.cell);
+  out = false;
+  u = clamp_axis(u, (double)(F.nx - 1), out);
+  v = clamp_axis(v, (double)(F.ny - 1), out);
+  w = clamp_axis(w, (double)(F.nz - 1), out);
+  int64_t ix = (int64_t)floor(u), iy = (int64_t)floor(v), iz = (int64_t)floor(w);
+  if (ix > F.nx - 2) ix = F.nx - 2;
+  if (iy > F.ny - 2) iy = F.ny - 2;
+  if (iz > F.nz - 2) iz = F.nz - 2;
+  const double fx = fsub<EXACT>(u, (double)ix);
+  const double fy = fsub<EXACT>(v, (double)iy);
+  const double fz = fsub<EXACT>(w, (double)iz);
+  const int64_t cx = F.nx - 1;
+  const double2* base = reinterpret_cast<const double2*>(F.corners);
+  const double2 c00 = __ldg(base + (iz * F.ny + iy) * cx + ix);
+  const double2 c01 = __ldg(base + (iz * F.ny + iy + 1) * cx + ix);
+  const double2 c10 = __ldg(base + ((iz + 1) * F.ny + iy) * cx + ix);
+  const double2 c11 = __ldg(base + ((iz + 1) * F.ny + iy + 1) * cx + ix);
+  const double gx = fsub<EXACT>(1.0, fx), gy = fsub<EXACT>(1.0, fy), gz = fsub<EXACT>(1.0, fz);
+  double v0 = fmul<EXACT>(fmul<EXACT>(c00.x, gx), gy);
+  v0 = fadd<EXACT>(v0, fmul<EXACT>(fmul<EXACT>(c00.y, fx), gy));
+  v0 = fadd<EXACT>(v0, fmul<EXACT>(fmul<EXACT>(c01.x, gx), fy));
+  v0 = fadd<EXACT>(v0, fmul<EXACT>(fmul<EXACT>(c01.y, fx), fy));
+  double v1 = fmul<EXACT>(fmul<EXACT>(c10.x, gx), gy);
+  v1 = fadd<EXACT>(v1, fmul<EXACT>(fmul<EXACT>(c10.y, fx), gy));
+  v1 = fadd<EXACT>(v1, fmul<EXACT>(fmul<EXACT>(c11.x, gx), fy));
+  v1 = fadd<EXACT>(v1, fmul<EXACT>(fmul<EXACT>(c11.y, fx), fy));
+  return fadd<EXACT>(fmul<EXACT>(v0, gz), fmul<EXACT>(v1, fz));
+}
+
+// ============================================= exact-contract moments kernel
+template <int N>
+__global__ void __launch_bounds__(128)
+factor_moments_kernel(int64_t nfac, const double* __restrict__ means,
+                      const double* __restrict__ chols, RuleDev R, FieldDev F, double radius_eps,
+                      double sigma_obs, double* __restrict__ e0, double* __restrict__ e1,
+                      double* __restrict__ e2, unsigned long long* __restrict__ oob) {
+  const int64_t f = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (f >= nfac) return;
+  double L[N][N], mu[N];
+#pragma unroll
+  for (int r = 0; r < N; ++r) {
+    mu[r] = __ldg(means + f * N + r);
+#pragma unroll
+    for (int c = 0; c < N; ++c) L[r][c] = __ldg(chols + (f * N + r) * N + c);
+  }
+  double s0 = 0.0, s1[N], s2[N][N];
+#pragma unroll
+  for (int r = 0; r < N; ++r) {
+    s1[r] = 0.0;
+#pragma unroll
+    for (int c = 0; c < N; ++c) s2[r][c] = 0.0;
+  }
+  unsigned long long nout = 0;
+  for (int64_t l = 0; l < R.npts; ++l) {
+    double dx[N];
+#pragma unroll
+    for (int r = 0; r < N; ++r) {
+      double acc = 0.0;
+#pragma unroll
+      for (int k = 0; k < N; ++k) acc = __dadd_rn(acc, __dmul_rn(L[r][k], __ldg(R.points + l * N + k)));
+      dx[r] = acc;
+    }
+    bool out;
+    double dist;
+    if (F.ndim == 2) {
+      dist = interp2<true>(F, __dadd_rn(mu[0], dx[0]), __dadd_rn(mu[1], dx[1]), out);
+    } else {
+      dist = interp3<true>(F, __dadd_rn(mu[0], dx[0]), __dadd_rn(mu[1], dx[1]),
+                           __dadd_rn(mu[N > 2 ? 2 : 0], dx[N > 2 ? 2 : 0]), out);
+    }
+    nout += out ? 1ull : 0ull;
+    const double gap = __dsub_rn(radius_eps, dist);
+    if (gap > 0.0) {
+      const double wc = __dmul_rn(__dmul_rn(__dmul_rn(__ldg(R.weights + l), sigma_obs), gap), gap);
+      s0 = __dadd_rn(s0, wc);
+#pragma unroll
+      for (int r = 0; r < N; ++r) s1[r] = __dadd_rn(s1[r], __dmul_rn(wc, dx[r]));
+#pragma unroll
+      for (int r = 0; r < N; ++r)
+#pragma unroll
+        for (int c = 0; c < N; ++c) s2[r][c] = __dadd_rn(s2[r][c], __dmul_rn(__dmul_rn(wc, dx[r]), dx[c]));
+    }
+  }
+  e0[f] = s0;
+#pragma unroll
+  for (int r = 0; r < N; ++r) {
+    e1[f * N + r] = s1[r];
+#pragma unroll
+    for (int c = 0; c < N; ++c) e2[(f * N + r) * N + c] = s2[r][c];
+  }
+  if (nout) atomicAdd(oob, nout);
+}
+
+template <int N>
+static int moments_impl(int64_t nfac, const double* means, const double* chols, const RuleDev& R,
+                        const FieldDev& F, double re, double so, double* e0, double* e1, double* e2,
+                        unsigned long long* oob, cudaStream_t s) {
+  if (nfac == 0) return GVP_OK;
+  const int tpb = 128;
+  factor_moments_kernel<N><<<(unsigned)((nfac + tpb - 1) / tpb), tpb, 0, s>>>(
+      nfac, means, chols, R, F, re, so, e0, e1, e2, oob);
+  GVP_CUDA(cudaGetLastError());
+  return GVP_OK;
+}
+
+int launch_factor_moments(int64_t nfac, int n, const double* means, const double* chols,
+                          const RuleDev& R, const FieldDev& F, double re, double so, double* e0,
+                          double* e1, double* e2, unsigned long long* oob, cudaStream_t s) {
+  if (F.ndim == 3 && n < 3) {
+    set_error("3D field needs a state of at least 3 dims");
+    return GVP_ERR_ARG;
+  }
+  switch (n) {
+#define GVP_CASE(K) \
+  case K:           \
+    return moments_impl<K>(nfac, means, chols, R, F, re, so, e0, e1, e2, oob, s);
+    GVP_CASE(1) GVP_CASE(2) GVP_CASE(3) GVP_CASE(4) GVP_CASE(5) GVP_CASE(6) GVP_CASE(7) GVP_CASE(8)
+#undef GVP_CASE
+    default:
+      set_error("block size n must be in 1..8");
+      return GVP_ERR_UNSUPPORTED;
+  }
+}
+
+// ===================================================== fused gradients kernel
+template <int N, int P>
+__global__ void __launch_bounds__(128)
+factor_grads_kernel(int nplans, int64_t nfac, View mean, View covs, RuleDev R, FieldDev F,
+                    double radius_eps, double sigma_obs, FactorOut out,
+                    const int* __restrict__ active) {
+  constexpr int T = N * (N + 1) / 2;
+  constexpr int M = 1 + N + T;
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= nfac * nplans) return;
+  const int64_t b = t % nplans;
+  const int64_t f = t / nplans;
+  const int64_t knot = f + 1;  // interior factors 1..N-1 (factors.py:159-164)
+  if (active && !active[b]) return;
+
+  double mu[N], S[N][N], L[N][N];
+#pragma unroll
+  for (int r = 0; r < N; ++r) mu[r] = mean(b, knot, r);
+#pragma unroll
+  for (int r = 0; r < N; ++r)
+#pragma unroll
+    for (int c = 0; c <= r; ++c) S[r][c] = covs(b, knot, r * N + c);
+  // gaussian_sqrt (quadrature.py:164-177): Cholesky, then one 1e-10 jitter retry
+  // np.linalg.cholesky has no 1e-300 pivot floor: FLOOR=false
+  bool ok = chol<N, false>(S, L);
+  if (!ok) {
+#pragma unroll
+    for (int r = 0; r < N; ++r) S[r][r] += 1e-10;
+    ok = chol<N, false>(S, L);
+  }
+  if (!ok) {  // the eigh root branch is not taken on device: report it
+    atomicMax(out.status + b, GVP_ERR_SQRT);
+    atomicMin(out.where + b, (int)knot);
+    return;
+  }
+
+  // ---- quadrature over distinct position projections
+  double e0 = 0.0, E1[N], E2[T];
+#pragma unroll
+  for (int r = 0; r < N; ++r) E1[r] = 0.0;
+#pragma unroll
+  for (int k = 0; k < T; ++k) E2[k] = 0.0;
+  unsigned long long nout = 0;
+  for (int64_t j = 0; j < R.nproj; ++j) {
+    double pos[P];
+#pragma unroll
+    for (int r = 0; r < P; ++r) {
+      double acc = 0.0;
+#pragma unroll
+      for (int k = 0; k <= r; ++k) acc += L[r][k] * __ldg(R.proj + j * P + k);
+      pos[r] = mu[r] + acc;
+    }
+    bool o;
+    const double d = (P == 2) ? interp2<false>(F, pos[0], pos[1], o)
+                              : interp3<false>(F, pos[0], pos[1], pos[P - 1], o);
+    if (o) nout += (unsigned long long)__ldg(R.cnt + j);
+    const double gap = radius_eps - d;
+    if (gap > 0.0) {
+      const double psi = sigma_obs * gap * gap;
+      const double* m = R.mom + j * M;
+      e0 += psi * __ldg(m);
+#pragma unroll
+      for (int r = 0; r < N; ++r) E1[r] += psi * __ldg(m + 1 + r);
+#pragma unroll
+      for (int k = 0; k < T; ++k) E2[k] += psi * __ldg(m + 1 + N + k);
+    }
+  }
+  if (nout) atomicAdd(out.oob + b, nout);
+
+  // ---- moment-form gradients (factors.py:95-104) in the L^{-1} basis
+  double Li[N][N];
+  tri_inv<N>(L, Li);
+  bool finite = isfinite(e0);
+#pragma unroll
+  for (int r = 0; r < N; ++r) finite = finite && isfinite(E1[r]);
+#pragma unroll
+  for (int k = 0; k < T; ++k) finite = finite && isfinite(E2[k]);
+  if (!finite) {
+    atomicMax(out.status + b, GVP_ERR_NONFINITE);
+    atomicMin(out.where + b, (int)knot);
+    return;
+  }
+  // g_mu = L^{-T} E1
+#pragma unroll
+  for (int r = 0; r < N; ++r) {
+    double acc = 0.0;
+#pragma unroll
+    for (int k = r; k < N; ++k) acc += Li[k][r] * E1[k];
+    out.g_mu(b, knot, r) = acc;
+  }
+  // W = E2 L^{-1}  (E2 symmetric, packed)
+  double W[N][N];
+#pragma unroll
+  for (int r = 0; r < N; ++r)
+#pragma unroll
+    for (int c = 0; c < N; ++c) {
+      double acc = 0.0;
+#pragma unroll
+      for (int k = c; k < N; ++k) acc += E2[r >= k ? tri_idx(r, k) : tri_idx(k, r)] * Li[k][c];
+      W[r][c] = acc;
+    }
+  const double h0 = -0.5 * e0;
+#pragma unroll
+  for (int r = 0; r < N; ++r)
+#pragma unroll
+    for (int c = 0; c <= r; ++c) {
+      double hp = 0.0, pp = 0.0;  // (L^{-T} W)[r][c] and P^{-1}[r][c]
+#pragma unroll
+      for (int k = r; k < N; ++k) {
+        hp += Li[k][r] * W[k][c];
+        pp += Li[k][r] * Li[k][c];
+      }
+      const double g = h0 * pp + 0.5 * hp;
+      out.g_diag(b, knot, r * N + c) = g;
+      if (c != r) out.g_diag(b, knot, c * N + r) = g;
+    }
+  out.e_psi(b, f, 0) = e0 > 0.0 ? e0 : 0.0;  // e_psi = max(e0, 0) (factors.py:218-224)
+}
+
+template <int N, int P>
+static int grads_impl(int nplans, int64_t K, const View& mean, const View& covs, const RuleDev& R,
+                      const FieldDev& F, double re, double so, const FactorOut& out,
+                      const int* active, cudaStream_t s) {
+  const int64_t nfac = K - 2;
+  if (nfac <= 0 || nplans == 0) return GVP_OK;
+  const int64_t total = nfac * nplans;
+  const int tpb = 128;
+  factor_grads_kernel<N, P><<<(unsigned)((total + tpb - 1) / tpb), tpb, 0, s>>>(
+      nplans, nfac, mean, covs, R, F, re, so, out, active);
+  GVP_CUDA(cudaGetLastError());
+  return GVP_OK;
+}
+
+int launch_factor_grads(int nplans, int64_t K, int n, const View& mean, const View& covs,
+                        const RuleDev& R, const FieldDev& F, double re, double so,
+                        const FactorOut& out, const int* active, cudaStream_t s) {
+  if (F.ndim > n) {
+    set_error("field dimension exceeds state dimension");
+    return GVP_ERR_ARG;
+  }
+  if (R.P != F.ndim) {
+    set_error("rule projection dim must equal the field dim");
+    return GVP_ERR_ARG;
+  }
+#define GVP_CASE2(K_) \
+  case K_:            \
+    return F.ndim == 2 ? grads_impl<K_, 2>(nplans, K, mean, covs, R, F, re, so, out, active, s) \
+                       : grads_impl<K_, 3>(nplans, K, mean, covs, R, F, re, so, out, active, s);
+  switch (n) {
+    case 2:
+      return grads_impl<2, 2>(nplans, K, mean, covs, R, F, re, so, out, active, s);
+    GVP_CASE2(3) GVP_CASE2(4) GVP_CASE2(5) GVP_CASE2(6) GVP_CASE2(7) GVP_CASE2(8)
+    default:
+      set_error("fused factor kernel supports n in 2..8");
+      return GVP_ERR_UNSUPPORTED;
+  }
+#undef GVP_CASE2
+}
+
+}  // namespace gvp

@@ -1,0 +1,134 @@
+// Internal (C++) interfaces shared by the translation units of libgvp_b200.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/gvp_b200.h"
+#include "gvp_block.cuh"
+
+namespace gvp {
+
+// ------------------------------------------------------------------ errors
+void set_error(const std::string& msg);
+int cuda_fail(cudaError_t err, const char* what);
+#define GVP_CUDA(call)                                         \
+  do {                                                         \
+    cudaError_t _e = (call);                                   \
+    if (_e != cudaSuccess) return ::gvp::cuda_fail(_e, #call); \
+  } while (0)
+
+// ------------------------------------------------------------------ SDF field
+// Signed-distance grid resident in HBM in a "corner-packed" layout: cell
+// (iz, iy, ix) stores its 4 (2D) or 8 (3D) corner values contiguously, so the
+// bi/trilinear gather of one sigma point is a single 32 B / 64 B sector
+// fetch instead of 4 / 8 scattered loads. Values are the reference's grid
+// values bit for bit (sdf.py:23-56 layout: (ny, nx) / (nz, ny, nx), x
+// fastest).
+struct FieldDev {
+  int ndim;
+  int64_t nx, ny, nz;
+  double ox, oy, oz, cell;
+  const double* corners;  // device
+};
+
+struct Field {
+  FieldDev dev{};
+  double* d_corners = nullptr;
+  int64_t bytes = 0;
+  ~Field();
+  int build(const double* grid_host, int ndim, const int64_t* shape, const double* origin,
+            double cell, cudaStream_t s);
+};
+
+// ------------------------------------------------------------------ rule
+// Quadrature rule plus its position-projection tables (DESIGN.md §kernel a):
+// the hinge potential reads only x[:P] = mu[:P] + L[:P,:P] xi[:P] (L lower
+// triangular), so sigma points sharing xi[:P] share psi. Per distinct
+// projection j: coords xi_j[:P], point count, and the moments
+// m0_j = sum w_l, m1_j = sum w_l xi_l (n), m2_j = sum w_l xi_l xi_l^T (packed).
+struct RuleDev {
+  int n, P;
+  int64_t npts, nproj;
+  const double* points;   // (npts, n)   exact-contract kernel
+  const double* weights;  // (npts)
+  const double* proj;     // (nproj, P)
+  const double* mom;      // (nproj, 1 + n + n(n+1)/2)
+  const int* cnt;         // (nproj)
+};
+
+struct Rule {
+  RuleDev dev{};
+  double* d_buf = nullptr;
+  int* d_cnt = nullptr;
+  ~Rule();
+  int build(const double* points, const double* weights, int64_t npts, int n, int P,
+            cudaStream_t s);
+};
+
+// ------------------------------------------------------------------ launches
+// factor kernels (factor_kernels.cu)
+int launch_factor_moments(int64_t nfac, int n, const double* means, const double* chols,
+                          const RuleDev& rule, const FieldDev& field, double radius_eps,
+                          double sigma_obs, double* e0, double* e1, double* e2,
+                          unsigned long long* oob, cudaStream_t s);
+
+struct FactorOut {
+  MutView e_psi;  // (F) per plan
+  MutView g_mu;   // knot-indexed: entry for factor f at knot f+1 (view base at knot 0)
+  MutView g_diag; // knot-indexed
+  unsigned long long* oob;  // per plan
+  int* status;              // per plan (0 ok, GVP_ERR_*)
+  int* where;               // per plan (atomicMin'd factor index)
+};
+int launch_factor_grads(int nplans, int64_t nknots, int n, const View& mean, const View& covs,
+                        const RuleDev& rule, const FieldDev& field, double radius_eps,
+                        double sigma_obs, const FactorOut& out, const int* active,
+                        cudaStream_t s);
+
+// chain kernels (chain_kernels.cu)
+int launch_marginals(int nplans, int64_t K, int n, const View& diag, const View& off,
+                     const MutView& covs, const MutView& crosses, double* logdet, int* status,
+                     int* where, double* scratch, const int* active, cudaStream_t s);
+int launch_mean_solve(int nplans, int64_t K, int n, const View& diag, const View& off,
+                      const View& eta, const MutView& out, int* status, int* where,
+                      double* scratch, cudaStream_t s);
+int launch_logdet_fwd(int nplans, int64_t K, int n, const View& diag, const View& off,
+                      double* out, int* status, int* where, double* scratch, cudaStream_t s);
+
+struct StepProblem {
+  View mean, diag, off;      // current iterate
+  View kdiag, koff, info;    // prior (kdiag/koff may be shared, sp = 0)
+  View gmu, gdiag, goff;     // joint gradients (goff may be a zero view)
+  bool has_goff;
+  View pmean;                // prior mean (for the prior cost at commit)
+  bool has_pmean;
+};
+struct StepOut {
+  MutView mean, diag, off, covs, crosses;  // may alias the inputs (in-place commit)
+  double* beta;        // per plan
+  double* kl;          // per plan
+  double* logdet_next; // per plan: log det of the accepted precision
+  double* mean_shift;  // per plan: ||mu' - mu||
+  double* prior_cost;  // per plan (optional): 1/2 d'K^{-1}d + 1/2 tr(K^{-1} Sigma') of the accepted state
+  double* probe_log;   // optional (nplans, max_probes, 3)
+  int max_probes;
+  int* nprobes;        // optional per plan
+  int* status;
+  int* where;
+};
+struct StepParams {
+  const double* temp;        // per plan
+  const double* logdet_cur;  // per plan
+  double kl_bound, beta_min, beta_max;
+  int lanes;                 // speculative candidates per plan
+  bool fixed_beta;           // proximal_update only (no bisection, no KL)
+  const double* beta_fixed;  // per plan when fixed_beta
+};
+int launch_select_step(int nplans, int64_t K, int n, const StepProblem& pb, const StepParams& pr,
+                       const StepOut& out, double* scratch, const int* active, cudaStream_t s);
+int64_t chain_scratch_doubles(int nplans, int64_t K, int n, int lanes);
+
+}  // namespace gvp

@@ -1,0 +1,175 @@
+"""Host handle of the batched device engine (csrc/engine.cu).
+
+``PlanBatch`` owns one ``gvp_engine``: B independent P-GVIMP problems on one
+GPU sharing an SDF and a quadrature rule, all state resident in HBM in the
+plan-minor layout (include/gvp_b200.h). Arrays cross this API batch-major,
+shape (B, K, ...); the transposition to plan-minor happens here.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from . import _native as N
+from .quadrature import QuadratureRule
+from .sdf import CollisionModel, SignedDistanceField
+
+RECORD_KEYS = ("beta", "temperature", "prior_cost", "collision_cost", "entropy_cost",
+               "total_cost", "kl_step", "mean_shift")
+
+
+def to_plan_minor(x: np.ndarray) -> np.ndarray:
+    """(B, ...) -> (..., B) C-contiguous."""
+    return np.ascontiguousarray(np.moveaxis(np.asarray(x, dtype=np.float64), 0, -1))
+
+
+def from_plan_minor(x: np.ndarray) -> np.ndarray:
+    return np.ascontiguousarray(np.moveaxis(x, -1, 0))
+
+
+_FAR_FIELD = None
+
+
+def far_field() -> SignedDistanceField:
+    """Obstacle-free stand-in (env=None): every hinge is exactly zero."""
+    global _FAR_FIELD
+    if _FAR_FIELD is None:
+        _FAR_FIELD = SignedDistanceField(origin=np.zeros(2), cell_size=1.0, values=np.full((2, 2), 1e6))
+    return _FAR_FIELD
+
+
+class PlanBatch:
+    def __init__(self, nplans: int, nknots: int, n: int, sdf: SignedDistanceField,
+                 model: CollisionModel, rule: QuadratureRule, cfg, shared_prior: bool = True,
+                 spec_lanes: int = 1):
+        self.lib = N.load()
+        self.B, self.K, self.n = int(nplans), int(nknots), int(n)
+        self.shared_prior = bool(shared_prior)
+        self.max_iters = int(cfg.max_iters)
+        c = N.PlanConfig(kl_bound=cfg.kl_bound, beta_min=cfg.beta_min, beta_max=cfg.beta_max,
+                         temp_low=cfg.temp_low, temp_high=cfg.temp_high,
+                         collision_tol=-1.0 if cfg.collision_tol is None else cfg.collision_tol,
+                         tol_mean=cfg.tol_mean, tol_cost=cfg.tol_cost,
+                         init_cov_scale=cfg.init_cov_scale, max_iters=cfg.max_iters,
+                         spec_lanes=spec_lanes)
+        self._cfg = c
+        h = C.c_void_p()
+        grid = N.f64(sdf.values)
+        shape = np.asarray(grid.shape, dtype=np.int64)
+        origin = N.f64(sdf.origin)
+        code = self.lib.gvp_engine_create(C.byref(h), self.B, self.K, self.n, int(self.shared_prior),
+                                          N.ptr(grid), grid.ndim, N.ptr(shape), N.ptr(origin),
+                                          float(sdf.cell_size), float(model.radius_eps),
+                                          float(model.sigma_obs), N.ptr(rule.points),
+                                          N.ptr(rule.weights), rule.npoints, C.byref(c))
+        N.check(code, "gvp_engine_create")
+        if code != N.GVP_OK:
+            raise RuntimeError(f"gvp_engine_create: {N.last_error()}")
+        self.handle = h
+
+    # ------------------------------------------------------------ lifecycle
+    def close(self):
+        if getattr(self, "handle", None):
+            self.lib.gvp_engine_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _ok(self, code, what):
+        N.check(code, what)
+        if code != N.GVP_OK:
+            raise RuntimeError(f"{what}: {N.last_error()}")
+
+    # ------------------------------------------------------------ problem
+    def load(self, kdiag, koff, info, prior_mean, init_mean):
+        """kdiag (K,n,n)/koff (K-1,n,n) if shared_prior else (B,K,n,n)/(B,K-1,n,n);
+        info, prior_mean, init_mean (B, K, n)."""
+        if self.shared_prior:
+            kd, ko = N.f64(kdiag), N.f64(koff)
+        else:
+            kd, ko = to_plan_minor(kdiag), to_plan_minor(koff)
+        inf, pm, m0 = to_plan_minor(info), to_plan_minor(prior_mean), to_plan_minor(init_mean)
+        self._ok(self.lib.gvp_engine_load(self.handle, N.ptr(kd), N.ptr(ko), N.ptr(inf), N.ptr(pm),
+                                          N.ptr(m0)), "gvp_engine_load")
+
+    def load_device(self, kdiag_ptr, koff_ptr, info_ptr, pmean_ptr, mean_ptr):
+        """Device pointers already in the plan-minor layout (no host traffic)."""
+        self._ok(self.lib.gvp_engine_load_dev(self.handle, kdiag_ptr, koff_ptr, info_ptr,
+                                              pmean_ptr, mean_ptr), "gvp_engine_load_dev")
+
+    # ------------------------------------------------------------ execution
+    def step(self, iters: int = 1, sync: bool = False):
+        self._ok(self.lib.gvp_engine_step(self.handle, int(iters), int(sync)), "gvp_engine_step")
+
+    def step_profiled(self, iters: int = 1) -> np.ndarray:
+        """Kernel-by-kernel iterations with CUDA events; returns summed device
+        ms of (select_step, factor_grads, control)."""
+        ms = np.zeros(3)
+        self._ok(self.lib.gvp_engine_step_profiled(self.handle, int(iters), N.ptr(ms)),
+                 "gvp_engine_step_profiled")
+        return ms
+
+    def stream_ptr(self) -> int:
+        return int(self.lib.gvp_engine_stream(self.handle) or 0)
+
+    def sync(self):
+        self._ok(self.lib.gvp_engine_sync(self.handle), "gvp_engine_sync")
+
+    def active(self) -> int:
+        out = np.zeros(1, dtype=np.int32)
+        self._ok(self.lib.gvp_engine_active(self.handle, N.ptr(out)), "gvp_engine_active")
+        return int(out[0])
+
+    def run(self, check_every: int = 8) -> int:
+        """Iterate until every plan stopped (converged, failed or max_iters)."""
+        done = 0
+        while done < self.max_iters:
+            k = min(check_every, self.max_iters - done)
+            self.step(k)
+            done += k
+            if self.active() == 0:
+                break
+        self.sync()
+        return done
+
+    def launches(self) -> int:
+        return int(self.lib.gvp_engine_launches(self.handle))
+
+    # ------------------------------------------------------------ results
+    def state(self):
+        B, K, n = self.B, self.K, self.n
+        mean = np.empty((K, n, B))
+        diag = np.empty((K, n, n, B))
+        off = np.empty((K - 1, n, n, B))
+        covs = np.empty((K, n, n, B))
+        crosses = np.empty((K - 1, n, n, B))
+        self._ok(self.lib.gvp_engine_get_state(self.handle, N.ptr(mean), N.ptr(diag), N.ptr(off),
+                                               N.ptr(covs), N.ptr(crosses)), "gvp_engine_get_state")
+        return {"mean": from_plan_minor(mean), "diag": from_plan_minor(diag),
+                "off": from_plan_minor(off), "covs": from_plan_minor(covs),
+                "crosses": from_plan_minor(crosses)}
+
+    def summary(self):
+        B = self.B
+        arrs = [np.zeros(B, dtype=np.int32) for _ in range(5)]
+        self._ok(self.lib.gvp_engine_get_summary(self.handle, *[N.ptr(a) for a in arrs]),
+                 "gvp_engine_get_summary")
+        return dict(zip(("converged", "iterations", "switch_iteration", "status", "where"), arrs))
+
+    def records(self) -> np.ndarray:
+        """(B, max_iters, 8) in RECORD_KEYS order; NaN past each plan's end."""
+        rec = np.empty((self.max_iters, self.B, N.GVP_NREC))
+        self._ok(self.lib.gvp_engine_get_records(self.handle, N.ptr(rec)), "gvp_engine_get_records")
+        return np.ascontiguousarray(np.moveaxis(rec, 1, 0))
+
+    def device_state(self):
+        ptrs = [C.c_void_p() for _ in range(5)]
+        self._ok(self.lib.gvp_engine_device_state(self.handle, *[C.byref(p) for p in ptrs]),
+                 "gvp_engine_device_state")
+        return dict(zip(("mean", "diag", "off", "covs", "crosses"), [p.value for p in ptrs]))

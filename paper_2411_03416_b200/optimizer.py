@@ -1,0 +1,348 @@
+"""KL-proximal update loop (API of gvplan/optimizer.py), on the GPU.
+
+* ``proximal_update``  -> gvp_proximal_update   (prox_update_kernel)
+* ``select_step_size`` -> gvp_select_step_size  (select_step_kernel: the whole
+                          bisection, each probe two fused chain passes)
+* ``run_pgvimp``       -> the batched engine with B = 1 (csrc/engine.cu):
+                          every iteration is one CUDA-graph replay of
+                          step-select, factor stage and cost/convergence
+                          control; nothing returns to the host until the
+                          run stops.
+* ``run_pgvimp_batch`` -> the same engine for many independent plans.
+"""
+
+from __future__ import annotations
+
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _native as N
+from .blocktri import BlockTridiagonalMatrix, NotPositiveDefiniteError, logdet_block_tridiag
+from .dynamics import LTVSystem
+from .engine import RECORD_KEYS, PlanBatch, far_field
+from .factors import FactorGradient, evaluate_all_factors
+from .gbp import ChainMarginals, gbp_marginals, trace_product
+from .prior import DiscretePrior, assemble_prior
+from .quadrature import QuadratureRule, smolyak_rule
+from .sdf import CollisionModel, SignedDistanceField
+
+_LOG_2PI = float(np.log(2.0 * np.pi))
+_BISECTION_RTOL = 1e-3
+
+
+@dataclass(frozen=True)
+class JointGaussian:
+    mean: np.ndarray
+    prec: BlockTridiagonalMatrix
+
+    def __post_init__(self):
+        mean = np.asarray(self.mean, dtype=np.float64).reshape(-1)
+        if mean.shape[0] != self.prec.dim:
+            raise ValueError(f"mean dim {mean.shape[0]} != precision dim {self.prec.dim}")
+        object.__setattr__(self, "mean", mean)
+
+    @property
+    def nblocks(self) -> int:
+        return self.prec.nblocks
+
+    @property
+    def block_size(self) -> int:
+        return self.prec.block_size
+
+
+@dataclass
+class Environment:
+    sdf: SignedDistanceField
+    model: CollisionModel
+
+
+@dataclass
+class OptimizerConfig:
+    """Defaults of optimizer.py:72-99."""
+
+    kl_bound: float = 0.1
+    beta_min: float = 1e-4
+    beta_max: float = 0.9
+    temp_low: float = 1.0
+    temp_high: float = 10.0
+    collision_tol: float | None = None
+    max_iters: int = 200
+    tol_mean: float = 1e-5
+    tol_cost: float = 1e-6
+    k_q: int = 3
+    init: str = "interp"
+    init_cov_scale: float = 0.1
+    init_mean: np.ndarray | None = None
+    threads: int = 1
+
+    def validate(self) -> None:
+        if self.kl_bound <= 0:
+            raise ValueError("kl_bound must be positive")
+        if not 0 < self.beta_min < self.beta_max:
+            raise ValueError("need 0 < beta_min < beta_max")
+        if self.temp_low <= 0 or self.temp_high <= 0:
+            raise ValueError("temperatures must be positive")
+        if self.max_iters < 1:
+            raise ValueError("max_iters must be >= 1")
+        if self.init not in ("interp", "flow", "prior"):
+            raise ValueError("init must be 'interp', 'flow', or 'prior'")
+
+
+@dataclass(frozen=True)
+class CostBreakdown:
+    prior_cost: float
+    collision_cost: float
+    entropy_cost: float
+
+    @property
+    def mp_cost(self) -> float:
+        return self.prior_cost + self.collision_cost
+
+    @property
+    def total(self) -> float:
+        return self.prior_cost + self.collision_cost + self.entropy_cost
+
+
+@dataclass
+class RunResult:
+    final: JointGaussian
+    marginals: ChainMarginals
+    records: list = field(default_factory=list)
+    converged: bool = False
+    iterations: int = 0
+    switch_iteration: int | None = None
+    wall_time_ms: float = 0.0
+
+
+@dataclass
+class StepSelection:
+    beta: float
+    next_state: JointGaussian
+    kl: float
+    marginals: ChainMarginals
+    probes: np.ndarray | None = None  # (nprobes, 3): beta, spd_ok, kl
+
+
+def _step_arrays(cur, prior, g_mu, g_sigma):
+    K, n = cur.nblocks, cur.block_size
+    return (N.f64(cur.mean).reshape(K, n), N.f64(cur.prec.diag_stack), N.f64(cur.prec.off_stack),
+            N.f64(prior.prec.diag_stack), N.f64(prior.prec.off_stack), N.f64(prior.info).reshape(K, n),
+            N.f64(g_mu).reshape(K, n), N.f64(g_sigma.diag_stack), N.f64(g_sigma.off_stack))
+
+
+def proximal_update(cur: JointGaussian, prior: DiscretePrior, g_mu: np.ndarray,
+                    g_sigma: BlockTridiagonalMatrix, beta: float, temp: float) -> JointGaussian:
+    """One Theorem-1 step at step size beta (optimizer.py:129-161)."""
+    if beta <= 0:
+        raise ValueError("beta must be positive")
+    lib = N.load()
+    K, n = cur.nblocks, cur.block_size
+    arrs = _step_arrays(cur, prior, g_mu, g_sigma)
+    om, od, oo = np.empty((K, n)), np.empty((K, n, n)), np.empty((max(K - 1, 0), n, n))
+    where = np.zeros(1, dtype=np.int64)
+    code = N.check(lib.gvp_proximal_update(*[N.ptr(a) for a in arrs], K, n, float(beta), float(temp),
+                                           N.ptr(om), N.ptr(od), N.ptr(oo), N.ptr(where)),
+                   "proximal_update")
+    if code == N.GVP_ERR_NOT_SPD:
+        raise NotPositiveDefiniteError(f"pivot block {int(where[0])} is not positive definite")
+    return JointGaussian(mean=om.reshape(-1), prec=BlockTridiagonalMatrix(od, oo))
+
+
+def kl_joint(nxt: JointGaussian, cur: JointGaussian, nxt_marginals: ChainMarginals | None = None) -> float:
+    """KL(next || cur), clipped at 0 (optimizer.py:164-177); marginals and
+    log-dets from the GPU."""
+    if nxt_marginals is None:
+        nxt_marginals = gbp_marginals(nxt.prec)
+    delta = cur.mean - nxt.mean
+    val = 0.5 * (trace_product(cur.prec, nxt_marginals) + cur.prec.quad_form(delta) - cur.prec.dim
+                 + logdet_block_tridiag(nxt.prec) - logdet_block_tridiag(cur.prec))
+    return max(val, 0.0)
+
+
+def select_step_size(cur: JointGaussian, prior: DiscretePrior, g_mu: np.ndarray,
+                     g_sigma: BlockTridiagonalMatrix, cfg: OptimizerConfig, temp: float,
+                     max_probes: int = 64) -> StepSelection:
+    """Largest feasible beta in [beta_min, beta_max] by bisection to 1e-3
+    relative width (optimizer.py:188-231); the whole search runs on device."""
+    lib = N.load()
+    K, n = cur.nblocks, cur.block_size
+    arrs = _step_arrays(cur, prior, g_mu, g_sigma)
+    beta, kl = np.zeros(1), np.zeros(1)
+    om, od, oo = np.empty((K, n)), np.empty((K, n, n)), np.empty((max(K - 1, 0), n, n))
+    cv, cr = np.empty((K, n, n)), np.empty((max(K - 1, 0), n, n))
+    plog = np.zeros((max_probes, 3))
+    nprobes = np.zeros(1, dtype=np.int32)
+    where = np.zeros(1, dtype=np.int64)
+    code = N.check(lib.gvp_select_step_size(
+        *[N.ptr(a) for a in arrs], K, n, float(temp), float(cfg.kl_bound), float(cfg.beta_min),
+        float(cfg.beta_max), N.ptr(beta), N.ptr(kl), N.ptr(om), N.ptr(od), N.ptr(oo), N.ptr(cv),
+        N.ptr(cr), N.ptr(plog), max_probes, N.ptr(nprobes), N.ptr(where)), "select_step_size")
+    if code == N.GVP_ERR_NO_FEASIBLE_STEP:
+        raise RuntimeError(f"no feasible step size at beta_min={cfg.beta_min} (KL bound {cfg.kl_bound})")
+    if code == N.GVP_ERR_NOT_SPD:
+        w = int(where[0]) & ~N.GVP_WHERE_MEAN_SOLVE_BIAS
+        raise NotPositiveDefiniteError(f"pivot block {w} is not positive definite")
+    return StepSelection(beta=float(beta[0]),
+                         next_state=JointGaussian(mean=om.reshape(-1), prec=BlockTridiagonalMatrix(od, oo)),
+                         kl=float(kl[0]), marginals=ChainMarginals.from_stacks(cv, cr),
+                         probes=plog[:min(int(nprobes[0]), max_probes)].copy())
+
+
+def entropy_of(prec: BlockTridiagonalMatrix) -> float:
+    return 0.5 * (prec.dim * (_LOG_2PI + 1.0) - logdet_block_tridiag(prec))
+
+
+def cost_breakdown(cur: JointGaussian, prior: DiscretePrior, temp: float,
+                   marginals: ChainMarginals | None = None,
+                   factor_values: list | None = None, env: Environment | None = None,
+                   rule: QuadratureRule | None = None, threads: int = 1) -> CostBreakdown:
+    """(prior, collision, -T H) costs of an iterate (optimizer.py:238-277)."""
+    if marginals is None:
+        marginals = gbp_marginals(cur.prec)
+    delta = cur.mean - prior.mean
+    prior_cost = 0.5 * prior.prec.quad_form(delta) + 0.5 * trace_product(prior.prec, marginals)
+    if factor_values is None:
+        if env is None:
+            factor_values = []
+        else:
+            if rule is None:
+                raise ValueError("rule required to evaluate collision cost")
+            factor_values = evaluate_all_factors(cur.mean, cur.prec, env.sdf, env.model, rule,
+                                                 threads=threads, marginals=marginals)
+    collision = float(sum(f.e_psi for f in factor_values))
+    return CostBreakdown(prior_cost=prior_cost, collision_cost=collision,
+                         entropy_cost=-temp * entropy_of(cur.prec))
+
+
+def initial_mean(prior: DiscretePrior, cfg: OptimizerConfig) -> np.ndarray:
+    K, n = prior.nsteps + 1, prior.n
+    if cfg.init_mean is not None:
+        mean = np.asarray(cfg.init_mean, dtype=np.float64).reshape(-1)
+        if mean.shape[0] != K * n:
+            raise ValueError("init_mean has wrong dimension")
+        return mean.copy()
+    if cfg.init == "flow":
+        return prior.flow_mean.copy()
+    if cfg.init == "prior":
+        return prior.mean.copy()
+    a = np.linspace(0.0, 1.0, K).reshape(-1, 1)
+    return ((1.0 - a) * prior.x0 + a * prior.goal).reshape(-1)
+
+
+def initial_state(prior: DiscretePrior, cfg: OptimizerConfig) -> JointGaussian:
+    """Sigma_0 = init_cov_scale K  <=>  Lambda_0 = K^{-1} / init_cov_scale
+    (optimizer.py:280-296)."""
+    return JointGaussian(mean=initial_mean(prior, cfg), prec=prior.prec.scaled(1.0 / cfg.init_cov_scale))
+
+
+def _records_to_dicts(rec: np.ndarray, iters: int, ms_per_iter: float) -> list:
+    out = []
+    for it in range(iters):
+        d = {"type": "iter", "iter": it + 1}
+        d.update({k: float(v) for k, v in zip(RECORD_KEYS, rec[it])})
+        d["wall_time_ms"] = ms_per_iter
+        out.append(d)
+    return out
+
+
+def _raise_plan_status(status: int, where: int, cfg: OptimizerConfig):
+    if status == N.GVP_ERR_NO_FEASIBLE_STEP:
+        raise RuntimeError(f"no feasible step size at beta_min={cfg.beta_min} (KL bound {cfg.kl_bound})")
+    if status == N.GVP_ERR_NOT_SPD:
+        raise NotPositiveDefiniteError(
+            f"pivot block {where & ~N.GVP_WHERE_MEAN_SOLVE_BIAS} is not positive definite")
+    if status == N.GVP_ERR_NONFINITE:
+        from .factors import FactorEvaluationError
+        raise FactorEvaluationError(where, "non-finite expectation")
+    if status == N.GVP_ERR_SQRT:
+        raise NotImplementedError(f"factor {where}: covariance needs the eigh root of gaussian_sqrt")
+    if status != 0:
+        raise RuntimeError(f"plan failed with status {status}")
+
+
+def run_pgvimp(sys_ltv: LTVSystem, env: Environment | None, cfg: OptimizerConfig, x0, goal,
+               q_c: float, sigma_b: float, prior: DiscretePrior | None = None,
+               spec_lanes: int = 1) -> RunResult:
+    """Algorithm 1 (optimizer.py:299-401) on the GPU engine."""
+    cfg.validate()
+    t0 = time.perf_counter()
+    if prior is None:
+        prior = assemble_prior(sys_ltv, x0, goal, q_c, sigma_b)
+    K, n = prior.nsteps + 1, prior.n
+    rule = smolyak_rule(cfg.k_q, n)
+    sdf = env.sdf if env is not None else far_field()
+    model = env.model if env is not None else CollisionModel(0.0, 1.0)
+    eng = PlanBatch(1, K, n, sdf, model, rule, cfg, shared_prior=True, spec_lanes=spec_lanes)
+    try:
+        eng.load(prior.prec.diag_stack, prior.prec.off_stack, prior.info.reshape(1, K, n),
+                 prior.mean.reshape(1, K, n), initial_mean(prior, cfg).reshape(1, K, n))
+        eng.run()
+        st = eng.state()
+        sm = eng.summary()
+        rec = eng.records()[0]
+    finally:
+        eng.close()
+    status, where = int(sm["status"][0]), int(sm["where"][0])
+    _raise_plan_status(status, where, cfg)
+    iters = int(sm["iterations"][0])
+    wall = (time.perf_counter() - t0) * 1e3
+    final = JointGaussian(mean=st["mean"][0].reshape(-1),
+                          prec=BlockTridiagonalMatrix(st["diag"][0], st["off"][0]))
+    sw = int(sm["switch_iteration"][0])
+    return RunResult(final=final, marginals=ChainMarginals.from_stacks(st["covs"][0], st["crosses"][0]),
+                     records=_records_to_dicts(rec, iters, wall / max(iters, 1)),
+                     converged=bool(sm["converged"][0]), iterations=iters,
+                     switch_iteration=None if sw < 0 else sw, wall_time_ms=wall)
+
+
+@dataclass
+class BatchResult:
+    """Batch-major results of ``run_pgvimp_batch``."""
+
+    mean: np.ndarray        # (B, K, n)
+    diag: np.ndarray        # (B, K, n, n)
+    off: np.ndarray         # (B, K-1, n, n)
+    covs: np.ndarray
+    crosses: np.ndarray
+    records: np.ndarray     # (B, max_iters, 8), RECORD_KEYS
+    converged: np.ndarray
+    iterations: np.ndarray
+    switch_iteration: np.ndarray
+    status: np.ndarray
+    wall_time_ms: float
+
+
+def run_pgvimp_batch(sys_ltv: LTVSystem, env: Environment | None, cfg: OptimizerConfig, x0s, goals,
+                     q_c: float, sigma_b: float, spec_lanes: int = 1) -> BatchResult:
+    """Many independent plans on one GPU: same system, map and settings, per
+    plan start/goal (SURVEY.md §8-e batch axis). Plans that fail are masked
+    out with their status; the batch never aborts."""
+    cfg.validate()
+    t0 = time.perf_counter()
+    x0s = np.atleast_2d(np.asarray(x0s, dtype=np.float64))
+    goals = np.atleast_2d(np.asarray(goals, dtype=np.float64))
+    B = max(len(x0s), len(goals))
+    x0s = np.broadcast_to(x0s, (B, x0s.shape[1]))
+    goals = np.broadcast_to(goals, (B, goals.shape[1]))
+    priors = [assemble_prior(sys_ltv, x0s[b], goals[b], q_c, sigma_b) for b in range(B)]
+    K, n = priors[0].nsteps + 1, priors[0].n
+    rule = smolyak_rule(cfg.k_q, n)
+    sdf = env.sdf if env is not None else far_field()
+    model = env.model if env is not None else CollisionModel(0.0, 1.0)
+    eng = PlanBatch(B, K, n, sdf, model, rule, cfg, shared_prior=True, spec_lanes=spec_lanes)
+    try:
+        eng.load(priors[0].prec.diag_stack, priors[0].prec.off_stack,
+                 np.stack([p.info.reshape(K, n) for p in priors]),
+                 np.stack([p.mean.reshape(K, n) for p in priors]),
+                 np.stack([initial_mean(p, cfg).reshape(K, n) for p in priors]))
+        eng.run()
+        st = eng.state()
+        sm = eng.summary()
+        rec = eng.records()
+    finally:
+        eng.close()
+    return BatchResult(records=rec, converged=sm["converged"].astype(bool),
+                       iterations=sm["iterations"], switch_iteration=sm["switch_iteration"],
+                       status=sm["status"], wall_time_ms=(time.perf_counter() - t0) * 1e3, **st)

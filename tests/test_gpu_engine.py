@@ -1,0 +1,108 @@
+"""GPU engine (csrc/engine.cu): whole Algorithm-1 runs vs the reference's
+recorded runs, and batch == independent single runs."""
+
+import numpy as np
+import pytest
+
+import gvp_oracle as O
+from conftest import golden, rel_err
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-9
+
+
+@pytest.fixture(scope="module")
+def P(gpu):
+    import paper_2411_03416_b200 as P
+
+    assert P.HAVE_EXTENSION
+    return P
+
+
+def c1_env(P):
+    sdf = P.rasterize([P.sdf.Disc(center=np.array([1.1, 0.55]), radius=0.45)], bounds=[[-2, 4], [-2, 4]],
+                      cell_size=0.05)
+    return P.Environment(sdf=sdf, model=P.CollisionModel(radius_eps=0.2, sigma_obs=8.0))
+
+
+def test_short_run_matches_reference_records(P):
+    """Reference test scene (test_optimizer.py:158-163), N=15, default config,
+    25 iterations (tests/golden runs.npz t15)."""
+    g = golden("runs")
+    sdf = P.rasterize([P.sdf.Disc(center=np.array([1.0, 0.75]), radius=0.45)], bounds=[[-2, 4], [-2, 4]],
+                      cell_size=0.05)
+    env = P.Environment(sdf=sdf, model=P.CollisionModel(radius_eps=0.2, sigma_obs=8.0))
+    res = P.run_pgvimp(P.point_robot_lti(2)(15, 0.2), env, P.OptimizerConfig(max_iters=25), np.zeros(4),
+                       np.array([2.0, 1.5, 0.0, 0.0]), 1.0, 1e-3)
+    keys = list(g["record_keys"])
+    got = np.array([[r[k] for k in keys] for r in res.records])
+    ref = g["t15_records"]
+    assert got.shape == ref.shape
+    assert np.array_equal(got[:, 0], ref[:, 0])  # identical beta sequence
+    assert np.array_equal(got[:, 1], ref[:, 1])  # identical temperature schedule
+    assert rel_err(got[:, 2:6], ref[:, 2:6]) <= TOL
+    assert rel_err(res.final.mean.reshape(16, 4), g["t15_final_mean"]) <= TOL
+    assert rel_err(np.stack(res.marginals.covs), g["t15_final_covs"]) <= TOL
+    assert res.converged == bool(g["t15_meta"][0]) and res.iterations == int(g["t15_meta"][1])
+
+
+@pytest.mark.slow
+def test_c1_converges_like_reference(P):
+    """C1 pinned: reference converges in 94 iterations."""
+    g = golden("runs")
+    cfg = P.OptimizerConfig(k_q=3, kl_bound=10.0, beta_max=0.5, max_iters=600)
+    res = P.run_pgvimp(P.point_robot_lti(2)(50, 3.0 / 50), c1_env(P), cfg, np.zeros(4),
+                       np.array([2.0, 1.5, 0.0, 0.0]), 1.0, 1e-3)
+    ref = g["c1_records"]
+    keys = list(g["record_keys"])
+    got = np.array([[r[k] for k in keys] for r in res.records])
+    assert res.converged and res.iterations == int(g["c1_meta"][1])
+    assert np.array_equal(got[:, 0], ref[:, 0])
+    assert rel_err(got[:, 5], ref[:, 5]) <= TOL
+    assert rel_err(res.final.mean.reshape(51, 4), g["c1_final_mean"]) <= TOL
+    assert rel_err(np.stack(res.marginals.covs), g["c1_final_covs"]) <= TOL
+
+
+def test_obstacle_free_converges_to_prior(P):
+    """test_optimizer.py:167-175 on the engine (env=None)."""
+    sys_ltv = P.point_robot_lti(2)(20, 0.2)
+    prior = P.assemble_prior(sys_ltv, np.zeros(4), np.array([2.0, 1.5, 0, 0]), 1.0, 1e-3)
+    cfg = P.OptimizerConfig(temp_low=1.0, temp_high=1.0, max_iters=300, kl_bound=10.0)
+    res = P.run_pgvimp(sys_ltv, None, cfg, np.zeros(4), np.array([2.0, 1.5, 0, 0]), 1.0, 1e-3)
+    assert res.converged
+    assert np.linalg.norm(res.final.mean - prior.mean) <= 1e-5 * np.linalg.norm(prior.mean)
+
+
+def test_batch_equals_single_runs(P):
+    """B plans in one engine give bit-identical results to B=1 runs."""
+    env = c1_env(P)
+    sys_ltv = P.point_robot_lti(2)(30, 0.1)
+    cfg = P.OptimizerConfig(k_q=3, kl_bound=10.0, beta_max=0.5, max_iters=12)
+    rng = np.random.default_rng(5)
+    goals = np.tile(np.array([2.0, 1.5, 0.0, 0.0]), (6, 1))
+    goals[:, :2] += rng.uniform(-0.3, 0.3, size=(6, 2))
+    batch = P.run_pgvimp_batch(sys_ltv, env, cfg, np.zeros(4), goals, 1.0, 1e-3)
+    assert np.all(batch.status == 0)
+    for b in range(6):
+        single = P.run_pgvimp(sys_ltv, env, cfg, np.zeros(4), goals[b], 1.0, 1e-3)
+        assert batch.iterations[b] == single.iterations
+        assert np.array_equal(batch.mean[b].reshape(-1), single.final.mean)
+        assert np.array_equal(batch.covs[b], np.stack(single.marginals.covs))
+
+
+def test_engine_matches_oracle_driver(P):
+    """A few C1 iterations: engine records vs the oracle's restated driver."""
+    env = c1_env(P)
+    sys_ltv = P.point_robot_lti(2)(50, 3.0 / 50)
+    prior = P.assemble_prior(sys_ltv, np.zeros(4), np.array([2.0, 1.5, 0, 0]), 1.0, 1e-3)
+    cfg = P.OptimizerConfig(k_q=3, kl_bound=10.0, beta_max=0.5, max_iters=6)
+    res = P.run_pgvimp(sys_ltv, env, cfg, np.zeros(4), np.array([2.0, 1.5, 0, 0]), 1.0, 1e-3, prior=prior)
+    rule = P.smolyak_rule(3, 4)
+    pr = {"diag": prior.prec.diag_stack, "off": prior.prec.off_stack, "info": prior.info.reshape(51, 4),
+          "mean": prior.mean.reshape(51, 4)}
+    ref = O.run_pgvimp(pr, env.sdf.values, env.sdf.origin, 0.05, 0.2, 8.0, rule.points, rule.weights,
+                       kl_bound=10.0, beta_max=0.5, max_iters=6, x0=np.zeros(4), goal=np.array([2.0, 1.5, 0, 0]))
+    assert [r["beta"] for r in res.records] == [r["beta"] for r in ref["records"]]
+    for a, b in zip(res.records, ref["records"]):
+        for k in ("prior_cost", "collision_cost", "entropy_cost", "total_cost"):
+            assert abs(a[k] - b[k]) <= TOL * max(1.0, abs(b[k])), (k, a[k], b[k])
