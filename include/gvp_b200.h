@@ -130,6 +130,10 @@ int gvp_select_step_size(const double* mean, const double* diag, const double* o
                          double* crosses, double* probe_log, int32_t max_probes,
                          int32_t* nprobes, int64_t* where);
 
+/* Candidate lanes (1, 4, 8, 16, 32) gvp_select_step_size probes concurrently;
+ * the beta sequence is the reference's for any value (default 32). */
+int gvp_set_step_lanes(int32_t lanes);
+
 /* -------------------------------------------------------- 2. batched engine */
 
 typedef struct gvp_plan_config {
@@ -143,7 +147,7 @@ typedef struct gvp_plan_config {
   double tol_cost;
   double init_cov_scale;
   int32_t max_iters;
-  int32_t spec_lanes;    /* candidate betas evaluated concurrently per plan (1 = plain bisection) */
+  int32_t spec_lanes;    /* candidate betas probed concurrently per plan: 0 = auto, else 1/4/8/16/32 */
 } gvp_plan_config;
 
 typedef struct gvp_engine gvp_engine;
@@ -197,7 +201,10 @@ int gvp_engine_get_summary(gvp_engine* e, int32_t* converged, int32_t* iteration
  * (optimizer.py:366-379); rows past a plan's last iteration are NaN. */
 #define GVP_NREC 8
 int gvp_engine_get_records(gvp_engine* e, double* records);
-/* Device pointers of the resident state, for zero-copy consumers. */
+/* Candidate lanes per plan the engine runs with (after auto selection). */
+int32_t gvp_engine_lanes(gvp_engine* e);
+/* Device pointers of the resident state, for zero-copy consumers. Layout:
+ * plan-minor; diag and covs are packed lower-symmetric, (nknots, n(n+1)/2, B). */
 int gvp_engine_device_state(gvp_engine* e, double** mean, double** diag, double** off,
                             double** covs, double** crosses);
 /* Launch counters: kernels launched by this engine since create. */

@@ -93,6 +93,40 @@ static int d2h(T* dst, const T* src, size_t count, cudaStream_t s) {
   return GVP_OK;
 }
 
+// full (K, n, n) -> packed lower (K, n(n+1)/2) and back (host side of the C ABI)
+static std::vector<double> pack_lower(const double* full, int64_t K, int n) {
+  const int T = n * (n + 1) / 2;
+  std::vector<double> out((size_t)(K * T));
+  for (int64_t i = 0; i < K; ++i)
+    for (int r = 0; r < n; ++r)
+      for (int c = 0; c <= r; ++c) out[(size_t)(i * T + r * (r + 1) / 2 + c)] = full[(i * n + r) * n + c];
+  return out;
+}
+static void unpack_sym(const double* packed, int64_t K, int n, double* full) {
+  const int T = n * (n + 1) / 2;
+  for (int64_t i = 0; i < K; ++i)
+    for (int r = 0; r < n; ++r)
+      for (int c = 0; c <= r; ++c) {
+        const double v = packed[i * T + r * (r + 1) / 2 + c];
+        full[(i * n + r) * n + c] = v;
+        full[(i * n + c) * n + r] = v;
+      }
+}
+static bool blocks_symmetric(const double* full, int64_t K, int n) {
+  for (int64_t i = 0; i < K; ++i)
+    for (int r = 0; r < n; ++r)
+      for (int c = 0; c < r; ++c)
+        if (full[(i * n + r) * n + c] != full[(i * n + c) * n + r]) return false;
+  return true;
+}
+static bool all_zero(const double* p, int64_t count) {
+  if (!p) return true;
+  for (int64_t k = 0; k < count; ++k)
+    if (p[k] != 0.0) return false;
+  return true;
+}
+static int g_step_lanes = 32;  // candidate lanes of the drop-in select_step_size (one plan)
+
 static int check_n(int n) {
   if (n < 1 || n > 8) {
     set_error("block size n must be in 1..8");
@@ -179,30 +213,36 @@ extern "C" int gvp_evaluate_factors(const double* mean, const double* covs, int6
   double *d_mean, *d_covs, *d_epsi, *d_gmu, *d_gd;
   unsigned long long* d_oob;
   int* d_st;
+  const int T = n * (n + 1) / 2;
   GVP_TRY(C.arena.get(0, K * n, &d_mean));
-  GVP_TRY(C.arena.get(1, K * n * n, &d_covs));
+  GVP_TRY(C.arena.get(1, K * T, &d_covs));
   GVP_TRY(C.arena.get(2, F, &d_epsi));
   GVP_TRY(C.arena.get(3, K * n, &d_gmu));
-  GVP_TRY(C.arena.get(4, K * n * n, &d_gd));
+  GVP_TRY(C.arena.get(4, K * T, &d_gd));
   GVP_TRY(C.arena.get(5, 1, &d_oob));
   GVP_TRY(C.arena.get(6, 2, &d_st));
+  // the kernel reads the lower triangle of each covariance block, like
+  // np.linalg.cholesky does in gaussian_sqrt (quadrature.py:175)
+  const std::vector<double> covs_p = pack_lower(covs, K, n);
   GVP_TRY(h2d(d_mean, mean, K * n, s));
-  GVP_TRY(h2d(d_covs, covs, K * n * n, s));
+  GVP_TRY(h2d(d_covs, covs_p.data(), K * T, s));
   GVP_CUDA(cudaMemsetAsync(d_oob, 0, sizeof(unsigned long long), s));
   const int init_st[2] = {0, INT_MAX};
   GVP_TRY(h2d(d_st, init_st, 2, s));
-  FactorOut fo{pmview(d_epsi, 1, 1), pmview(d_gmu, n, 1), pmview(d_gd, n * n, 1), d_oob, d_st,
+  FactorOut fo{pmview(d_epsi, 1, 1), pmview(d_gmu, n, 1), pmview(d_gd, T, 1), d_oob, d_st,
                d_st + 1};
-  GVP_TRY(launch_factor_grads(1, K, n, pview(d_mean, n, 1), pview(d_covs, n * n, 1),
-                              C.rule.dev, C.field.dev, radius_eps, sigma_obs, fo, nullptr, s));
+  GVP_TRY(launch_factor_grads(1, K, n, pview(d_mean, n, 1), pview(d_covs, T, 1), C.rule.dev,
+                              C.field.dev, radius_eps, sigma_obs, fo, nullptr, s));
   int st[2];
   unsigned long long h_oob;
+  std::vector<double> gd_p((size_t)(F * T));
   GVP_TRY(d2h(st, d_st, 2, s));
   GVP_TRY(d2h(&h_oob, d_oob, 1, s));
   GVP_TRY(d2h(e_psi, d_epsi, F, s));
   GVP_TRY(d2h(g_mu, d_gmu + n, F * n, s));
-  GVP_TRY(d2h(g_sigma, d_gd + n * n, F * n * n, s));
+  GVP_TRY(d2h(gd_p.data(), d_gd + T, F * T, s));
   GVP_CUDA(cudaStreamSynchronize(s));
+  unpack_sym(gd_p.data(), F, n, g_sigma);
   *oob = (int64_t)h_oob;
   if (st[0] != GVP_OK) {
     *where = st[1];
@@ -400,18 +440,17 @@ extern "C" int gvp_proximal_update(const double* mean, const double* diag, const
   return GVP_OK;
 }
 
-extern "C" int gvp_select_step_size(const double* mean, const double* diag, const double* off,
-                                    const double* kdiag, const double* koff, const double* info,
-                                    const double* g_mu, const double* gdiag, const double* goff,
-                                    int64_t nblocks, int32_t n, double temp, double kl_bound,
-                                    double beta_min, double beta_max, double* beta, double* kl,
-                                    double* out_mean, double* out_diag, double* out_off,
-                                    double* covs, double* crosses, double* probe_log,
-                                    int32_t max_probes, int32_t* nprobes, int64_t* where) {
+// general-layout fallback (full blocks, one thread, pairwise-factor off
+// gradients and non-symmetric diagonal blocks allowed): chain_kernels.cu
+static int select_step_size_v1(const double* mean, const double* diag, const double* off,
+                               const double* kdiag, const double* koff, const double* info,
+                               const double* g_mu, const double* gdiag, const double* goff,
+                               int64_t nblocks, int32_t n, double temp, double kl_bound,
+                               double beta_min, double beta_max, double* beta, double* kl,
+                               double* out_mean, double* out_diag, double* out_off, double* covs,
+                               double* crosses, double* probe_log, int32_t max_probes,
+                               int32_t* nprobes, int64_t* where) {
   Context& C = ctx();
-  std::lock_guard<std::mutex> lock(C.mu);
-  GVP_TRY(C.init());
-  GVP_TRY(check_n(n));
   const int64_t K = nblocks, B2 = (int64_t)n * n;
   StepBufs b;
   StepProblem pb;
@@ -476,6 +515,134 @@ extern "C" int gvp_select_step_size(const double* mean, const double* diag, cons
   GVP_TRY(d2h(covs, b.covs, K * B2, s));
   GVP_TRY(d2h(crosses, b.crosses, (K - 1) * B2, s));
   GVP_CUDA(cudaStreamSynchronize(s));
+  *beta = sc[0];
+  *kl = sc[1];
+  if (where) *where = -1;
+  return GVP_OK;
+}
+
+extern "C" int gvp_set_step_lanes(int32_t lanes) {
+  if (lanes != 1 && lanes != 4 && lanes != 8 && lanes != 16 && lanes != 32) {
+    set_error("lanes must be 1, 4, 8, 16 or 32");
+    return GVP_ERR_ARG;
+  }
+  g_step_lanes = lanes;
+  return GVP_OK;
+}
+
+extern "C" int gvp_select_step_size(const double* mean, const double* diag, const double* off,
+                                    const double* kdiag, const double* koff, const double* info,
+                                    const double* g_mu, const double* gdiag, const double* goff,
+                                    int64_t nblocks, int32_t n, double temp, double kl_bound,
+                                    double beta_min, double beta_max, double* beta, double* kl,
+                                    double* out_mean, double* out_diag, double* out_off,
+                                    double* covs, double* crosses, double* probe_log,
+                                    int32_t max_probes, int32_t* nprobes, int64_t* where) {
+  Context& C = ctx();
+  std::lock_guard<std::mutex> lock(C.mu);
+  GVP_TRY(C.init());
+  GVP_TRY(check_n(n));
+  const int64_t K = nblocks, N2 = (int64_t)n * n, K1 = std::max<int64_t>(K - 1, 0);
+  const bool v2_ok = (n == 2 || n == 4 || n == 6) && blocks_symmetric(diag, K, n) &&
+                     blocks_symmetric(kdiag, K, n) && blocks_symmetric(gdiag, K, n) &&
+                     all_zero(goff, K1 * N2);
+  if (!v2_ok)
+    return select_step_size_v1(mean, diag, off, kdiag, koff, info, g_mu, gdiag, goff, nblocks, n,
+                               temp, kl_bound, beta_min, beta_max, beta, kl, out_mean, out_diag,
+                               out_off, covs, crosses, probe_log, max_probes, nprobes, where);
+  // ---- v2: packed layout, speculative bisection lanes (step_kernel.cu)
+  cudaStream_t s = C.stream;
+  const int T = n * (n + 1) / 2;
+  const int L = g_step_lanes;
+  const std::vector<double> ld_p = pack_lower(diag, K, n), kd_p = pack_lower(kdiag, K, n),
+                            gd_p = pack_lower(gdiag, K, n);
+  double *ld, *lo, *kd, *ko, *gd, *g, *eta, *v, *mu, *omu, *old_, *olo, *ocov, *ocr, *ov, *scal,
+      *plog, *scr;
+  int* st;
+  const int64_t K1a = std::max<int64_t>(K1, 1);
+  GVP_TRY(C.arena.get(40, K * T, &ld));
+  GVP_TRY(C.arena.get(41, K1a * N2, &lo));
+  GVP_TRY(C.arena.get(42, K * T, &kd));
+  GVP_TRY(C.arena.get(43, K1a * N2, &ko));
+  GVP_TRY(C.arena.get(44, K * T, &gd));
+  GVP_TRY(C.arena.get(45, K * n, &g));
+  GVP_TRY(C.arena.get(46, K * n, &eta));
+  GVP_TRY(C.arena.get(47, K * n, &v));
+  GVP_TRY(C.arena.get(48, K * n, &mu));
+  GVP_TRY(C.arena.get(49, K * n, &omu));
+  GVP_TRY(C.arena.get(50, K * T, &old_));
+  GVP_TRY(C.arena.get(51, K1a * N2, &olo));
+  GVP_TRY(C.arena.get(52, K * T, &ocov));
+  GVP_TRY(C.arena.get(53, K1a * N2, &ocr));
+  GVP_TRY(C.arena.get(54, K * n, &ov));
+  GVP_TRY(C.arena.get(55, 8, &scal));
+  GVP_TRY(C.arena.get(56, std::max(max_probes, 1) * 3, &plog));
+  GVP_TRY(C.arena.get(57, (size_t)std::max(step_scratch_doubles(1, K, n, L), K * T), &scr));
+  GVP_TRY(C.arena.get(58, 4, &st));
+  GVP_TRY(h2d(ld, ld_p.data(), K * T, s));
+  GVP_TRY(h2d(lo, off, K1 * N2, s));
+  GVP_TRY(h2d(kd, kd_p.data(), K * T, s));
+  GVP_TRY(h2d(ko, koff, K1 * N2, s));
+  GVP_TRY(h2d(gd, gd_p.data(), K * T, s));
+  GVP_TRY(h2d(g, g_mu, K * n, s));
+  GVP_TRY(h2d(eta, info, K * n, s));
+  GVP_TRY(h2d(mu, mean, K * n, s));
+  GVP_TRY(h2d(scal + 4, &temp, 1, s));
+  // rhs piece Lambda mu, and log det of the current precision from the same
+  // backward Schur pivots the probes use (consistent KL)
+  GVP_TRY(launch_lam_mu(1, K, n, 1, ld, lo, mu, v, s));
+  GVP_TRY(launch_marginals_packed(1, K, n, 1, ld, lo, ocov, ocr, scal + 5, st, st + 1, scr,
+                                  nullptr, s));
+  int64_t w0 = -1;
+  if (fetch_status(C, st, &w0) != GVP_OK) {
+    if (where) *where = w0;
+    set_error("current precision is not positive definite at knot " + std::to_string(w0));
+    return GVP_ERR_NOT_SPD;
+  }
+  V2Launch q{};
+  q.nplans = 1; q.K = K; q.n = n; q.Bp = 1; q.lanes = L;
+  q.ld = ld; q.lo = lo; q.kd = kd; q.ko = ko; q.gd = gd; q.g = g; q.eta = eta; q.v = v;
+  q.mu = mu; q.pmean = mu; q.kshared = false;
+  q.o_mu = omu; q.o_ld = old_; q.o_lo = olo; q.o_cov = ocov; q.o_cr = ocr; q.o_v = ov;
+  q.beta = scal; q.kl = scal + 1; q.ld_next = scal + 2; q.shift = scal + 3; q.prior_cost = nullptr;
+  q.temp = scal + 4; q.ld_cur = scal + 5;
+  q.kl_bound = kl_bound; q.beta_min = beta_min; q.beta_max = beta_max;
+  q.status = st; q.where = st + 1;
+  q.probe_log = probe_log ? plog : nullptr; q.max_probes = max_probes; q.nprobes = st + 2;
+  q.scratch = scr; q.active = nullptr;
+  GVP_TRY(launch_select_step_v2(q, s));
+  int stw[3];
+  GVP_TRY(d2h(stw, st, 3, s));
+  GVP_CUDA(cudaStreamSynchronize(s));
+  if (nprobes) *nprobes = stw[2];
+  if (probe_log && stw[2] > 0) {
+    GVP_TRY(d2h(probe_log, plog, (size_t)std::min(stw[2], max_probes) * 3, s));
+    GVP_CUDA(cudaStreamSynchronize(s));
+  }
+  if (stw[0] != GVP_OK) {
+    if (where) *where = stw[1];
+    if (stw[0] == GVP_ERR_NO_FEASIBLE_STEP) {
+      char msg[160];
+      std::snprintf(msg, sizeof msg, "no feasible step size at beta_min=%g (KL bound %g)", beta_min,
+                    kl_bound);
+      set_error(msg);
+    } else {
+      set_error("pivot block " + std::to_string(stw[1] & ~GVP_WHERE_MEAN_SOLVE_BIAS) +
+                " is not positive definite");
+    }
+    return stw[0];
+  }
+  double sc[2];
+  std::vector<double> ldo((size_t)(K * T)), covo((size_t)(K * T));
+  GVP_TRY(d2h(sc, scal, 2, s));
+  GVP_TRY(d2h(out_mean, omu, K * n, s));
+  GVP_TRY(d2h(ldo.data(), old_, K * T, s));
+  GVP_TRY(d2h(out_off, olo, K1 * N2, s));
+  GVP_TRY(d2h(covo.data(), ocov, K * T, s));
+  GVP_TRY(d2h(crosses, ocr, K1 * N2, s));
+  GVP_CUDA(cudaStreamSynchronize(s));
+  unpack_sym(ldo.data(), K, n, out_diag);
+  unpack_sym(covo.data(), K, n, covs);
   *beta = sc[0];
   *kl = sc[1];
   if (where) *where = -1;

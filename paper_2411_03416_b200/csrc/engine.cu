@@ -2,19 +2,25 @@
 // independent plans, all state resident in HBM, no host round trip inside an
 // iteration. One iteration = 3 kernels on the engine stream:
 //
-//   select_step_kernel   bisection + in-place commit of (mu, Lambda) and the
-//                        accepted marginals, KL, log det, prior cost
-//   factor_grads_kernel  collision factors at the accepted state (the cache
-//                        the next iteration's step uses, optimizer.py:354-360)
-//   control_kernel       cost_breakdown (optimizer.py:238-277), the record,
-//                        convergence and temperature switch (optimizer.py:381-398)
+//   select_step_v2_kernel  bisection (speculative lanes) + in-place commit of
+//                          (mu, Lambda), the accepted marginals, KL, log det,
+//                          prior cost and Lambda mu for the next rhs
+//   factor_grads_kernel    collision factors at the accepted state (the cache
+//                          the next iteration's step uses, optimizer.py:354-360)
+//   control_kernel         cost_breakdown (optimizer.py:238-277), the record,
+//                          convergence and temperature switch (optimizer.py:381-398)
 //
 // The iteration is captured once into a CUDA graph and replayed.
+//
+// Device layout: plan-minor with plan stride B; diagonal blocks (precision,
+// prior precision, covariances, collision Hessian terms) packed lower
+// symmetric, n(n+1)/2 entries; off-diagonal blocks full n x n.
 #include <cuda_runtime.h>
 
 #include <algorithm>
 #include <climits>
 #include <cmath>
+#include <cstdlib>
 #include <vector>
 
 #include "gvp_internal.cuh"
@@ -25,7 +31,6 @@ namespace {
 constexpr double kLog2Pi = 1.8378770664093453;  // log(2 pi), optimizer.py:38
 
 struct PlanState {
-  // per-plan scalars (device)
   double *temp, *logdet, *beta, *kl, *shift, *prior_cost, *prev_total, *prev_temp, *total;
   int *active, *status, *where, *converged, *iters, *switch_it, *switched, *fstatus, *fwhere;
   unsigned long long* oob;
@@ -50,21 +55,24 @@ __global__ void init_plans_kernel(int B, PlanState ps, double temp_low) {
   ps.oob[b] = 0;
 }
 
-// initial_state (optimizer.py:280-296): Lambda_0 = K^{-1} / init_cov_scale
-__global__ void init_prec_kernel(int64_t count_diag, int64_t count_off, const double* kd,
-                                 const double* ko, int64_t ksp_diag, int64_t ksp_off, double* d,
-                                 double* o, int B, double inv_scale) {
+// full (K, n, n, kb) -> packed (K, T, kb) times `scale`
+__global__ void pack_sym_kernel(int64_t K, int n, int64_t kb, const double* __restrict__ src,
+                                double* __restrict__ dst, double scale) {
+  const int T = n * (n + 1) / 2;
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  // count_* = number of (knot, entry) pairs; plans interleaved
-  if (t < count_diag * B) {
-    const int64_t b = t % B, e = t / B;
-    d[t] = kd[ksp_diag ? t : e] * inv_scale;
-  } else if (t < (count_diag + count_off) * B) {
-    const int64_t u = t - count_diag * B;
-    const int64_t b = u % B, e = u / B;
-    (void)b;
-    o[u] = ko[ksp_off ? u : e] * inv_scale;
-  }
+  if (t >= K * T * kb) return;
+  const int64_t b = t % kb, q = (t / kb) % T, i = t / (kb * T);
+  int r = 0;
+  while ((r + 1) * (r + 2) / 2 <= q) ++r;
+  const int c = (int)q - r * (r + 1) / 2;
+  dst[t] = src[((i * n + r) * n + c) * kb + b] * scale;
+}
+// broadcast a shared (K, E) array to per-plan (K, E, B) times `scale`
+__global__ void scale_copy_kernel(int64_t count, int64_t B, const double* __restrict__ src,
+                                  int64_t src_sp, double* __restrict__ dst, double scale) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= count) return;
+  dst[t] = (src_sp ? src[t] : src[t / B]) * scale;
 }
 
 __global__ void control_kernel(int B, int64_t F, int n64dim, const double* __restrict__ epsi,
@@ -122,7 +130,6 @@ __global__ void control_kernel(int B, int64_t F, int n64dim, const double* __res
     ps.active[b] = 0;
     return;
   }
-  atomicAdd(ps.nactive, 1);
 }
 
 __global__ void fill_kernel(double* p, int64_t count, double v) {
@@ -134,22 +141,26 @@ __global__ void count_active_kernel(int B, const int* active, int* out) {
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b < B && active[b]) atomicAdd(out, 1);
 }
+
+inline unsigned nblk(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
 }  // namespace
 
 struct gvp_engine {
   int B = 0;
   int64_t K = 0;
-  int n = 0;
+  int n = 0, T = 0;
   bool shared_prior = false;
+  int lanes = 1;
   cudaStream_t stream = nullptr;
   Field field;
   Rule rule;
   double radius_eps = 0, sigma_obs = 0;
   gvp_plan_config cfg{};
-  // resident state (plan-minor)
+  // resident state (plan-minor; diag-type blocks packed)
   double *mean = nullptr, *diag = nullptr, *off = nullptr, *covs = nullptr, *crosses = nullptr;
   double *kdiag = nullptr, *koff = nullptr, *info = nullptr, *pmean = nullptr;
-  double *gmu = nullptr, *gdiag = nullptr, *epsi = nullptr, *scratch = nullptr;
+  double *gmu = nullptr, *gdiag = nullptr, *v = nullptr, *epsi = nullptr, *scratch = nullptr;
+  double *kfull_d = nullptr;  // staging for full-block prior uploads
   double* records = nullptr;
   double* scal = nullptr;
   int* ints = nullptr;
@@ -160,12 +171,12 @@ struct gvp_engine {
   int64_t launches = 0;
   std::vector<void*> allocs;
 
-  template <class T>
-  int alloc(T** p, size_t count) {
+  template <class Tp>
+  int alloc(Tp** p, size_t count) {
     void* q = nullptr;
-    GVP_CUDA(cudaMalloc(&q, std::max<size_t>(count, 1) * sizeof(T)));
+    GVP_CUDA(cudaMalloc(&q, std::max<size_t>(count, 1) * sizeof(Tp)));
     allocs.push_back(q);
-    *p = static_cast<T*>(q);
+    *p = static_cast<Tp*>(q);
     return GVP_OK;
   }
   ~gvp_engine() {
@@ -173,45 +184,66 @@ struct gvp_engine {
     for (void* p : allocs) cudaFree(p);
     if (stream) cudaStreamDestroy(stream);
   }
-
-  int64_t B2() const { return (int64_t)n * n; }
-  View v(const double* p, int64_t E) const { return View{p, E * B, B, 1}; }
-  MutView mv(double* p, int64_t E) const { return MutView{p, E * B, B, 1}; }
-  View kv(const double* p) const {
-    return shared_prior ? View{p, B2(), 1, 0} : View{p, B2() * B, B, 1};
-  }
+  int64_t kb() const { return shared_prior ? 1 : B; }
+  View vw(const double* p, int64_t E) const { return View{p, E * B, B, 1}; }
+  MutView mvw(double* p, int64_t E) const { return MutView{p, E * B, B, 1}; }
 
   int factors() {
-    FactorOut fo{mv(epsi, 1), mv(gmu, n), mv(gdiag, B2()), ps.oob, ps.fstatus, ps.fwhere};
+    FactorOut fo{mvw(epsi, 1), mvw(gmu, n), mvw(gdiag, T), ps.oob, ps.fstatus, ps.fwhere};
     launches += (K > 2);
-    return launch_factor_grads(B, K, n, v(mean, n), v(covs, B2()), rule.dev, field.dev,
-                               radius_eps, sigma_obs, fo, ps.active, stream);
+    return launch_factor_grads(B, K, n, vw(mean, n), vw(covs, T), rule.dev, field.dev, radius_eps,
+                               sigma_obs, fo, ps.active, stream);
   }
 
-  int iteration_body() {
-    StepProblem pb{v(mean, n),  v(diag, B2()), v(off, B2()), kv(kdiag),   kv(koff),
-                   v(info, n),  v(gmu, n),     v(gdiag, B2()), v(gdiag, B2()), false,
-                   v(pmean, n), true};
-    StepParams pr{ps.temp, ps.logdet, cfg.kl_bound, cfg.beta_min, cfg.beta_max,
-                  std::max(1, cfg.spec_lanes), false, nullptr};
-    StepOut out{mv(mean, n),     mv(diag, B2()), mv(off, B2()), mv(covs, B2()),
-                mv(crosses, B2()), ps.beta,      ps.kl,         ps.logdet,
-                ps.shift,        ps.prior_cost,  nullptr,       0,
-                nullptr,         ps.status,      ps.where};
-    int r = launch_select_step(B, K, n, pb, pr, out, scratch, ps.active, stream);
-    if (r) return r;
-    ++launches;
-    r = factors();
-    if (r) return r;
+  V2Launch step_args() const {
+    V2Launch q{};
+    q.nplans = B;
+    q.K = K;
+    q.n = n;
+    q.Bp = B;
+    q.lanes = lanes;
+    q.ld = diag; q.lo = off; q.kd = kdiag; q.ko = koff; q.gd = gdiag;
+    q.g = gmu; q.eta = info; q.v = v; q.mu = mean; q.pmean = pmean;
+    q.kshared = shared_prior;
+    q.o_mu = mean; q.o_ld = diag; q.o_lo = off; q.o_cov = covs; q.o_cr = crosses; q.o_v = v;
+    q.beta = ps.beta; q.kl = ps.kl; q.ld_next = ps.logdet; q.shift = ps.shift;
+    q.prior_cost = ps.prior_cost;
+    q.temp = ps.temp; q.ld_cur = ps.logdet;
+    q.kl_bound = cfg.kl_bound; q.beta_min = cfg.beta_min; q.beta_max = cfg.beta_max;
+    q.status = ps.status; q.where = ps.where;
+    q.probe_log = nullptr; q.max_probes = 0; q.nprobes = nullptr;
+    q.scratch = scratch;
+    q.active = ps.active;
+    return q;
+  }
+
+  int control() {
     const double ctol = cfg.collision_tol >= 0 ? cfg.collision_tol : 1e-4 * (double)(K - 1);
-    control_kernel<<<(B + 127) / 128, 128, 0, stream>>>(
-        B, std::max<int64_t>(K - 2, 0), (int)(K * n), epsi, ps, records, cfg.max_iters,
-        cfg.temp_high, cfg.tol_mean, cfg.tol_cost, ctol);
+    control_kernel<<<nblk(B, 128), 128, 0, stream>>>(B, std::max<int64_t>(K - 2, 0), (int)(K * n),
+                                                     epsi, ps, records, cfg.max_iters,
+                                                     cfg.temp_high, cfg.tol_mean, cfg.tol_cost, ctol);
     ++launches;
     GVP_CUDA(cudaGetLastError());
     return GVP_OK;
   }
+
+  int iteration_body() {
+    int r = launch_select_step_v2(step_args(), stream);
+    if (r) return r;
+    ++launches;
+    if ((r = factors())) return r;
+    return control();
+  }
 };
+
+static int pick_lanes(const gvp_plan_config* cfg, int B) {
+  if (cfg->spec_lanes > 0) return cfg->spec_lanes;
+  // fill the GPU: ~2 warps per SM of candidate lanes, at most 32 per plan
+  int L = 1;
+  while (L < 32 && (int64_t)B * L < 148 * 64) L *= 2;
+  if (L == 2) L = 4;
+  return L;
+}
 
 extern "C" int gvp_engine_create(gvp_engine** out, int32_t nplans, int64_t nknots, int32_t n,
                                  int32_t shared_prior, const double* grid, int32_t grid_ndim,
@@ -220,12 +252,22 @@ extern "C" int gvp_engine_create(gvp_engine** out, int32_t nplans, int64_t nknot
                                  const double* points, const double* weights, int64_t npts,
                                  const gvp_plan_config* cfg) {
   *out = nullptr;
-  if (nplans < 1 || nknots < 2 || n < 1 || n > 8 || !cfg) {
+  if (nplans < 1 || nknots < 2 || !cfg) {
     set_error("bad engine dimensions");
     return GVP_ERR_ARG;
   }
-  if (cfg->max_iters < 1 || !(cfg->kl_bound > 0) || !(0 < cfg->beta_min && cfg->beta_min < cfg->beta_max)) {
+  if (n != 2 && n != 4 && n != 6) {
+    set_error("engine supports state size n in {2, 4, 6}");
+    return GVP_ERR_UNSUPPORTED;
+  }
+  if (cfg->max_iters < 1 || !(cfg->kl_bound > 0) ||
+      !(0 < cfg->beta_min && cfg->beta_min < cfg->beta_max)) {
     set_error("invalid optimizer config (optimizer.py:89-99)");
+    return GVP_ERR_ARG;
+  }
+  const int lanes = pick_lanes(cfg, nplans);
+  if (lanes != 1 && lanes != 4 && lanes != 8 && lanes != 16 && lanes != 32) {
+    set_error("spec_lanes must be 0 (auto), 1, 4, 8, 16 or 32");
     return GVP_ERR_ARG;
   }
   int ndev = 0;
@@ -238,6 +280,8 @@ extern "C" int gvp_engine_create(gvp_engine** out, int32_t nplans, int64_t nknot
   e->B = nplans;
   e->K = nknots;
   e->n = n;
+  e->T = n * (n + 1) / 2;
+  e->lanes = lanes;
   e->shared_prior = shared_prior != 0;
   e->cfg = *cfg;
   e->radius_eps = radius_eps;
@@ -252,16 +296,16 @@ extern "C" int gvp_engine_create(gvp_engine** out, int32_t nplans, int64_t nknot
   if ((r = e->field.build(grid, grid_ndim, grid_shape, origin, cell_size, e->stream))) return fail(r);
   if (grid_ndim > n) return set_error("grid dim exceeds state dim"), fail(GVP_ERR_ARG);
   if ((r = e->rule.build(points, weights, npts, n, grid_ndim, e->stream))) return fail(r);
-  const int64_t B = nplans, K = nknots, B2 = (int64_t)n * n;
-  const int64_t kb = e->shared_prior ? 1 : B;
-  if ((r = e->alloc(&e->mean, K * n * B)) || (r = e->alloc(&e->diag, K * B2 * B)) ||
-      (r = e->alloc(&e->off, (K - 1) * B2 * B)) || (r = e->alloc(&e->covs, K * B2 * B)) ||
-      (r = e->alloc(&e->crosses, (K - 1) * B2 * B)) || (r = e->alloc(&e->kdiag, K * B2 * kb)) ||
-      (r = e->alloc(&e->koff, (K - 1) * B2 * kb)) || (r = e->alloc(&e->info, K * n * B)) ||
+  const int64_t B = nplans, K = nknots, N2 = (int64_t)n * n, T = e->T, kb = e->kb();
+  const int64_t scr = std::max(step_scratch_doubles(nplans, K, n, lanes), K * T * B);
+  if ((r = e->alloc(&e->mean, K * n * B)) || (r = e->alloc(&e->diag, K * T * B)) ||
+      (r = e->alloc(&e->off, (K - 1) * N2 * B)) || (r = e->alloc(&e->covs, K * T * B)) ||
+      (r = e->alloc(&e->crosses, (K - 1) * N2 * B)) || (r = e->alloc(&e->kdiag, K * T * kb)) ||
+      (r = e->alloc(&e->koff, (K - 1) * N2 * kb)) || (r = e->alloc(&e->info, K * n * B)) ||
       (r = e->alloc(&e->pmean, K * n * B)) || (r = e->alloc(&e->gmu, K * n * B)) ||
-      (r = e->alloc(&e->gdiag, K * B2 * B)) ||
+      (r = e->alloc(&e->gdiag, K * T * B)) || (r = e->alloc(&e->v, K * n * B)) ||
       (r = e->alloc(&e->epsi, std::max<int64_t>(K - 2, 1) * B)) ||
-      (r = e->alloc(&e->scratch, (size_t)chain_scratch_doubles(nplans, K, n, std::max(1, cfg->spec_lanes)))) ||
+      (r = e->alloc(&e->kfull_d, K * N2 * kb)) || (r = e->alloc(&e->scratch, (size_t)scr)) ||
       (r = e->alloc(&e->records, (size_t)cfg->max_iters * B * GVP_NREC)) ||
       (r = e->alloc(&e->scal, 9 * B)) || (r = e->alloc(&e->ints, 10 * B + 1)) ||
       (r = e->alloc(&e->oob, B)))
@@ -281,31 +325,33 @@ extern "C" int gvp_engine_create(gvp_engine** out, int32_t nplans, int64_t nknot
 
 extern "C" void gvp_engine_destroy(gvp_engine* e) { delete e; }
 
+// after kfull_d (full prior diag blocks), koff, info, pmean, mean are on device
 static int engine_reset(gvp_engine* e) {
-  const int64_t B = e->B, K = e->K, B2 = e->B2();
+  const int64_t B = e->B, K = e->K, T = e->T, N2 = (int64_t)e->n * e->n, kb = e->kb();
   cudaStream_t s = e->stream;
   // knots 0 and K-1 carry no factor: their gradient blocks stay zero
   GVP_CUDA(cudaMemsetAsync(e->gmu, 0, K * e->n * B * sizeof(double), s));
-  GVP_CUDA(cudaMemsetAsync(e->gdiag, 0, K * B2 * B * sizeof(double), s));
-  {
-    const int64_t cnt = (int64_t)e->cfg.max_iters * B * GVP_NREC;
-    fill_kernel<<<(unsigned)((cnt + 255) / 256), 256, 0, s>>>(e->records, cnt, NAN);
-  }
-  init_plans_kernel<<<(unsigned)((B + 127) / 128), 128, 0, s>>>((int)B, e->ps, e->cfg.temp_low);
-  const int64_t cd = K * B2, co = (K - 1) * B2;
-  const int64_t tot = (cd + co) * B;
-  init_prec_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(
-      cd, co, e->kdiag, e->koff, e->shared_prior ? 0 : 1, e->shared_prior ? 0 : 1, e->diag,
-      e->off, (int)B, 1.0 / e->cfg.init_cov_scale);
+  GVP_CUDA(cudaMemsetAsync(e->gdiag, 0, K * T * B * sizeof(double), s));
+  const int64_t cnt = (int64_t)e->cfg.max_iters * B * GVP_NREC;
+  fill_kernel<<<nblk(cnt, 256), 256, 0, s>>>(e->records, cnt, NAN);
+  init_plans_kernel<<<nblk(B, 128), 128, 0, s>>>((int)B, e->ps, e->cfg.temp_low);
+  // prior precision diag -> packed; initial_state (optimizer.py:280-296):
+  // Lambda_0 = K^{-1} / init_cov_scale, per plan
+  pack_sym_kernel<<<nblk(K * T * kb, 256), 256, 0, s>>>(K, e->n, kb, e->kfull_d, e->kdiag, 1.0);
+  const double inv_scale = 1.0 / e->cfg.init_cov_scale;
+  scale_copy_kernel<<<nblk(K * T * B, 256), 256, 0, s>>>(K * T * B, B, e->kdiag, e->shared_prior ? 0 : 1,
+                                                         e->diag, inv_scale);
+  scale_copy_kernel<<<nblk((K - 1) * N2 * B, 256), 256, 0, s>>>(
+      (K - 1) * N2 * B, B, e->koff, e->shared_prior ? 0 : 1, e->off, inv_scale);
   GVP_CUDA(cudaGetLastError());
-  // result.marginals = gbp_marginals(cur.prec) (optimizer.py:329) + log det
-  int r = launch_marginals((int)B, K, e->n, e->v(e->diag, B2), e->v(e->off, B2),
-                           e->mv(e->covs, B2), e->mv(e->crosses, B2), e->ps.logdet, e->ps.status,
-                           e->ps.where, e->scratch, nullptr, s);
+  // result.marginals = gbp_marginals(cur.prec) (optimizer.py:329) + log det, v = Lambda mu
+  int r = launch_marginals_packed((int)B, K, e->n, B, e->diag, e->off, e->covs, e->crosses,
+                                  e->ps.logdet, e->ps.status, e->ps.where, e->scratch, nullptr, s);
   if (r) return r;
+  if ((r = launch_lam_mu((int)B, K, e->n, B, e->diag, e->off, e->mean, e->v, s))) return r;
   // first factor sweep (optimizer.py:338-344)
   if ((r = e->factors())) return r;
-  e->launches += 3;
+  e->launches += 8;
   e->iters_launched = 0;
   if (e->graph) {
     cudaGraphExecDestroy(e->graph);
@@ -314,30 +360,29 @@ static int engine_reset(gvp_engine* e) {
   return GVP_OK;
 }
 
+static int engine_upload(gvp_engine* e, const double* kdiag, const double* koff,
+                         const double* info, const double* pm, const double* m0,
+                         cudaMemcpyKind kind) {
+  const int64_t B = e->B, K = e->K, N2 = (int64_t)e->n * e->n, kb = e->kb();
+  cudaStream_t s = e->stream;
+  GVP_CUDA(cudaMemcpyAsync(e->kfull_d, kdiag, K * N2 * kb * 8, kind, s));
+  GVP_CUDA(cudaMemcpyAsync(e->koff, koff, (K - 1) * N2 * kb * 8, kind, s));
+  GVP_CUDA(cudaMemcpyAsync(e->info, info, K * e->n * B * 8, kind, s));
+  GVP_CUDA(cudaMemcpyAsync(e->pmean, pm, K * e->n * B * 8, kind, s));
+  GVP_CUDA(cudaMemcpyAsync(e->mean, m0, K * e->n * B * 8, kind, s));
+  return engine_reset(e);
+}
+
 extern "C" int gvp_engine_load(gvp_engine* e, const double* kdiag, const double* koff,
                                const double* info, const double* prior_mean,
                                const double* init_mean) {
-  const int64_t B = e->B, K = e->K, B2 = e->B2(), kb = e->shared_prior ? 1 : B;
-  cudaStream_t s = e->stream;
-  GVP_CUDA(cudaMemcpyAsync(e->kdiag, kdiag, K * B2 * kb * sizeof(double), cudaMemcpyHostToDevice, s));
-  GVP_CUDA(cudaMemcpyAsync(e->koff, koff, (K - 1) * B2 * kb * sizeof(double), cudaMemcpyHostToDevice, s));
-  GVP_CUDA(cudaMemcpyAsync(e->info, info, K * e->n * B * sizeof(double), cudaMemcpyHostToDevice, s));
-  GVP_CUDA(cudaMemcpyAsync(e->pmean, prior_mean, K * e->n * B * sizeof(double), cudaMemcpyHostToDevice, s));
-  GVP_CUDA(cudaMemcpyAsync(e->mean, init_mean, K * e->n * B * sizeof(double), cudaMemcpyHostToDevice, s));
-  return engine_reset(e);
+  return engine_upload(e, kdiag, koff, info, prior_mean, init_mean, cudaMemcpyHostToDevice);
 }
 
 extern "C" int gvp_engine_load_dev(gvp_engine* e, const double* kdiag, const double* koff,
                                    const double* info, const double* prior_mean,
                                    const double* init_mean) {
-  const int64_t B = e->B, K = e->K, B2 = e->B2(), kb = e->shared_prior ? 1 : B;
-  cudaStream_t s = e->stream;
-  GVP_CUDA(cudaMemcpyAsync(e->kdiag, kdiag, K * B2 * kb * sizeof(double), cudaMemcpyDeviceToDevice, s));
-  GVP_CUDA(cudaMemcpyAsync(e->koff, koff, (K - 1) * B2 * kb * sizeof(double), cudaMemcpyDeviceToDevice, s));
-  GVP_CUDA(cudaMemcpyAsync(e->info, info, K * e->n * B * sizeof(double), cudaMemcpyDeviceToDevice, s));
-  GVP_CUDA(cudaMemcpyAsync(e->pmean, prior_mean, K * e->n * B * sizeof(double), cudaMemcpyDeviceToDevice, s));
-  GVP_CUDA(cudaMemcpyAsync(e->mean, init_mean, K * e->n * B * sizeof(double), cudaMemcpyDeviceToDevice, s));
-  return engine_reset(e);
+  return engine_upload(e, kdiag, koff, info, prior_mean, init_mean, cudaMemcpyDeviceToDevice);
 }
 
 extern "C" int gvp_engine_step(gvp_engine* e, int32_t iters, int32_t sync) {
@@ -363,38 +408,20 @@ extern "C" int gvp_engine_step(gvp_engine* e, int32_t iters, int32_t sync) {
   return GVP_OK;
 }
 
-// Same iterations as gvp_engine_step, launched kernel by kernel (no graph)
-// with CUDA events around each kernel on the engine stream; accumulates the
-// per-kernel device time (ms) over the iterations into ms[0..2] =
-// {select_step, factor_grads, control}.
 extern "C" int gvp_engine_step_profiled(gvp_engine* e, int32_t iters, double* ms) {
   cudaStream_t s = e->stream;
   cudaEvent_t ev[4];
   for (auto& x : ev) GVP_CUDA(cudaEventCreate(&x));
   double acc[3] = {0, 0, 0};
   for (int k = 0; k < iters && e->iters_launched < e->cfg.max_iters; ++k) {
-    StepProblem pb{e->v(e->mean, e->n), e->v(e->diag, e->B2()), e->v(e->off, e->B2()),
-                   e->kv(e->kdiag),     e->kv(e->koff),         e->v(e->info, e->n),
-                   e->v(e->gmu, e->n),  e->v(e->gdiag, e->B2()), e->v(e->gdiag, e->B2()),
-                   false,               e->v(e->pmean, e->n),   true};
-    StepParams pr{e->ps.temp, e->ps.logdet, e->cfg.kl_bound, e->cfg.beta_min, e->cfg.beta_max,
-                  std::max(1, e->cfg.spec_lanes), false, nullptr};
-    StepOut out{e->mv(e->mean, e->n),      e->mv(e->diag, e->B2()), e->mv(e->off, e->B2()),
-                e->mv(e->covs, e->B2()),   e->mv(e->crosses, e->B2()), e->ps.beta,
-                e->ps.kl,                  e->ps.logdet,            e->ps.shift,
-                e->ps.prior_cost,          nullptr,                 0,
-                nullptr,                   e->ps.status,            e->ps.where};
     GVP_CUDA(cudaEventRecord(ev[0], s));
-    int r = launch_select_step(e->B, e->K, e->n, pb, pr, out, e->scratch, e->ps.active, s);
+    int r = launch_select_step_v2(e->step_args(), s);
     if (r) return r;
+    ++e->launches;
     GVP_CUDA(cudaEventRecord(ev[1], s));
     if ((r = e->factors())) return r;
     GVP_CUDA(cudaEventRecord(ev[2], s));
-    const double ctol = e->cfg.collision_tol >= 0 ? e->cfg.collision_tol : 1e-4 * (double)(e->K - 1);
-    control_kernel<<<(e->B + 127) / 128, 128, 0, s>>>(
-        e->B, std::max<int64_t>(e->K - 2, 0), (int)(e->K * e->n), e->epsi, e->ps, e->records,
-        e->cfg.max_iters, e->cfg.temp_high, e->cfg.tol_mean, e->cfg.tol_cost, ctol);
-    GVP_CUDA(cudaGetLastError());
+    if ((r = e->control())) return r;
     GVP_CUDA(cudaEventRecord(ev[3], s));
     GVP_CUDA(cudaEventSynchronize(ev[3]));
     for (int j = 0; j < 3; ++j) {
@@ -402,7 +429,6 @@ extern "C" int gvp_engine_step_profiled(gvp_engine* e, int32_t iters, double* ms
       GVP_CUDA(cudaEventElapsedTime(&t, ev[j], ev[j + 1]));
       acc[j] += t;
     }
-    e->launches += 2;  // select + control (factors() counted itself)
     ++e->iters_launched;
   }
   for (auto& x : ev) cudaEventDestroy(x);
@@ -419,7 +445,7 @@ extern "C" int gvp_engine_sync(gvp_engine* e) {
 
 extern "C" int gvp_engine_active(gvp_engine* e, int32_t* nactive) {
   GVP_CUDA(cudaMemsetAsync(e->ps.nactive, 0, sizeof(int), e->stream));
-  count_active_kernel<<<(e->B + 127) / 128, 128, 0, e->stream>>>(e->B, e->ps.active, e->ps.nactive);
+  count_active_kernel<<<nblk(e->B, 128), 128, 0, e->stream>>>(e->B, e->ps.active, e->ps.nactive);
   GVP_CUDA(cudaGetLastError());
   GVP_CUDA(cudaMemcpyAsync(nactive, e->ps.nactive, sizeof(int), cudaMemcpyDeviceToHost, e->stream));
   GVP_CUDA(cudaStreamSynchronize(e->stream));
@@ -427,16 +453,39 @@ extern "C" int gvp_engine_active(gvp_engine* e, int32_t* nactive) {
   return GVP_OK;
 }
 
+// packed (K, T, B) device -> full (K, n, n, B) host
+static int fetch_sym(gvp_engine* e, double* host, const double* dev) {
+  const int64_t B = e->B, K = e->K, T = e->T, n = e->n;
+  std::vector<double> tmp((size_t)(K * T * B));
+  GVP_CUDA(cudaMemcpyAsync(tmp.data(), dev, tmp.size() * 8, cudaMemcpyDeviceToHost, e->stream));
+  GVP_CUDA(cudaStreamSynchronize(e->stream));
+  for (int64_t i = 0; i < K; ++i)
+    for (int64_t r = 0; r < n; ++r)
+      for (int64_t c = 0; c <= r; ++c) {
+        const double* src = &tmp[(size_t)((i * T + r * (r + 1) / 2 + c) * B)];
+        double* d1 = host + ((i * n + r) * n + c) * B;
+        double* d2 = host + ((i * n + c) * n + r) * B;
+        for (int64_t b = 0; b < B; ++b) d1[b] = d2[b] = src[b];
+      }
+  return GVP_OK;
+}
+
 extern "C" int gvp_engine_get_state(gvp_engine* e, double* mean, double* diag, double* off,
                                     double* covs, double* crosses) {
-  const int64_t B = e->B, K = e->K, B2 = e->B2();
+  const int64_t B = e->B, K = e->K, N2 = (int64_t)e->n * e->n;
   cudaStream_t s = e->stream;
   if (mean) GVP_CUDA(cudaMemcpyAsync(mean, e->mean, K * e->n * B * 8, cudaMemcpyDeviceToHost, s));
-  if (diag) GVP_CUDA(cudaMemcpyAsync(diag, e->diag, K * B2 * B * 8, cudaMemcpyDeviceToHost, s));
-  if (off) GVP_CUDA(cudaMemcpyAsync(off, e->off, (K - 1) * B2 * B * 8, cudaMemcpyDeviceToHost, s));
-  if (covs) GVP_CUDA(cudaMemcpyAsync(covs, e->covs, K * B2 * B * 8, cudaMemcpyDeviceToHost, s));
-  if (crosses) GVP_CUDA(cudaMemcpyAsync(crosses, e->crosses, (K - 1) * B2 * B * 8, cudaMemcpyDeviceToHost, s));
+  if (off) GVP_CUDA(cudaMemcpyAsync(off, e->off, (K - 1) * N2 * B * 8, cudaMemcpyDeviceToHost, s));
+  if (crosses) GVP_CUDA(cudaMemcpyAsync(crosses, e->crosses, (K - 1) * N2 * B * 8, cudaMemcpyDeviceToHost, s));
   GVP_CUDA(cudaStreamSynchronize(s));
+  if (diag) {
+    int r = fetch_sym(e, diag, e->diag);
+    if (r) return r;
+  }
+  if (covs) {
+    int r = fetch_sym(e, covs, e->covs);
+    if (r) return r;
+  }
   return GVP_OK;
 }
 
@@ -471,4 +520,4 @@ extern "C" int gvp_engine_device_state(gvp_engine* e, double** mean, double** di
 }
 
 extern "C" int64_t gvp_engine_launches(gvp_engine* e) { return e->launches; }
-
+extern "C" int32_t gvp_engine_lanes(gvp_engine* e) { return e->lanes; }

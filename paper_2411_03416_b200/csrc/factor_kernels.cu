@@ -366,7 +366,7 @@ factor_grads_kernel(int nplans, int64_t nfac, View mean, View covs, RuleDev R, F
 #pragma unroll
   for (int r = 0; r < N; ++r)
 #pragma unroll
-    for (int c = 0; c <= r; ++c) S[r][c] = covs(b, knot, r * N + c);
+    for (int c = 0; c <= r; ++c) S[r][c] = covs(b, knot, tri_idx(r, c));  // packed lower
   // gaussian_sqrt (quadrature.py:164-177): Cholesky, then one 1e-10 jitter retry
   // np.linalg.cholesky has no 1e-300 pivot floor: FLOOR=false
   bool ok = chol<N, false>(S, L);
@@ -457,9 +457,7 @@ factor_grads_kernel(int nplans, int64_t nfac, View mean, View covs, RuleDev R, F
         hp += Li[k][r] * W[k][c];
         pp += Li[k][r] * Li[k][c];
       }
-      const double g = h0 * pp + 0.5 * hp;
-      out.g_diag(b, knot, r * N + c) = g;
-      if (c != r) out.g_diag(b, knot, c * N + r) = g;
+      out.g_diag(b, knot, tri_idx(r, c)) = h0 * pp + 0.5 * hp;  // packed lower
     }
   out.e_psi(b, f, 0) = e0 > 0.0 ? e0 : 0.0;  // e_psi = max(e0, 0) (factors.py:218-224)
 }

@@ -131,4 +131,36 @@ int launch_select_step(int nplans, int64_t K, int n, const StepProblem& pb, cons
                        const StepOut& out, double* scratch, const int* active, cudaStream_t s);
 int64_t chain_scratch_doubles(int nplans, int64_t K, int n, int lanes);
 
+// ---- step kernel v2 (step_kernel.cu): plan-minor arrays with plan stride Bp,
+// diagonal blocks packed lower-symmetric (n(n+1)/2 entries), off blocks full.
+struct V2Launch {
+  int nplans;
+  int64_t K;
+  int n;
+  int64_t Bp;
+  int lanes;
+  const double *ld, *lo, *kd, *ko, *gd, *g, *eta, *v, *mu, *pmean;
+  bool kshared;
+  double *o_mu, *o_ld, *o_lo, *o_cov, *o_cr, *o_v;
+  double *beta, *kl, *ld_next, *shift, *prior_cost;
+  const double* temp;
+  const double* ld_cur;
+  double kl_bound, beta_min, beta_max;
+  int *status, *where;
+  double* probe_log;
+  int max_probes;
+  int* nprobes;
+  double* scratch;
+  const int* active;
+};
+int launch_select_step_v2(const V2Launch& q, cudaStream_t s);
+int64_t step_scratch_doubles(int nplans, int64_t K, int n, int lanes);
+// packed-layout helpers (step_kernel.cu)
+int launch_marginals_packed(int nplans, int64_t K, int n, int64_t Bp, const double* ld,
+                            const double* lo, double* cov, double* cr, double* logdet,
+                            int* status, int* where, double* scratch, const int* active,
+                            cudaStream_t s);
+int launch_lam_mu(int nplans, int64_t K, int n, int64_t Bp, const double* ld, const double* lo,
+                  const double* mu, double* v, cudaStream_t s);
+
 }  // namespace gvp

@@ -43,7 +43,7 @@ def far_field() -> SignedDistanceField:
 class PlanBatch:
     def __init__(self, nplans: int, nknots: int, n: int, sdf: SignedDistanceField,
                  model: CollisionModel, rule: QuadratureRule, cfg, shared_prior: bool = True,
-                 spec_lanes: int = 1):
+                 spec_lanes: int = 0):
         self.lib = N.load()
         self.B, self.K, self.n = int(nplans), int(nknots), int(n)
         self.shared_prior = bool(shared_prior)
@@ -137,6 +137,9 @@ class PlanBatch:
                 break
         self.sync()
         return done
+
+    def lanes(self) -> int:
+        return int(self.lib.gvp_engine_lanes(self.handle))
 
     def launches(self) -> int:
         return int(self.lib.gvp_engine_launches(self.handle))

@@ -264,7 +264,7 @@ def _raise_plan_status(status: int, where: int, cfg: OptimizerConfig):
 
 def run_pgvimp(sys_ltv: LTVSystem, env: Environment | None, cfg: OptimizerConfig, x0, goal,
                q_c: float, sigma_b: float, prior: DiscretePrior | None = None,
-               spec_lanes: int = 1) -> RunResult:
+               spec_lanes: int = 0) -> RunResult:
     """Algorithm 1 (optimizer.py:299-401) on the GPU engine."""
     cfg.validate()
     t0 = time.perf_counter()
@@ -315,7 +315,7 @@ class BatchResult:
 
 
 def run_pgvimp_batch(sys_ltv: LTVSystem, env: Environment | None, cfg: OptimizerConfig, x0s, goals,
-                     q_c: float, sigma_b: float, spec_lanes: int = 1) -> BatchResult:
+                     q_c: float, sigma_b: float, spec_lanes: int = 0) -> BatchResult:
     """Many independent plans on one GPU: same system, map and settings, per
     plan start/goal (SURVEY.md §8-e batch axis). Plans that fail are masked
     out with their status; the batch never aborts."""
