@@ -125,7 +125,7 @@ static bool all_zero(const double* p, int64_t count) {
     if (p[k] != 0.0) return false;
   return true;
 }
-static int g_step_lanes = 32;  // candidate lanes of the drop-in select_step_size (one plan)
+static int g_step_lanes = 16;  // candidate lanes of the drop-in select_step_size (one plan)
 
 static int check_n(int n) {
   if (n < 1 || n > 8) {
@@ -522,8 +522,8 @@ static int select_step_size_v1(const double* mean, const double* diag, const dou
 }
 
 extern "C" int gvp_set_step_lanes(int32_t lanes) {
-  if (lanes != 1 && lanes != 4 && lanes != 8 && lanes != 16 && lanes != 32) {
-    set_error("lanes must be 1, 4, 8, 16 or 32");
+  if (lanes != 1 && lanes != 4 && lanes != 8 && lanes != 16) {
+    set_error("lanes must be 1, 4, 8 or 16");
     return GVP_ERR_ARG;
   }
   g_step_lanes = lanes;
@@ -550,48 +550,63 @@ extern "C" int gvp_select_step_size(const double* mean, const double* diag, cons
     return select_step_size_v1(mean, diag, off, kdiag, koff, info, g_mu, gdiag, goff, nblocks, n,
                                temp, kl_bound, beta_min, beta_max, beta, kl, out_mean, out_diag,
                                out_off, covs, crosses, probe_log, max_probes, nprobes, where);
-  // ---- v2: packed layout, speculative bisection lanes (step_kernel.cu)
+  // ---- packed layout, TMA-staged step kernel with speculative lanes (step_tma.cu).
+  // The step kernel wants an even plan stride: the plan goes in column 0 of
+  // 2-wide arrays (column 1 is a copy), the prior is the 2-wide shared prior.
   cudaStream_t s = C.stream;
   const int T = n * (n + 1) / 2;
   const int L = g_step_lanes;
+  auto wide = [](const double* src, int64_t rows) {
+    std::vector<double> w((size_t)(2 * rows));
+    for (int64_t r = 0; r < rows; ++r) w[2 * r] = w[2 * r + 1] = src[r];
+    return w;
+  };
   const std::vector<double> ld_p = pack_lower(diag, K, n), kd_p = pack_lower(kdiag, K, n),
                             gd_p = pack_lower(gdiag, K, n);
   double *ld, *lo, *kd, *ko, *gd, *g, *eta, *v, *mu, *omu, *old_, *olo, *ocov, *ocr, *ov, *scal,
       *plog, *scr;
   int* st;
   const int64_t K1a = std::max<int64_t>(K1, 1);
-  GVP_TRY(C.arena.get(40, K * T, &ld));
-  GVP_TRY(C.arena.get(41, K1a * N2, &lo));
-  GVP_TRY(C.arena.get(42, K * T, &kd));
-  GVP_TRY(C.arena.get(43, K1a * N2, &ko));
-  GVP_TRY(C.arena.get(44, K * T, &gd));
-  GVP_TRY(C.arena.get(45, K * n, &g));
-  GVP_TRY(C.arena.get(46, K * n, &eta));
-  GVP_TRY(C.arena.get(47, K * n, &v));
-  GVP_TRY(C.arena.get(48, K * n, &mu));
-  GVP_TRY(C.arena.get(49, K * n, &omu));
-  GVP_TRY(C.arena.get(50, K * T, &old_));
-  GVP_TRY(C.arena.get(51, K1a * N2, &olo));
-  GVP_TRY(C.arena.get(52, K * T, &ocov));
-  GVP_TRY(C.arena.get(53, K1a * N2, &ocr));
-  GVP_TRY(C.arena.get(54, K * n, &ov));
-  GVP_TRY(C.arena.get(55, 8, &scal));
-  GVP_TRY(C.arena.get(56, std::max(max_probes, 1) * 3, &plog));
-  GVP_TRY(C.arena.get(57, (size_t)std::max(step_scratch_doubles(1, K, n, L), K * T), &scr));
-  GVP_TRY(C.arena.get(58, 4, &st));
-  GVP_TRY(h2d(ld, ld_p.data(), K * T, s));
-  GVP_TRY(h2d(lo, off, K1 * N2, s));
-  GVP_TRY(h2d(kd, kd_p.data(), K * T, s));
-  GVP_TRY(h2d(ko, koff, K1 * N2, s));
-  GVP_TRY(h2d(gd, gd_p.data(), K * T, s));
-  GVP_TRY(h2d(g, g_mu, K * n, s));
-  GVP_TRY(h2d(eta, info, K * n, s));
-  GVP_TRY(h2d(mu, mean, K * n, s));
-  GVP_TRY(h2d(scal + 4, &temp, 1, s));
+  GVP_TRY(C.arena.get(40, 2 * K * T, &ld));
+  GVP_TRY(C.arena.get(41, 2 * K1a * N2, &lo));
+  GVP_TRY(C.arena.get(42, 2 * K * T, &kd));
+  GVP_TRY(C.arena.get(43, 2 * K1a * N2, &ko));
+  GVP_TRY(C.arena.get(44, 2 * K * T, &gd));
+  GVP_TRY(C.arena.get(45, 2 * K * n, &g));
+  GVP_TRY(C.arena.get(46, 2 * K * n, &eta));
+  GVP_TRY(C.arena.get(47, 2 * K * n, &v));
+  GVP_TRY(C.arena.get(48, 2 * K * n, &mu));
+  GVP_TRY(C.arena.get(49, 2 * K * n, &omu));
+  GVP_TRY(C.arena.get(50, 2 * K * T, &old_));
+  GVP_TRY(C.arena.get(51, 2 * K1a * N2, &olo));
+  GVP_TRY(C.arena.get(52, 2 * K * T, &ocov));
+  GVP_TRY(C.arena.get(53, 2 * K1a * N2, &ocr));
+  GVP_TRY(C.arena.get(54, 2 * K * n, &ov));
+  GVP_TRY(C.arena.get(55, 16, &scal));
+  GVP_TRY(C.arena.get(56, std::max(max_probes, 1) * 3 * 2, &plog));
+  GVP_TRY(C.arena.get(57, (size_t)std::max(step_scratch_doubles(2, K, n, L), 2 * K * T), &scr));
+  GVP_TRY(C.arena.get(58, 8, &st));
+  {
+    const auto w_ld = wide(ld_p.data(), K * T), w_lo = wide(off, K1 * N2),
+               w_kd = wide(kd_p.data(), K * T), w_ko = wide(koff, K1 * N2),
+               w_gd = wide(gd_p.data(), K * T), w_g = wide(g_mu, K * n), w_eta = wide(info, K * n),
+               w_mu = wide(mean, K * n);
+    GVP_TRY(h2d(ld, w_ld.data(), w_ld.size(), s));
+    GVP_TRY(h2d(lo, w_lo.data(), w_lo.size(), s));
+    GVP_TRY(h2d(kd, w_kd.data(), w_kd.size(), s));
+    GVP_TRY(h2d(ko, w_ko.data(), w_ko.size(), s));
+    GVP_TRY(h2d(gd, w_gd.data(), w_gd.size(), s));
+    GVP_TRY(h2d(g, w_g.data(), w_g.size(), s));
+    GVP_TRY(h2d(eta, w_eta.data(), w_eta.size(), s));
+    GVP_TRY(h2d(mu, w_mu.data(), w_mu.size(), s));
+    const double tt[2] = {temp, temp};
+    GVP_TRY(h2d(scal + 8, tt, 2, s));
+    GVP_CUDA(cudaStreamSynchronize(s));
+  }
   // rhs piece Lambda mu, and log det of the current precision from the same
   // backward Schur pivots the probes use (consistent KL)
-  GVP_TRY(launch_lam_mu(1, K, n, 1, ld, lo, mu, v, s));
-  GVP_TRY(launch_marginals_packed(1, K, n, 1, ld, lo, ocov, ocr, scal + 5, st, st + 1, scr,
+  GVP_TRY(launch_lam_mu(2, K, n, 2, ld, lo, mu, v, s));
+  GVP_TRY(launch_marginals_packed(1, K, n, 2, ld, lo, ocov, ocr, scal + 10, st, st + 1, scr,
                                   nullptr, s));
   int64_t w0 = -1;
   if (fetch_status(C, st, &w0) != GVP_OK) {
@@ -600,20 +615,21 @@ extern "C" int gvp_select_step_size(const double* mean, const double* diag, cons
     return GVP_ERR_NOT_SPD;
   }
   V2Launch q{};
-  q.nplans = 1; q.K = K; q.n = n; q.Bp = 1; q.lanes = L;
+  q.nplans = 1; q.K = K; q.n = n; q.Bp = 2; q.lanes = L;
   q.ld = ld; q.lo = lo; q.kd = kd; q.ko = ko; q.gd = gd; q.g = g; q.eta = eta; q.v = v;
-  q.mu = mu; q.pmean = mu; q.kshared = false;
+  q.mu = mu; q.pmean = mu; q.kshared = true;
   q.o_mu = omu; q.o_ld = old_; q.o_lo = olo; q.o_cov = ocov; q.o_cr = ocr; q.o_v = ov;
-  q.beta = scal; q.kl = scal + 1; q.ld_next = scal + 2; q.shift = scal + 3; q.prior_cost = nullptr;
-  q.temp = scal + 4; q.ld_cur = scal + 5;
+  q.beta = scal; q.kl = scal + 2; q.ld_next = scal + 4; q.shift = scal + 6; q.prior_cost = nullptr;
+  q.temp = scal + 8; q.ld_cur = scal + 10;
   q.kl_bound = kl_bound; q.beta_min = beta_min; q.beta_max = beta_max;
-  q.status = st; q.where = st + 1;
-  q.probe_log = probe_log ? plog : nullptr; q.max_probes = max_probes; q.nprobes = st + 2;
+  q.status = st; q.where = st + 2;
+  q.probe_log = probe_log ? plog : nullptr; q.max_probes = max_probes; q.nprobes = st + 4;
   q.scratch = scr; q.active = nullptr;
   GVP_TRY(launch_select_step_v2(q, s));
-  int stw[3];
-  GVP_TRY(d2h(stw, st, 3, s));
+  int stv[5];
+  GVP_TRY(d2h(stv, st, 5, s));
   GVP_CUDA(cudaStreamSynchronize(s));
+  const int stw[3] = {stv[0], stv[2], stv[4]};
   if (nprobes) *nprobes = stw[2];
   if (probe_log && stw[2] > 0) {
     GVP_TRY(d2h(probe_log, plog, (size_t)std::min(stw[2], max_probes) * 3, s));
@@ -632,19 +648,24 @@ extern "C" int gvp_select_step_size(const double* mean, const double* diag, cons
     }
     return stw[0];
   }
-  double sc[2];
+  double sc[4];
   std::vector<double> ldo((size_t)(K * T)), covo((size_t)(K * T));
-  GVP_TRY(d2h(sc, scal, 2, s));
-  GVP_TRY(d2h(out_mean, omu, K * n, s));
-  GVP_TRY(d2h(ldo.data(), old_, K * T, s));
-  GVP_TRY(d2h(out_off, olo, K1 * N2, s));
-  GVP_TRY(d2h(covo.data(), ocov, K * T, s));
-  GVP_TRY(d2h(crosses, ocr, K1 * N2, s));
+  auto narrow = [&](double* dst, const double* src, int64_t rows) -> int {
+    if (rows > 0)
+      GVP_CUDA(cudaMemcpy2DAsync(dst, 8, src, 16, 8, rows, cudaMemcpyDeviceToHost, s));
+    return GVP_OK;
+  };
+  GVP_TRY(d2h(sc, scal, 4, s));
+  GVP_TRY(narrow(out_mean, omu, K * n));
+  GVP_TRY(narrow(ldo.data(), old_, K * T));
+  GVP_TRY(narrow(out_off, olo, K1 * N2));
+  GVP_TRY(narrow(covo.data(), ocov, K * T));
+  GVP_TRY(narrow(crosses, ocr, K1 * N2));
   GVP_CUDA(cudaStreamSynchronize(s));
   unpack_sym(ldo.data(), K, n, out_diag);
   unpack_sym(covo.data(), K, n, covs);
   *beta = sc[0];
-  *kl = sc[1];
+  *kl = sc[2];
   if (where) *where = -1;
   return GVP_OK;
 }

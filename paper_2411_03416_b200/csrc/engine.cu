@@ -55,24 +55,27 @@ __global__ void init_plans_kernel(int B, PlanState ps, double temp_low) {
   ps.oob[b] = 0;
 }
 
-// full (K, n, n, kb) -> packed (K, T, kb) times `scale`
-__global__ void pack_sym_kernel(int64_t K, int n, int64_t kb, const double* __restrict__ src,
-                                double* __restrict__ dst, double scale) {
+// full (K, n, n, sw) -> packed (K, T, dw) times `scale`; a shared prior
+// (sw = 1) is written to both columns of its 2-wide copy (dw = 2)
+__global__ void pack_sym_kernel(int64_t K, int n, int64_t sw, int64_t dw,
+                                const double* __restrict__ src, double* __restrict__ dst,
+                                double scale) {
   const int T = n * (n + 1) / 2;
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= K * T * kb) return;
-  const int64_t b = t % kb, q = (t / kb) % T, i = t / (kb * T);
+  if (t >= K * T * dw) return;
+  const int64_t b = t % dw, q = (t / dw) % T, i = t / (dw * T);
   int r = 0;
   while ((r + 1) * (r + 2) / 2 <= q) ++r;
   const int c = (int)q - r * (r + 1) / 2;
-  dst[t] = src[((i * n + r) * n + c) * kb + b] * scale;
+  dst[t] = src[((i * n + r) * n + c) * sw + (sw == 1 ? 0 : b)] * scale;
 }
-// broadcast a shared (K, E) array to per-plan (K, E, B) times `scale`
-__global__ void scale_copy_kernel(int64_t count, int64_t B, const double* __restrict__ src,
-                                  int64_t src_sp, double* __restrict__ dst, double scale) {
+// dst (rows, Bp) = src (rows, sw) times `scale`; sw = 2 (shared, column 0) or Bp
+__global__ void scale_copy_kernel(int64_t count, int64_t Bp, const double* __restrict__ src,
+                                  int64_t sw, double* __restrict__ dst, double scale) {
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= count) return;
-  dst[t] = (src_sp ? src[t] : src[t / B]) * scale;
+  const int64_t row = t / Bp, b = t % Bp;
+  dst[t] = src[row * sw + (sw == Bp ? b : 0)] * scale;
 }
 
 __global__ void control_kernel(int B, int64_t F, int n64dim, const double* __restrict__ epsi,
@@ -146,7 +149,8 @@ inline unsigned nblk(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
 }  // namespace
 
 struct gvp_engine {
-  int B = 0;
+  int B = 0;        // plans on device (even: the step kernel's TMA boxes need a 16-B plan stride)
+  int nreal = 0;    // plans of the caller; an odd count is padded with a copy of plan 0
   int64_t K = 0;
   int n = 0, T = 0;
   bool shared_prior = false;
@@ -184,7 +188,7 @@ struct gvp_engine {
     for (void* p : allocs) cudaFree(p);
     if (stream) cudaStreamDestroy(stream);
   }
-  int64_t kb() const { return shared_prior ? 1 : B; }
+  int64_t kb() const { return shared_prior ? 2 : B; }  // prior columns (2-wide when shared)
   View vw(const double* p, int64_t E) const { return View{p, E * B, B, 1}; }
   MutView mvw(double* p, int64_t E) const { return MutView{p, E * B, B, 1}; }
 
@@ -240,7 +244,7 @@ static int pick_lanes(const gvp_plan_config* cfg, int B) {
   if (cfg->spec_lanes > 0) return cfg->spec_lanes;
   // fill the GPU: ~2 warps per SM of candidate lanes, at most 32 per plan
   int L = 1;
-  while (L < 32 && (int64_t)B * L < 148 * 64) L *= 2;
+  while (L < 16 && (int64_t)B * L * 2 < 148 * 64) L *= 2;
   if (L == 2) L = 4;
   return L;
 }
@@ -266,8 +270,8 @@ extern "C" int gvp_engine_create(gvp_engine** out, int32_t nplans, int64_t nknot
     return GVP_ERR_ARG;
   }
   const int lanes = pick_lanes(cfg, nplans);
-  if (lanes != 1 && lanes != 4 && lanes != 8 && lanes != 16 && lanes != 32) {
-    set_error("spec_lanes must be 0 (auto), 1, 4, 8, 16 or 32");
+  if (lanes != 1 && lanes != 4 && lanes != 8 && lanes != 16) {
+    set_error("spec_lanes must be 0 (auto), 1, 4, 8 or 16");
     return GVP_ERR_ARG;
   }
   int ndev = 0;
@@ -277,7 +281,8 @@ extern "C" int gvp_engine_create(gvp_engine** out, int32_t nplans, int64_t nknot
     return GVP_ERR_NO_DEVICE;
   }
   auto* e = new gvp_engine();
-  e->B = nplans;
+  e->nreal = nplans;
+  e->B = (int)step_plan_stride(nplans);
   e->K = nknots;
   e->n = n;
   e->T = n * (n + 1) / 2;
@@ -296,8 +301,8 @@ extern "C" int gvp_engine_create(gvp_engine** out, int32_t nplans, int64_t nknot
   if ((r = e->field.build(grid, grid_ndim, grid_shape, origin, cell_size, e->stream))) return fail(r);
   if (grid_ndim > n) return set_error("grid dim exceeds state dim"), fail(GVP_ERR_ARG);
   if ((r = e->rule.build(points, weights, npts, n, grid_ndim, e->stream))) return fail(r);
-  const int64_t B = nplans, K = nknots, N2 = (int64_t)n * n, T = e->T, kb = e->kb();
-  const int64_t scr = std::max(step_scratch_doubles(nplans, K, n, lanes), K * T * B);
+  const int64_t B = e->B, K = nknots, N2 = (int64_t)n * n, T = e->T, kb = e->kb();
+  const int64_t scr = std::max(step_scratch_doubles(e->B, K, n, lanes), K * T * B);
   if ((r = e->alloc(&e->mean, K * n * B)) || (r = e->alloc(&e->diag, K * T * B)) ||
       (r = e->alloc(&e->off, (K - 1) * N2 * B)) || (r = e->alloc(&e->covs, K * T * B)) ||
       (r = e->alloc(&e->crosses, (K - 1) * N2 * B)) || (r = e->alloc(&e->kdiag, K * T * kb)) ||
@@ -337,12 +342,13 @@ static int engine_reset(gvp_engine* e) {
   init_plans_kernel<<<nblk(B, 128), 128, 0, s>>>((int)B, e->ps, e->cfg.temp_low);
   // prior precision diag -> packed; initial_state (optimizer.py:280-296):
   // Lambda_0 = K^{-1} / init_cov_scale, per plan
-  pack_sym_kernel<<<nblk(K * T * kb, 256), 256, 0, s>>>(K, e->n, kb, e->kfull_d, e->kdiag, 1.0);
+  pack_sym_kernel<<<nblk(K * T * kb, 256), 256, 0, s>>>(K, e->n, e->shared_prior ? 1 : B, kb,
+                                                        e->kfull_d, e->kdiag, 1.0);
   const double inv_scale = 1.0 / e->cfg.init_cov_scale;
-  scale_copy_kernel<<<nblk(K * T * B, 256), 256, 0, s>>>(K * T * B, B, e->kdiag, e->shared_prior ? 0 : 1,
-                                                         e->diag, inv_scale);
-  scale_copy_kernel<<<nblk((K - 1) * N2 * B, 256), 256, 0, s>>>(
-      (K - 1) * N2 * B, B, e->koff, e->shared_prior ? 0 : 1, e->off, inv_scale);
+  scale_copy_kernel<<<nblk(K * T * B, 256), 256, 0, s>>>(K * T * B, B, e->kdiag, kb, e->diag,
+                                                         inv_scale);
+  scale_copy_kernel<<<nblk((K - 1) * N2 * B, 256), 256, 0, s>>>((K - 1) * N2 * B, B, e->koff, kb,
+                                                                e->off, inv_scale);
   GVP_CUDA(cudaGetLastError());
   // result.marginals = gbp_marginals(cur.prec) (optimizer.py:329) + log det, v = Lambda mu
   int r = launch_marginals_packed((int)B, K, e->n, B, e->diag, e->off, e->covs, e->crosses,
@@ -363,14 +369,34 @@ static int engine_reset(gvp_engine* e) {
 static int engine_upload(gvp_engine* e, const double* kdiag, const double* koff,
                          const double* info, const double* pm, const double* m0,
                          cudaMemcpyKind kind) {
-  const int64_t B = e->B, K = e->K, N2 = (int64_t)e->n * e->n, kb = e->kb();
+  const int64_t K = e->K, N2 = (int64_t)e->n * e->n;
   cudaStream_t s = e->stream;
-  GVP_CUDA(cudaMemcpyAsync(e->kfull_d, kdiag, K * N2 * kb * 8, kind, s));
-  GVP_CUDA(cudaMemcpyAsync(e->koff, koff, (K - 1) * N2 * kb * 8, kind, s));
-  GVP_CUDA(cudaMemcpyAsync(e->info, info, K * e->n * B * 8, kind, s));
-  GVP_CUDA(cudaMemcpyAsync(e->pmean, pm, K * e->n * B * 8, kind, s));
-  GVP_CUDA(cudaMemcpyAsync(e->mean, m0, K * e->n * B * 8, kind, s));
+  // caller layout (rows, nreal) -> device (rows, B); a padding column is a copy of plan 0
+  auto put = [&](double* dst, const double* src, int64_t rows) -> int {
+    const size_t sp = (size_t)e->nreal * 8, dp = (size_t)e->B * 8;
+    GVP_CUDA(cudaMemcpy2DAsync(dst, dp, src, sp, sp, rows, kind, s));
+    if (e->B > e->nreal) GVP_CUDA(cudaMemcpy2DAsync(dst + e->nreal, dp, src, sp, 8, rows, kind, s));
+    return GVP_OK;
+  };
+  int r;
+  if (e->shared_prior) {
+    GVP_CUDA(cudaMemcpyAsync(e->kfull_d, kdiag, K * N2 * 8, kind, s));
+    for (int col = 0; col < 2; ++col)  // 2-wide copy of the shared off blocks
+      GVP_CUDA(cudaMemcpy2DAsync(e->koff + col, 16, koff, 8, 8, (K - 1) * N2, kind, s));
+  } else {
+    if ((r = put(e->kfull_d, kdiag, K * N2)) || (r = put(e->koff, koff, (K - 1) * N2))) return r;
+  }
+  if ((r = put(e->info, info, K * e->n)) || (r = put(e->pmean, pm, K * e->n)) ||
+      (r = put(e->mean, m0, K * e->n)))
+    return r;
   return engine_reset(e);
+}
+
+// device (rows, B) -> caller (rows, nreal)
+static int get_cols(gvp_engine* e, double* dst, const double* src, int64_t rows) {
+  const size_t sp = (size_t)e->B * 8, dp = (size_t)e->nreal * 8;
+  GVP_CUDA(cudaMemcpy2DAsync(dst, dp, src, sp, dp, rows, cudaMemcpyDeviceToHost, e->stream));
+  return GVP_OK;
 }
 
 extern "C" int gvp_engine_load(gvp_engine* e, const double* kdiag, const double* koff,
@@ -387,7 +413,14 @@ extern "C" int gvp_engine_load_dev(gvp_engine* e, const double* kdiag, const dou
 
 extern "C" int gvp_engine_step(gvp_engine* e, int32_t iters, int32_t sync) {
   cudaStream_t s = e->stream;
+  static const bool no_graph = std::getenv("GVP_NO_GRAPH") != nullptr;
   for (int k = 0; k < iters && e->iters_launched < e->cfg.max_iters; ++k) {
+    if (no_graph) {  // debugging aid: plain launches
+      int r = e->iteration_body();
+      if (r) return r;
+      ++e->iters_launched;
+      continue;
+    }
     if (!e->graph) {
       cudaGraph_t g;
       GVP_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
@@ -445,7 +478,7 @@ extern "C" int gvp_engine_sync(gvp_engine* e) {
 
 extern "C" int gvp_engine_active(gvp_engine* e, int32_t* nactive) {
   GVP_CUDA(cudaMemsetAsync(e->ps.nactive, 0, sizeof(int), e->stream));
-  count_active_kernel<<<nblk(e->B, 128), 128, 0, e->stream>>>(e->B, e->ps.active, e->ps.nactive);
+  count_active_kernel<<<nblk(e->nreal, 128), 128, 0, e->stream>>>(e->nreal, e->ps.active, e->ps.nactive);
   GVP_CUDA(cudaGetLastError());
   GVP_CUDA(cudaMemcpyAsync(nactive, e->ps.nactive, sizeof(int), cudaMemcpyDeviceToHost, e->stream));
   GVP_CUDA(cudaStreamSynchronize(e->stream));
@@ -455,9 +488,10 @@ extern "C" int gvp_engine_active(gvp_engine* e, int32_t* nactive) {
 
 // packed (K, T, B) device -> full (K, n, n, B) host
 static int fetch_sym(gvp_engine* e, double* host, const double* dev) {
-  const int64_t B = e->B, K = e->K, T = e->T, n = e->n;
+  const int64_t B = e->nreal, K = e->K, T = e->T, n = e->n;
   std::vector<double> tmp((size_t)(K * T * B));
-  GVP_CUDA(cudaMemcpyAsync(tmp.data(), dev, tmp.size() * 8, cudaMemcpyDeviceToHost, e->stream));
+  int rr = get_cols(e, tmp.data(), dev, K * T);
+  if (rr) return rr;
   GVP_CUDA(cudaStreamSynchronize(e->stream));
   for (int64_t i = 0; i < K; ++i)
     for (int64_t r = 0; r < n; ++r)
@@ -472,11 +506,12 @@ static int fetch_sym(gvp_engine* e, double* host, const double* dev) {
 
 extern "C" int gvp_engine_get_state(gvp_engine* e, double* mean, double* diag, double* off,
                                     double* covs, double* crosses) {
-  const int64_t B = e->B, K = e->K, N2 = (int64_t)e->n * e->n;
+  const int64_t K = e->K, N2 = (int64_t)e->n * e->n;
   cudaStream_t s = e->stream;
-  if (mean) GVP_CUDA(cudaMemcpyAsync(mean, e->mean, K * e->n * B * 8, cudaMemcpyDeviceToHost, s));
-  if (off) GVP_CUDA(cudaMemcpyAsync(off, e->off, (K - 1) * N2 * B * 8, cudaMemcpyDeviceToHost, s));
-  if (crosses) GVP_CUDA(cudaMemcpyAsync(crosses, e->crosses, (K - 1) * N2 * B * 8, cudaMemcpyDeviceToHost, s));
+  int r0;
+  if (mean && (r0 = get_cols(e, mean, e->mean, K * e->n))) return r0;
+  if (off && (r0 = get_cols(e, off, e->off, (K - 1) * N2))) return r0;
+  if (crosses && (r0 = get_cols(e, crosses, e->crosses, (K - 1) * N2))) return r0;
   GVP_CUDA(cudaStreamSynchronize(s));
   if (diag) {
     int r = fetch_sym(e, diag, e->diag);
@@ -492,7 +527,7 @@ extern "C" int gvp_engine_get_state(gvp_engine* e, double* mean, double* diag, d
 extern "C" int gvp_engine_get_summary(gvp_engine* e, int32_t* converged, int32_t* iterations,
                                       int32_t* switch_iteration, int32_t* status, int32_t* where) {
   cudaStream_t s = e->stream;
-  const size_t bytes = e->B * sizeof(int);
+  const size_t bytes = e->nreal * sizeof(int);
   if (converged) GVP_CUDA(cudaMemcpyAsync(converged, e->ps.converged, bytes, cudaMemcpyDeviceToHost, s));
   if (iterations) GVP_CUDA(cudaMemcpyAsync(iterations, e->ps.iters, bytes, cudaMemcpyDeviceToHost, s));
   if (switch_iteration) GVP_CUDA(cudaMemcpyAsync(switch_iteration, e->ps.switch_it, bytes, cudaMemcpyDeviceToHost, s));
@@ -503,8 +538,9 @@ extern "C" int gvp_engine_get_summary(gvp_engine* e, int32_t* converged, int32_t
 }
 
 extern "C" int gvp_engine_get_records(gvp_engine* e, double* records) {
-  GVP_CUDA(cudaMemcpyAsync(records, e->records, (size_t)e->cfg.max_iters * e->B * GVP_NREC * 8,
-                           cudaMemcpyDeviceToHost, e->stream));
+  const size_t sp = (size_t)e->B * GVP_NREC * 8, dp = (size_t)e->nreal * GVP_NREC * 8;
+  GVP_CUDA(cudaMemcpy2DAsync(records, dp, e->records, sp, dp, e->cfg.max_iters,
+                             cudaMemcpyDeviceToHost, e->stream));
   GVP_CUDA(cudaStreamSynchronize(e->stream));
   return GVP_OK;
 }

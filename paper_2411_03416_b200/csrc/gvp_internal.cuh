@@ -154,6 +154,8 @@ struct V2Launch {
   const int* active;
 };
 int launch_select_step_v2(const V2Launch& q, cudaStream_t s);
+// even plan stride >= 2 required by the TMA-staged step kernel
+int64_t step_plan_stride(int nplans);
 int64_t step_scratch_doubles(int nplans, int64_t K, int n, int lanes);
 // packed-layout helpers (step_kernel.cu)
 int launch_marginals_packed(int nplans, int64_t K, int n, int64_t Bp, const double* ld,

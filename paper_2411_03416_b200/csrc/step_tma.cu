@@ -1,0 +1,892 @@
+// Kernel (b)+(c) v3: select_step_size (optimizer.py:188-231) for a batch of
+// plans — TMA-staged, two threads per probe lane, speculative bisection.
+//
+// Thread mapping. A CTA owns P plans; each plan has L candidate lanes
+// (speculative bisection, see below) and each lane is a PAIR of threads:
+//   role A: the candidate precision's GBP chain — backward Schur pivots
+//           Phi_i (SPD test, log det), forward covariance sweep Sigma_ii,
+//           Sigma_i,i+1 and tr(Lambda_k Sigma') (gbp.py:43-80, gbp.py:109-120)
+//   role B: the proximal mean system (optimizer.py:155-159) — backward
+//           elimination pivots Psi_i, forward substitution mu', the
+//           Mahalanobis term of kl_joint (optimizer.py:164-177) and, on
+//           commit, Lambda' mu' for the next iteration's rhs.
+// The two chains only meet in the KL; role B also forms U' Phi^{-1} for role A.
+//
+// Speculation. In a round the L lanes of a plan probe the nodes of the
+// bisection subtree the reference would walk next (BFS order, identical
+// float operations for every mid point); after the round the group replays
+// the reference's sequential decisions over floor(log2(L+1)) levels, so the
+// beta sequence is the reference's bit for bit; off-path nodes are dropped.
+//
+// Staging. Every knot's inputs for the CTA are brought into shared memory by
+// the Tensor Memory Accelerator: one elected thread issues one
+// cp.async.bulk.tensor per array per knot (boxes of [plans x entries]) two
+// knots ahead, completion tracked by mbarrier transaction counts; the
+// per-lane sweep intermediates of pass B return for pass F the same way.
+// All plan arrays are plan-minor with an even plan stride Bp; diagonal
+// blocks are packed lower-symmetric; a prior precision shared by all plans is
+// stored 2-wide (two identical plan columns) so its boxes meet TMA's 16-byte
+// rule.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstring>
+
+#include "gvp_internal.cuh"
+
+namespace gvp {
+namespace v3 {
+
+constexpr int kStages = 4;  // prefetch distance 2; slot of knot i-1 stays valid during knot i
+constexpr int kAhead = 2;
+
+template <int N> constexpr int T_ = N * (N + 1) / 2;
+
+GVP_DEV uint32_t saddr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+GVP_DEV void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(saddr(bar)), "r"(count) : "memory");
+}
+GVP_DEV void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(saddr(bar)), "r"(bytes)
+               : "memory");
+}
+GVP_DEV bool mbar_try(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+      : "=r"(ok)
+      : "r"(saddr(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+GVP_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
+  while (!mbar_try(bar, parity)) {
+  }
+}
+GVP_DEV void tma3(double* dst, const CUtensorMap* map, int c0, int c1, int c2, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];\n" ::"r"(
+          saddr(dst)),
+      "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(saddr(bar))
+      : "memory");
+}
+GVP_DEV void fence_proxy_async() { asm volatile("fence.proxy.async.global;\n" ::: "memory"); }
+
+// ------------------------------------------------------------ packed algebra
+template <int N>
+GVP_DEV bool chol_inv(const double (&A)[T_<N>], double (&Li)[T_<N>], double& pivprod) {
+  double L[T_<N>], inv[N];
+  bool ok = true;
+  pivprod = 1.0;
+#pragma unroll
+  for (int j = 0; j < N; ++j) {
+    double s = A[tri_idx(j, j)];
+#pragma unroll
+    for (int k = 0; k < j; ++k) s -= L[tri_idx(j, k)] * L[tri_idx(j, k)];
+    ok = ok && (s > 0.0);
+    const double r = rsqrt(s);
+    const double d = s * r;
+    ok = ok && (d > kPivotFloor);
+    L[tri_idx(j, j)] = d;
+    inv[j] = r;
+    pivprod *= d;
+#pragma unroll
+    for (int i = j + 1; i < N; ++i) {
+      double t = A[tri_idx(i, j)];
+#pragma unroll
+      for (int k = 0; k < j; ++k) t -= L[tri_idx(i, k)] * L[tri_idx(j, k)];
+      L[tri_idx(i, j)] = t * r;
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < N; ++c) {
+    Li[tri_idx(c, c)] = inv[c];
+#pragma unroll
+    for (int r = c + 1; r < N; ++r) {
+      double t = 0.0;
+#pragma unroll
+      for (int k = c; k < r; ++k) t += L[tri_idx(r, k)] * Li[tri_idx(k, c)];
+      Li[tri_idx(r, c)] = -t * inv[r];
+    }
+  }
+  return ok;
+}
+template <int N>
+GVP_DEV double sym_at(const double (&A)[T_<N>], int r, int c) {
+  return r >= c ? A[tri_idx(r, c)] : A[tri_idx(c, r)];
+}
+
+// ------------------------------------------------------------ stage layout
+// rows per plan (pass B / pass F), and per lane (pass F scratch)
+template <int N>
+struct Ly {
+  static constexpr int T = T_<N>, N2 = N * N;
+  // pass B plan rows
+  static constexpr int B_LD = 0, B_GD = T, B_G = 2 * T, B_ETA = 2 * T + N, B_V = 2 * T + 2 * N,
+                       B_LO = 2 * T + 3 * N, B_PLAN = 2 * T + 3 * N + N2;
+  // pass F plan rows
+  static constexpr int F_LD = 0, F_GD = T, F_MU = 2 * T, F_PM = 2 * T + N, F_LO = 2 * T + 2 * N,
+                       F_PLAN = 2 * T + 2 * N + N2;
+  // prior rows (both passes): KD | KO
+  static constexpr int K_KD = 0, K_KO = T, K_ROWS = T + N2;
+  // scratch entries per knot per lane: PHIINV | LIPSI | Y
+  static constexpr int SE = 2 * T + N, S_PHI = 0, S_LIPSI = T, S_Y = 2 * T;
+};
+
+struct Args {
+  CUtensorMap m_ld, m_lo, m_kd, m_ko, m_gd, m_g, m_eta, m_v, m_mu, m_pm, m_phi, m_psiy;
+  int B;
+  int64_t K, Bp;
+  int P, Pbox, Kbox;   // plans per CTA, plan box width (even), prior box width (2 if shared)
+  int ksp;             // 1 per-plan prior, 0 shared (2-wide)
+  double *o_mu, *o_ld, *o_lo, *o_cov, *o_cr, *o_v;
+  double *beta, *kl, *ld_next, *shift, *prior_cost;
+  const double *temp, *ld_cur;
+  double kl_bound, beta_min, beta_max;
+  int *status, *where, *nprobes;
+  double* probe_log;
+  int max_probes;
+  double* scratch;
+  int64_t BLp;
+  const int* active;
+  // smem offsets (doubles) of the regions inside one stage; first row of each
+  // array inside its region (every TMA box lands on a 128-byte boundary)
+  int off_plan, off_prior, off_phi, off_psiy, stage_doubles, bm_off, bar_off;
+  int rB[6], rF[5], rK[2];
+  uint32_t bytes_B, bytes_F;
+};
+
+template <int N, int L>
+__global__ void __launch_bounds__(128)
+select_step_v3_kernel(const __grid_constant__ Args a) {
+  using Y = Ly<N>;
+  constexpr int T = Y::T, N2 = Y::N2, SE = Y::SE;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  double* smem = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + a.bar_off);
+  const int tid = threadIdx.x;
+  const int role = tid & 1;
+  const int lane = (tid >> 1) % L;
+  const int p = (tid >> 1) / L;
+  const int P = a.P, Pb = a.Pbox, Kb = a.Kbox;
+  const int LP = P * L;                       // lanes per CTA
+  const int64_t b0 = (int64_t)blockIdx.x * P;
+  const int64_t b = b0 + p;
+  const int64_t K = a.K;
+  const int kcol = a.ksp ? p : 0;             // prior column in its box
+  const int lcol = p * L + lane;              // this lane's scratch column in the CTA
+  constexpr int GW = 2 * L;                   // group width in threads (<= 32)
+  const unsigned gmask = (GW == 32) ? 0xffffffffu : (((1u << GW) - 1u) << ((tid & 31) / GW * GW));
+  double* bm_area = smem + a.bm_off;          // per-lane U' Phi^{-1} handed from role B to A
+
+  if (tid == 0) {
+    for (int s = 0; s < kStages; ++s) mbar_init(&bars[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  uint32_t uses[kStages] = {0, 0, 0, 0};  // per-slot completed-phase counters (uniform)
+
+  // ---- per-plan bisection state (identical in every thread of the group)
+  const bool plan_ok = (b < a.B) && (!a.active || a.active[b]);
+  int phase = plan_ok ? 0 : 4;  // 0 first round, 1 beta_min (L==1), 2 bisect, 3 commit, 4 done
+  double lo = a.beta_min, hi = a.beta_max, best = a.beta_max;
+  const double temp = plan_ok ? a.temp[b] : 1.0;
+  const double ldc = plan_ok ? a.ld_cur[b] : 0.0;
+  int nprobe = 0;
+  auto log_probe = [&](double bt, bool spd, double klv) {
+    if (tid % GW == 0 && a.probe_log && nprobe < a.max_probes) {
+      double* row = a.probe_log + (b * a.max_probes + nprobe) * 3;
+      row[0] = bt;
+      row[1] = spd ? 1.0 : 0.0;
+      row[2] = spd ? klv : INFINITY;
+    }
+    ++nprobe;
+  };
+  double* scr = a.scratch;
+  const int64_t sc_col = b0 * L + lcol;  // global scratch column
+
+  auto slot = [&](int64_t s) { return smem + (s % kStages) * a.stage_doubles; };
+  // issue the TMA loads of one knot of a pass into slot s % kStages
+  auto issue = [&](int64_t s, int64_t i, bool passB) {
+    double* st = slot(s);
+    uint64_t* bar = &bars[s % kStages];
+    mbar_expect_tx(bar, passB ? a.bytes_B : a.bytes_F);
+    const int ck = (int)(b0 * a.ksp);
+    double* pl = st + a.off_plan;
+    double* pr = st + a.off_prior;
+    tma3(pr + a.rK[0] * Kb, &a.m_kd, ck, 0, (int)i, bar);
+    tma3(pr + a.rK[1] * Kb, &a.m_ko, ck, 0, (int)i, bar);
+    if (passB) {
+      tma3(pl + a.rB[0] * Pb, &a.m_ld, (int)b0, 0, (int)i, bar);
+      tma3(pl + a.rB[1] * Pb, &a.m_gd, (int)b0, 0, (int)i, bar);
+      tma3(pl + a.rB[2]* Pb, &a.m_g, (int)b0, 0, (int)i, bar);
+      tma3(pl + a.rB[3] * Pb, &a.m_eta, (int)b0, 0, (int)i, bar);
+      tma3(pl + a.rB[4]* Pb, &a.m_v, (int)b0, 0, (int)i, bar);
+      tma3(pl + a.rB[5] * Pb, &a.m_lo, (int)b0, 0, (int)i, bar);
+    } else {
+      tma3(pl + a.rF[0] * Pb, &a.m_ld, (int)b0, 0, (int)i, bar);
+      tma3(pl + a.rF[1] * Pb, &a.m_gd, (int)b0, 0, (int)i, bar);
+      tma3(pl + a.rF[2] * Pb, &a.m_mu, (int)b0, 0, (int)i, bar);
+      tma3(pl + a.rF[3] * Pb, &a.m_pm, (int)b0, 0, (int)i, bar);
+      tma3(pl + a.rF[4] * Pb, &a.m_lo, (int)b0, 0, (int)i, bar);
+      tma3(st + a.off_phi, &a.m_phi, (int)(b0 * L), 0, (int)(i + 1), bar);        // PHIINV of knot i+1
+      tma3(st + a.off_psiy, &a.m_psiy, (int)(b0 * L), Y::S_LIPSI, (int)i, bar);  // LIPSI | Y of knot i
+    }
+  };
+  auto wait_slot = [&](int64_t s) {
+    const int k = (int)(s % kStages);
+    mbar_wait(&bars[k], uses[k] & 1u);
+    ++uses[k];
+  };
+
+  for (;;) {
+    // ---------------- candidate beta of this lane
+    bool lane_on = false, write = false;
+    double beta = 0.0;
+    const bool tree_phase = (phase == 2) || (phase == 0 && L >= 2 && lane >= 2);
+    if (phase == 0 && lane == 0) {
+      lane_on = true;
+      beta = a.beta_max;
+    } else if (phase == 0 && L >= 2 && lane == 1) {
+      lane_on = true;
+      beta = a.beta_min;
+    } else if (phase == 1 && lane == 0) {
+      lane_on = true;
+      beta = a.beta_min;
+    } else if (phase == 3 && lane == 0) {
+      lane_on = true;
+      write = true;
+      beta = best;
+    } else if (tree_phase) {
+      const int k = (phase == 2) ? lane + 1 : lane - 1;
+      double l = (phase == 2) ? lo : a.beta_min, h = (phase == 2) ? hi : a.beta_max;
+      const int depth = 31 - __clz(k);
+      bool valid = true;
+      for (int lev = depth - 1; lev >= 0 && valid; --lev) {
+        if (!((h - l) > 1e-3 * h)) valid = false;
+        const double mid = 0.5 * (l + h);
+        if ((k >> lev) & 1) l = mid; else h = mid;
+      }
+      valid = valid && ((h - l) > 1e-3 * h);
+      if (valid) {
+        lane_on = true;
+        beta = 0.5 * (l + h);
+      }
+    }
+    if (!__syncthreads_or(phase < 4)) break;
+
+    const double inv_t = 1.0 / temp, two_t = 2.0 / temp;
+    const double inv_b = lane_on ? 1.0 / beta : 0.0, c = lane_on ? beta / (beta + 1.0) : 0.0;
+    int res = 0;  // role A: 1 = Phi not SPD; role B: 2 = mean pivot not SPD
+    int fail_knot = -1;
+    double ld_sum = 0.0;
+
+    // =============================== pass B: knots K-1 .. 0
+    double LiN[T], yN[N];
+    int64_t sbase = 0;
+    if (tid == 0)
+      for (int s = 0; s < kAhead && s < K; ++s) issue(s, K - 1 - s, true);
+    for (int64_t s = 0; s < K; ++s) {
+      wait_slot(s);
+      __syncthreads();  // everyone past knot s-1: its slot may be refilled
+      if (tid == 0 && s + kAhead < K) issue(s + kAhead, K - 1 - (s + kAhead), true);
+      const int64_t i = K - 1 - s;
+      if (!(lane_on && res == 0)) continue;
+      const double* st = slot(s);
+      const double* pl = st + a.off_plan;
+      const double* pr = st + a.off_prior;
+      auto pv = [&](int row) { return pl[row * Pb + p]; };
+      auto kv = [&](int row) { return pr[row * Kb + kcol]; };
+      double A_[T];
+      if (role == 0) {  // Lambda' diag block (optimizer.py:151-153), already symmetric
+#pragma unroll
+        for (int q = 0; q < T; ++q)
+          A_[q] = ((pv(a.rB[1] + q) * two_t + kv(a.rK[0] + q) * inv_t) + pv(a.rB[0] + q) * inv_b) * c;
+      } else {          // S diag block (optimizer.py:155)
+#pragma unroll
+        for (int q = 0; q < T; ++q) A_[q] = kv(a.rK[0] + q) * inv_t + pv(a.rB[0] + q) * inv_b;
+      }
+      double rhs[N];
+      if (role == 1) {
+#pragma unroll
+        for (int r = 0; r < N; ++r)
+          rhs[r] = ((-pv(a.rB[2]+ r)) * inv_t + pv(a.rB[3] + r) * inv_t) + pv(a.rB[4]+ r) * inv_b;
+      }
+      if (i < K - 1) {
+        // off block: S_off = K_off/T + Lambda_off/beta; role A uses U' = c * S_off
+        const double sc_ = role == 0 ? c : 1.0;
+        double W[N2];  // W = Li_{i+1} X^T, X = sc_ * S_off
+#pragma unroll
+        for (int r = 0; r < N; ++r)
+#pragma unroll
+          for (int q = 0; q < N; ++q) {
+            double t = 0.0;
+#pragma unroll
+            for (int k2 = 0; k2 <= r; ++k2)
+              t += LiN[tri_idx(r, k2)] * ((kv(a.rK[1] + q * N + k2) * inv_t + pv(a.rB[5] + q * N + k2) * inv_b) * sc_);
+            W[r * N + q] = t;
+          }
+#pragma unroll
+        for (int r = 0; r < N; ++r)
+#pragma unroll
+          for (int q = 0; q <= r; ++q) {
+            double t = 0.0;
+#pragma unroll
+            for (int k2 = 0; k2 < N; ++k2) t += W[k2 * N + r] * W[k2 * N + q];
+            A_[tri_idx(r, q)] -= t;
+          }
+        if (role == 1) {
+#pragma unroll
+          for (int r = 0; r < N; ++r) {
+            double t = 0.0;
+#pragma unroll
+            for (int k2 = 0; k2 < N; ++k2) t += W[k2 * N + r] * yN[k2];
+            rhs[r] -= t;
+          }
+        }
+      }
+      double Li[T], pp;
+      if (!chol_inv<N>(A_, Li, pp)) {
+        res = role == 0 ? 1 : 2;
+        fail_knot = (int)i;
+        continue;
+      }
+      double* sc = scr + (i * SE) * a.BLp + sc_col;
+      if (role == 0) {
+        ld_sum += 2.0 * log(pp);
+        // Phi^{-1} = Li^T Li -> scratch for the covariance sweep
+#pragma unroll
+        for (int r = 0; r < N; ++r)
+#pragma unroll
+          for (int q = 0; q <= r; ++q) {
+            double t = 0.0;
+#pragma unroll
+            for (int k2 = r; k2 < N; ++k2) t += Li[tri_idx(k2, r)] * Li[tri_idx(k2, q)];
+            sc[(Y::S_PHI + tri_idx(r, q)) * a.BLp] = t;
+          }
+      } else {
+#pragma unroll
+        for (int r = 0; r < N; ++r) {
+          double t = 0.0;
+#pragma unroll
+          for (int k2 = 0; k2 <= r; ++k2) t += Li[tri_idx(r, k2)] * rhs[k2];
+          yN[r] = t;
+          sc[(Y::S_Y + r) * a.BLp] = t;
+        }
+#pragma unroll
+        for (int q = 0; q < T; ++q) sc[(Y::S_LIPSI + q) * a.BLp] = Li[q];
+      }
+#pragma unroll
+      for (int q = 0; q < T; ++q) LiN[q] = Li[q];
+    }
+    sbase += K;
+    fence_proxy_async();  // scratch stores (generic proxy) -> TMA reads (async proxy)
+    __syncthreads();
+    // both threads of a lane agree on the outcome (the mean solve fails first,
+    // like proximal_update raising before gbp_marginals, optimizer.py:203-207)
+    {
+      const int other = __shfl_xor_sync(0xffffffffu, res, 1);
+      const int otherk = __shfl_xor_sync(0xffffffffu, fail_knot, 1);
+      const int rA = role == 0 ? res : other, rB = role == 0 ? other : res;
+      const int kA = role == 0 ? fail_knot : otherk, kB = role == 0 ? otherk : fail_knot;
+      res = rB ? 2 : (rA ? 1 : 0);
+      fail_knot = rB ? kB : kA;
+    }
+
+    // =============================== pass F: knots 0 .. K-1
+    const bool passF = lane_on && res == 0;
+    double Sig[T], mprev[N], dprev[N], dpprev[N], part[N];
+    double trace = 0.0, mahal = 0.0, sh2 = 0.0, pq_c = 0.0, ptr_c = 0.0;
+    if (passF && role == 0) {
+      const double* sc = scr + sc_col;  // Sigma_00 = Phi_0^{-1}
+#pragma unroll
+      for (int q = 0; q < T; ++q) Sig[q] = sc[(Y::S_PHI + q) * a.BLp];
+    }
+    if (tid == 0)
+      for (int s = 0; s < kAhead && s < K; ++s) issue(sbase + s, s, false);
+    for (int64_t i = 0; i < K; ++i) {
+      const int64_t s = sbase + i;
+      wait_slot(s);
+      __syncthreads();
+      if (tid == 0 && i + kAhead < K) issue(s + kAhead, i + kAhead, false);
+      const double* st = slot(s);
+      const double* pl = st + a.off_plan;
+      const double* pr = st + a.off_prior;
+      const double* stp = slot(s - 1);  // knot i-1 (valid when i > 0)
+      const double* plp = stp + a.off_plan;
+      const double* prp = stp + a.off_prior;
+      auto pv = [&](int row) { return pl[row * Pb + p]; };
+      auto kv = [&](int row) { return pr[row * Kb + kcol]; };
+      auto pvp = [&](int row) { return plp[row * Pb + p]; };
+      auto kvp = [&](int row) { return prp[row * Kb + kcol]; };
+      auto phi = [&](int q) { return st[a.off_phi + q * LP + lcol]; };
+      auto psi = [&](int q) { return st[a.off_psiy + q * LP + lcol]; };  // LIPSI rows then Y rows
+      double* bm = bm_area + lcol * N2;
+      if (passF && role == 1) {
+        // ---- mean: mu'_i = Li^T (y_i - Li S_{i-1,i}^T mu'_{i-1})
+        double m[N];
+        {
+          double z[N], w[N];
+#pragma unroll
+          for (int r = 0; r < N; ++r) {
+            double t = 0.0;
+            if (i > 0) {
+#pragma unroll
+              for (int q = 0; q < N; ++q)
+                t += (kvp(a.rK[1] + q * N + r) * inv_t + pvp(a.rF[4] + q * N + r) * inv_b) * mprev[q];
+            }
+            z[r] = t;
+          }
+#pragma unroll
+          for (int r = 0; r < N; ++r) {
+            double t = 0.0;
+#pragma unroll
+            for (int q = 0; q <= r; ++q) t += psi(tri_idx(r, q)) * z[q];
+            w[r] = psi(T + r) - t;
+          }
+#pragma unroll
+          for (int r = 0; r < N; ++r) {
+            double t = 0.0;
+#pragma unroll
+            for (int q = r; q < N; ++q) t += psi(tri_idx(q, r)) * w[q];
+            m[r] = t;
+          }
+        }
+        double dl[N];
+#pragma unroll
+        for (int r = 0; r < N; ++r) {
+          dl[r] = pv(a.rF[2] + r) - m[r];  // delta = cur.mean - nxt.mean
+          sh2 += dl[r] * dl[r];
+        }
+#pragma unroll
+        for (int r = 0; r < N; ++r)
+#pragma unroll
+          for (int q = 0; q <= r; ++q)
+            mahal += ((q == r) ? 1.0 : 2.0) * pv(a.rF[0] + tri_idx(r, q)) * dl[r] * dl[q];
+        if (i > 0) {
+          double t = 0.0;
+#pragma unroll
+          for (int r = 0; r < N; ++r)
+#pragma unroll
+            for (int q = 0; q < N; ++q) t += dprev[r] * pvp(a.rF[4] + r * N + q) * dl[q];
+          mahal += 2.0 * t;
+        }
+        if (write) {
+          double dp[N], Pn[T];
+#pragma unroll
+          for (int q = 0; q < T; ++q)
+            Pn[q] = ((pv(a.rF[1] + q) * two_t + kv(a.rK[0] + q) * inv_t) + pv(a.rF[0] + q) * inv_b) * c;
+#pragma unroll
+          for (int r = 0; r < N; ++r) {
+            a.o_mu[(i * N + r) * a.Bp + b] = m[r];
+            dp[r] = m[r] - pv(a.rF[3] + r);
+          }
+#pragma unroll
+          for (int r = 0; r < N; ++r)
+#pragma unroll
+            for (int q = 0; q <= r; ++q)
+              pq_c += ((q == r) ? 1.0 : 2.0) * kv(a.rK[0] + tri_idx(r, q)) * dp[r] * dp[q];
+          double pt[N];
+#pragma unroll
+          for (int r = 0; r < N; ++r) {
+            double t = 0.0;
+#pragma unroll
+            for (int q = 0; q < N; ++q) t += sym_at<N>(Pn, r, q) * m[q];
+            if (i > 0) {
+#pragma unroll
+              for (int q = 0; q < N; ++q)
+                t += ((kvp(a.rK[1] + q * N + r) * inv_t + pvp(a.rF[4] + q * N + r) * inv_b) * c) * mprev[q];
+            }
+            pt[r] = t;
+          }
+          if (i > 0) {
+            double t2 = 0.0;
+#pragma unroll
+            for (int r = 0; r < N; ++r)
+#pragma unroll
+              for (int q = 0; q < N; ++q) t2 += dpprev[r] * kvp(a.rK[1] + r * N + q) * dp[q];
+            pq_c += 2.0 * t2;
+#pragma unroll
+            for (int r = 0; r < N; ++r) {
+              double t = part[r];
+#pragma unroll
+              for (int q = 0; q < N; ++q)
+                t += ((kvp(a.rK[1] + r * N + q) * inv_t + pvp(a.rF[4] + r * N + q) * inv_b) * c) * m[q];
+              a.o_v[((i - 1) * N + r) * a.Bp + b] = t;
+            }
+          }
+#pragma unroll
+          for (int r = 0; r < N; ++r) {
+            part[r] = pt[r];
+            dpprev[r] = dp[r];
+          }
+          if (i == K - 1) {
+#pragma unroll
+            for (int r = 0; r < N; ++r) a.o_v[(i * N + r) * a.Bp + b] = pt[r];
+          }
+        }
+#pragma unroll
+        for (int r = 0; r < N; ++r) {
+          mprev[r] = m[r];
+          dprev[r] = dl[r];
+        }
+        // ---- U' Phi_{i+1}^{-1} for role A
+        if (i + 1 < K) {
+#pragma unroll
+          for (int r = 0; r < N; ++r)
+#pragma unroll
+            for (int q = 0; q < N; ++q) {
+              double t = 0.0;
+#pragma unroll
+              for (int k2 = 0; k2 < N; ++k2)
+                t += ((kv(a.rK[1] + r * N + k2) * inv_t + pv(a.rF[4] + r * N + k2) * inv_b) * c) *
+                     phi(k2 >= q ? tri_idx(k2, q) : tri_idx(q, k2));
+              bm[r * N + q] = t;
+            }
+        }
+      }
+      __syncwarp();
+      if (passF && role == 0) {
+        // ---- tr(Lambda_ii Sigma_ii)
+#pragma unroll
+        for (int r = 0; r < N; ++r)
+#pragma unroll
+          for (int q = 0; q <= r; ++q)
+            trace += ((q == r) ? 1.0 : 2.0) * pv(a.rF[0] + tri_idx(r, q)) * Sig[tri_idx(r, q)];
+        if (write) {
+#pragma unroll
+          for (int q = 0; q < T; ++q) {
+            a.o_ld[(i * T + q) * a.Bp + b] =
+                ((pv(a.rF[1] + q) * two_t + kv(a.rK[0] + q) * inv_t) + pv(a.rF[0] + q) * inv_b) * c;
+            a.o_cov[(i * T + q) * a.Bp + b] = Sig[q];
+          }
+#pragma unroll
+          for (int r = 0; r < N; ++r)
+#pragma unroll
+            for (int q = 0; q <= r; ++q)
+              ptr_c += ((q == r) ? 1.0 : 2.0) * kv(a.rK[0] + tri_idx(r, q)) * Sig[tri_idx(r, q)];
+        }
+        if (i + 1 < K) {
+          // M = Sigma_ii U' Phi^{-1} = -Sigma_{i,i+1};  Sigma_{i+1} = Phi^{-1} + (U' Phi^{-1})^T M
+          double Up[N2], M[N2];
+#pragma unroll
+          for (int q = 0; q < N2; ++q) Up[q] = (kv(a.rK[1] + q) * inv_t + pv(a.rF[4] + q) * inv_b) * c;
+#pragma unroll
+          for (int r = 0; r < N; ++r)
+#pragma unroll
+            for (int q = 0; q < N; ++q) {
+              double t = 0.0;
+#pragma unroll
+              for (int k2 = 0; k2 < N; ++k2) t += sym_at<N>(Sig, r, k2) * bm[k2 * N + q];
+              M[r * N + q] = t;
+            }
+          double tc = 0.0;
+#pragma unroll
+          for (int q = 0; q < N2; ++q) tc += pv(a.rF[4] + q) * M[q];
+          trace -= 2.0 * tc;  // 2 <Lambda_{i,i+1}, Sigma_{i,i+1}>
+          if (write) {
+            double tk = 0.0;
+#pragma unroll
+            for (int q = 0; q < N2; ++q) {
+              a.o_cr[(i * N2 + q) * a.Bp + b] = -M[q];
+              a.o_lo[(i * N2 + q) * a.Bp + b] = Up[q];
+              tk += kv(a.rK[1] + q) * M[q];
+            }
+            ptr_c -= 2.0 * tk;
+          }
+#pragma unroll
+          for (int r = 0; r < N; ++r)
+#pragma unroll
+            for (int q = 0; q <= r; ++q) {
+              double t = 0.0;
+#pragma unroll
+              for (int k2 = 0; k2 < N; ++k2) t += bm[k2 * N + r] * M[k2 * N + q];
+              Sig[tri_idx(r, q)] = phi(tri_idx(r, q)) + t;
+            }
+        }
+      }
+    }
+    sbase += K;
+    __syncthreads();
+
+    // ---------------- KL of each lane: role A holds trace + log det, role B mahal + shift
+    // each thread sends its own quantity: A -> trace, ptr, log det; B -> mahal, pq, shift
+    const double o_trace_or_mahal = __shfl_xor_sync(0xffffffffu, role == 0 ? trace : mahal, 1);
+    const double o_ld = __shfl_xor_sync(0xffffffffu, ld_sum, 1);
+    const double o_sh = __shfl_xor_sync(0xffffffffu, sh2, 1);
+    const double o_pq = __shfl_xor_sync(0xffffffffu, role == 0 ? ptr_c : pq_c, 1);
+    const double tr_ = role == 0 ? trace : o_trace_or_mahal;
+    const double mh_ = role == 0 ? o_trace_or_mahal : mahal;
+    const double ld_ = role == 0 ? ld_sum : o_ld;
+    const double sh_ = role == 0 ? o_sh : sh2;
+    const double ptr_ = role == 0 ? ptr_c : o_pq, pq_ = role == 0 ? o_pq : pq_c;
+    double klv = 0.0;
+    if (passF) {
+      const double x = 0.5 * ((((tr_ + mh_) - (double)(K * N)) + ld_) - ldc);
+      klv = (0.0 > x) ? 0.0 : x;  // python max(x, 0.0): NaN stays NaN
+    }
+    if (write && role == 0) {
+      a.beta[b] = best;
+      a.kl[b] = klv;
+      a.ld_next[b] = ld_;
+      a.shift[b] = sqrt(sh_);
+      if (a.prior_cost) a.prior_cost[b] = 0.5 * pq_ + 0.5 * ptr_;
+      a.status[b] = GVP_OK;
+      a.where[b] = -1;
+      if (a.nprobes) a.nprobes[b] = nprobe;
+    }
+
+    // ---------------- group decision (the reference's sequential logic)
+    double r_kl[L], r_beta[L];
+    int r_res[L], r_on[L], r_fail[L];
+#pragma unroll
+    for (int q = 0; q < L; ++q) {
+      r_kl[q] = __shfl_sync(gmask, klv, 2 * q, GW);
+      r_res[q] = __shfl_sync(gmask, res, 2 * q, GW);
+      r_on[q] = __shfl_sync(gmask, (int)lane_on, 2 * q, GW);
+      r_beta[q] = __shfl_sync(gmask, beta, 2 * q, GW);
+      r_fail[q] = __shfl_sync(gmask, fail_knot, 2 * q, GW);
+    }
+    if (phase >= 4) continue;
+    auto feasible = [&](int q) { return r_res[q] == 0 && !(r_kl[q] > a.kl_bound); };
+    auto fail = [&](int code, int w) {
+      if (tid % GW == 0) {
+        a.status[b] = code;
+        a.where[b] = w;
+        if (a.nprobes) a.nprobes[b] = nprobe;
+      }
+      phase = 4;
+    };
+    auto walk = [&](int off, int depth_avail) -> bool {
+      int k = 1;
+      for (int lev = 0; lev < depth_avail; ++lev) {
+        if (!((hi - lo) > 1e-3 * hi)) return true;
+        const int q = k - 1 + off;
+        if (q >= L || !r_on[q]) return true;
+        log_probe(r_beta[q], r_res[q] != 1, r_kl[q]);
+        if (r_res[q] == 2) {
+          fail(GVP_ERR_NOT_SPD, r_fail[q] | GVP_WHERE_MEAN_SOLVE_BIAS);
+          return false;
+        }
+        if (feasible(q)) {
+          lo = r_beta[q];
+          best = r_beta[q];
+          k = 2 * k + 1;
+        } else {
+          hi = r_beta[q];
+          k = 2 * k;
+        }
+      }
+      return true;
+    };
+    auto tree_depth = [](int nodes) {
+      int d = 0;
+      while ((2 << d) - 1 <= nodes) ++d;
+      return d;
+    };
+    if (phase == 3) {
+      phase = 4;
+    } else if (phase == 0) {
+      log_probe(r_beta[0], r_res[0] != 1, r_kl[0]);
+      if (r_res[0] == 2) {
+        fail(GVP_ERR_NOT_SPD, r_fail[0] | GVP_WHERE_MEAN_SOLVE_BIAS);
+      } else if (feasible(0)) {
+        best = a.beta_max;
+        phase = 3;
+      } else if (L == 1) {
+        phase = 1;
+      } else {
+        log_probe(r_beta[1], r_res[1] != 1, r_kl[1]);
+        if (r_res[1] == 2) {
+          fail(GVP_ERR_NOT_SPD, r_fail[1] | GVP_WHERE_MEAN_SOLVE_BIAS);
+        } else if (!feasible(1)) {
+          fail(GVP_ERR_NO_FEASIBLE_STEP, -1);
+        } else {
+          best = a.beta_min;
+          lo = a.beta_min;
+          hi = a.beta_max;
+          if (walk(2, tree_depth(L - 2))) phase = ((hi - lo) > 1e-3 * hi) ? 2 : 3;
+        }
+      }
+    } else if (phase == 1) {
+      log_probe(r_beta[0], r_res[0] != 1, r_kl[0]);
+      if (r_res[0] == 2) {
+        fail(GVP_ERR_NOT_SPD, r_fail[0] | GVP_WHERE_MEAN_SOLVE_BIAS);
+      } else if (!feasible(0)) {
+        fail(GVP_ERR_NO_FEASIBLE_STEP, -1);
+      } else {
+        best = a.beta_min;
+        lo = a.beta_min;
+        hi = a.beta_max;
+        phase = ((hi - lo) > 1e-3 * hi) ? 2 : 3;
+      }
+    } else if (phase == 2) {
+      if (walk(0, tree_depth(L))) phase = ((hi - lo) > 1e-3 * hi) ? 2 : 3;
+    }
+  }
+}
+
+// ------------------------------------------------------------ host side
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (EncodeTiledFn)p;
+  }
+  return fn;
+}
+
+// 3D map over a plan-minor array [K][E][W] (W = plan stride), box [bw, rows, 1]
+static int make_map(CUtensorMap* m, const double* base, int64_t W, int64_t E, int64_t K, int bw,
+                    int rows) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) {
+    set_error("cuTensorMapEncodeTiled unavailable");
+    return GVP_ERR_CUDA;
+  }
+  cuuint64_t dims[3] = {(cuuint64_t)W, (cuuint64_t)E, (cuuint64_t)std::max<int64_t>(K, 1)};
+  cuuint64_t strides[2] = {(cuuint64_t)(W * 8), (cuuint64_t)(W * E * 8)};
+  cuuint32_t box[3] = {(cuuint32_t)bw, (cuuint32_t)rows, 1};
+  cuuint32_t es[3] = {1, 1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, (void*)base, dims, strides, box, es,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_error("cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+    return GVP_ERR_CUDA;
+  }
+  return GVP_OK;
+}
+
+}  // namespace v3
+
+int64_t step_scratch_doubles(int nplans, int64_t K, int n, int lanes) {
+  const int64_t T = (int64_t)n * (n + 1) / 2;
+  const int64_t BL = (((int64_t)nplans + 1) & ~1LL) * lanes + 64;  // padded columns
+  return std::max<int64_t>(1, K * (2 * T + n) * BL);
+}
+
+int64_t step_plan_stride(int nplans) { return std::max<int64_t>(2, ((int64_t)nplans + 1) & ~1LL); }
+
+static int round_up(int x, int m) { return (x + m - 1) / m * m; }
+
+int launch_select_step_v2(const V2Launch& q, cudaStream_t s) {
+  if (q.nplans == 0 || q.K == 0) return GVP_OK;
+  const int L = q.lanes;
+  if (L != 1 && L != 4 && L != 8 && L != 16) {
+    set_error("lanes must be 1, 4, 8 or 16");
+    return GVP_ERR_ARG;
+  }
+  if (q.Bp % 2 || q.Bp < 2) {
+    set_error("plan stride must be even (step_plan_stride)");
+    return GVP_ERR_ARG;
+  }
+  // threads per CTA: 2 per lane; enough CTAs to cover the SMs. Plans per CTA
+  // must be even: a TMA box's first plan column must sit on a 16-byte boundary.
+  int TB = ((int64_t)q.nplans * L * 2 <= 148 * 64) ? 32 : 64;
+  if (4 * L > TB) TB = 4 * L;
+  const int P = TB / (2 * L);
+  const int Pb = round_up(P, 2);
+  const int Kb = q.kshared ? 2 : Pb;
+  const int n = q.n;
+  const int T = n * (n + 1) / 2, N2 = n * n, SE = 2 * T + n;
+  v3::Args a;
+  std::memset(&a, 0, sizeof(a));
+  a.B = q.nplans;
+  a.K = q.K;
+  a.Bp = q.Bp;
+  a.P = P;
+  a.Pbox = Pb;
+  a.Kbox = Kb;
+  a.ksp = q.kshared ? 0 : 1;
+  const int64_t K = q.K, K1 = std::max<int64_t>(K - 1, 1);
+  const int64_t KW = q.kshared ? 2 : q.Bp;
+  const int64_t BLp = (q.Bp * L) + 64;
+  int r;
+  if ((r = v3::make_map(&a.m_ld, q.ld, q.Bp, T, K, Pb, T)) || (r = v3::make_map(&a.m_lo, q.lo, q.Bp, N2, K1, Pb, N2)) ||
+      (r = v3::make_map(&a.m_kd, q.kd, KW, T, K, Kb, T)) || (r = v3::make_map(&a.m_ko, q.ko, KW, N2, K1, Kb, N2)) ||
+      (r = v3::make_map(&a.m_gd, q.gd, q.Bp, T, K, Pb, T)) || (r = v3::make_map(&a.m_g, q.g, q.Bp, n, K, Pb, n)) ||
+      (r = v3::make_map(&a.m_eta, q.eta, q.Bp, n, K, Pb, n)) || (r = v3::make_map(&a.m_v, q.v, q.Bp, n, K, Pb, n)) ||
+      (r = v3::make_map(&a.m_mu, q.mu, q.Bp, n, K, Pb, n)) || (r = v3::make_map(&a.m_pm, q.pmean, q.Bp, n, K, Pb, n)) ||
+      (r = v3::make_map(&a.m_phi, q.scratch, BLp, SE, K, P * L < 2 ? 2 : P * L, T)) ||
+      (r = v3::make_map(&a.m_psiy, q.scratch, BLp, SE, K, P * L < 2 ? 2 : P * L, T + n)))
+    return r;
+  a.o_mu = q.o_mu; a.o_ld = q.o_ld; a.o_lo = q.o_lo; a.o_cov = q.o_cov; a.o_cr = q.o_cr; a.o_v = q.o_v;
+  a.beta = q.beta; a.kl = q.kl; a.ld_next = q.ld_next; a.shift = q.shift; a.prior_cost = q.prior_cost;
+  a.temp = q.temp; a.ld_cur = q.ld_cur;
+  a.kl_bound = q.kl_bound; a.beta_min = q.beta_min; a.beta_max = q.beta_max;
+  a.status = q.status; a.where = q.where; a.nprobes = q.nprobes;
+  a.probe_log = q.probe_log; a.max_probes = q.max_probes;
+  a.scratch = q.scratch;
+  a.BLp = BLp;
+  a.active = q.active;
+  // one stage: plan rows | prior rows | PHI rows (lanes) | LIPSI+Y rows (lanes).
+  // Every array's box starts on a 128-byte boundary (TMA destination rule):
+  // row starts are rounded to a multiple of 16 / gcd(width, 16) rows.
+  const int LPb = P * L < 2 ? 2 : P * L;
+  auto gran = [](int width) {
+    int g = 16;
+    while (g > 1 && (width * g) % 16 == 0 && (width * (g / 2)) % 16 == 0) g /= 2;
+    return g;
+  };
+  auto layout = [&](const int* sizes, int cnt, int width, int* starts) {
+    const int g = gran(width);
+    int row = 0;
+    for (int k = 0; k < cnt; ++k) {
+      starts[k] = row;
+      row = round_up(row + sizes[k], g);
+    }
+    return row;
+  };
+  const int szB[6] = {T, T, n, n, n, N2}, szF[5] = {T, T, n, n, N2}, szK[2] = {T, N2};
+  const int rowsB = layout(szB, 6, Pb, a.rB), rowsF = layout(szF, 5, Pb, a.rF);
+  const int rowsK = layout(szK, 2, Kb, a.rK);
+  a.off_plan = 0;
+  a.off_prior = round_up(std::max(rowsB, rowsF) * Pb, 16);
+  a.off_phi = a.off_prior + round_up(rowsK * Kb, 16);
+  a.off_psiy = a.off_phi + round_up(T * LPb, 16);
+  a.stage_doubles = a.off_psiy + round_up((T + n) * LPb, 16);
+  a.bm_off = v3::kStages * a.stage_doubles;
+  a.bar_off = a.bm_off + round_up(P * L * N2, 16);
+  a.bytes_B = (uint32_t)(((2 * T + 3 * n + N2) * Pb + (T + N2) * Kb) * 8);
+  a.bytes_F = (uint32_t)(((2 * T + 2 * n + N2) * Pb + (T + N2) * Kb + (2 * T + n) * LPb) * 8);
+  (void)SE;
+  const size_t bytes = (size_t)(a.bar_off + 2 * v3::kStages) * sizeof(double) + 1024;
+  const unsigned grid = (unsigned)((q.nplans + P - 1) / P);
+#define GVP_V3(NN, LL)                                                                        \
+  {                                                                                           \
+    GVP_CUDA(cudaFuncSetAttribute(v3::select_step_v3_kernel<NN, LL>,                          \
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));  \
+    v3::select_step_v3_kernel<NN, LL><<<grid, TB, bytes, s>>>(a);                             \
+  }
+#define GVP_V3_L(NN)                  \
+  switch (L) {                        \
+    case 1: GVP_V3(NN, 1) break;      \
+    case 4: GVP_V3(NN, 4) break;      \
+    case 8: GVP_V3(NN, 8) break;      \
+    default: GVP_V3(NN, 16) break;    \
+  }
+  switch (n) {
+    case 2: GVP_V3_L(2) break;
+    case 4: GVP_V3_L(4) break;
+    case 6: GVP_V3_L(6) break;
+    default:
+      set_error("step kernel supports n in {2, 4, 6}");
+      return GVP_ERR_UNSUPPORTED;
+  }
+#undef GVP_V3_L
+#undef GVP_V3
+  GVP_CUDA(cudaGetLastError());
+  return GVP_OK;
+}
+
+}  // namespace gvp
