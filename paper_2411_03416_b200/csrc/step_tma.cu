@@ -166,19 +166,22 @@ select_step_v3_kernel(const __grid_constant__ Args a) {
   double* smem = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + a.bar_off);
   const int tid = threadIdx.x;
-  const int role = tid & 1;
-  const int lane = (tid >> 1) % L;
-  const int p = (tid >> 1) / L;
+  // warp-specialised roles: even warps run chain A, odd warps chain B for the
+  // same 32 lane slots, so neither chain diverges inside a warp
+  const int role = (tid >> 5) & 1;
+  const int lcol = ((tid >> 6) << 5) | (tid & 31);  // lane slot in the CTA
+  const int lane = lcol % L;
+  const int p = lcol / L;
   const int P = a.P, Pb = a.Pbox, Kb = a.Kbox;
   const int LP = P * L;                       // lanes per CTA
   const int64_t b0 = (int64_t)blockIdx.x * P;
   const int64_t b = b0 + p;
   const int64_t K = a.K;
   const int kcol = a.ksp ? p : 0;             // prior column in its box
-  const int lcol = p * L + lane;              // this lane's scratch column in the CTA
-  constexpr int GW = 2 * L;                   // group width in threads (<= 32)
-  const unsigned gmask = (GW == 32) ? 0xffffffffu : (((1u << GW) - 1u) << ((tid & 31) / GW * GW));
-  double* bm_area = smem + a.bm_off;          // per-lane U' Phi^{-1} handed from role B to A
+  constexpr int GW = L;                       // group width in threads (<= 16, inside a warp)
+  const unsigned gmask = ((1u << GW) - 1u) << ((tid & 31) / GW * GW);
+  double* xch = smem + a.bm_off;              // per-slot exchange between the two roles
+  const bool leader = role == 0 && lane == 0;
 
   if (tid == 0) {
     for (int s = 0; s < kStages; ++s) mbar_init(&bars[s], 1);
@@ -195,7 +198,7 @@ select_step_v3_kernel(const __grid_constant__ Args a) {
   const double ldc = plan_ok ? a.ld_cur[b] : 0.0;
   int nprobe = 0;
   auto log_probe = [&](double bt, bool spd, double klv) {
-    if (tid % GW == 0 && a.probe_log && nprobe < a.max_probes) {
+    if (leader && a.probe_log && nprobe < a.max_probes) {
       double* row = a.probe_log + (b * a.max_probes + nprobe) * 3;
       row[0] = bt;
       row[1] = spd ? 1.0 : 0.0;
@@ -386,8 +389,13 @@ select_step_v3_kernel(const __grid_constant__ Args a) {
     // both threads of a lane agree on the outcome (the mean solve fails first,
     // like proximal_update raising before gbp_marginals, optimizer.py:203-207)
     {
-      const int other = __shfl_xor_sync(0xffffffffu, res, 1);
-      const int otherk = __shfl_xor_sync(0xffffffffu, fail_knot, 1);
+      int* xi = reinterpret_cast<int*>(xch);  // [role][slot] result codes, then fail knots
+      xi[role * LP + lcol] = res;
+      xi[2 * LP + role * LP + lcol] = fail_knot;
+      __syncthreads();
+      const int other = xi[(1 - role) * LP + lcol];
+      const int otherk = xi[2 * LP + (1 - role) * LP + lcol];
+      __syncthreads();
       const int rA = role == 0 ? res : other, rB = role == 0 ? other : res;
       const int kA = role == 0 ? fail_knot : otherk, kB = role == 0 ? otherk : fail_knot;
       res = rB ? 2 : (rA ? 1 : 0);
@@ -422,7 +430,6 @@ select_step_v3_kernel(const __grid_constant__ Args a) {
       auto kvp = [&](int row) { return prp[row * Kb + kcol]; };
       auto phi = [&](int q) { return st[a.off_phi + q * LP + lcol]; };
       auto psi = [&](int q) { return st[a.off_psiy + q * LP + lcol]; };  // LIPSI rows then Y rows
-      double* bm = bm_area + lcol * N2;
       if (passF && role == 1) {
         // ---- mean: mu'_i = Li^T (y_i - Li S_{i-1,i}^T mu'_{i-1})
         double m[N];
@@ -531,22 +538,7 @@ select_step_v3_kernel(const __grid_constant__ Args a) {
           mprev[r] = m[r];
           dprev[r] = dl[r];
         }
-        // ---- U' Phi_{i+1}^{-1} for role A
-        if (i + 1 < K) {
-#pragma unroll
-          for (int r = 0; r < N; ++r)
-#pragma unroll
-            for (int q = 0; q < N; ++q) {
-              double t = 0.0;
-#pragma unroll
-              for (int k2 = 0; k2 < N; ++k2)
-                t += ((kv(a.rK[1] + r * N + k2) * inv_t + pv(a.rF[4] + r * N + k2) * inv_b) * c) *
-                     phi(k2 >= q ? tri_idx(k2, q) : tri_idx(q, k2));
-              bm[r * N + q] = t;
-            }
-        }
       }
-      __syncwarp();
       if (passF && role == 0) {
         // ---- tr(Lambda_ii Sigma_ii)
 #pragma unroll
@@ -569,9 +561,20 @@ select_step_v3_kernel(const __grid_constant__ Args a) {
         }
         if (i + 1 < K) {
           // M = Sigma_ii U' Phi^{-1} = -Sigma_{i,i+1};  Sigma_{i+1} = Phi^{-1} + (U' Phi^{-1})^T M
-          double Up[N2], M[N2];
+          double Up[N2], M[N2], bm[N2];
 #pragma unroll
           for (int q = 0; q < N2; ++q) Up[q] = (kv(a.rK[1] + q) * inv_t + pv(a.rF[4] + q) * inv_b) * c;
+          // U' Phi_{i+1}^{-1}
+#pragma unroll
+          for (int r = 0; r < N; ++r)
+#pragma unroll
+            for (int q = 0; q < N; ++q) {
+              double t = 0.0;
+#pragma unroll
+              for (int k2 = 0; k2 < N; ++k2)
+                t += Up[r * N + k2] * phi(k2 >= q ? tri_idx(k2, q) : tri_idx(q, k2));
+              bm[r * N + q] = t;
+            }
 #pragma unroll
           for (int r = 0; r < N; ++r)
 #pragma unroll
@@ -611,11 +614,17 @@ select_step_v3_kernel(const __grid_constant__ Args a) {
     __syncthreads();
 
     // ---------------- KL of each lane: role A holds trace + log det, role B mahal + shift
-    // each thread sends its own quantity: A -> trace, ptr, log det; B -> mahal, pq, shift
-    const double o_trace_or_mahal = __shfl_xor_sync(0xffffffffu, role == 0 ? trace : mahal, 1);
-    const double o_ld = __shfl_xor_sync(0xffffffffu, ld_sum, 1);
-    const double o_sh = __shfl_xor_sync(0xffffffffu, sh2, 1);
-    const double o_pq = __shfl_xor_sync(0xffffffffu, role == 0 ? ptr_c : pq_c, 1);
+    // each role publishes its quantities: A -> trace, ptr, log det; B -> mahal, pq, shift
+    xch[(0 * 2 + role) * LP + lcol] = role == 0 ? trace : mahal;
+    xch[(1 * 2 + role) * LP + lcol] = ld_sum;
+    xch[(2 * 2 + role) * LP + lcol] = sh2;
+    xch[(3 * 2 + role) * LP + lcol] = role == 0 ? ptr_c : pq_c;
+    __syncthreads();
+    const double o_trace_or_mahal = xch[(0 * 2 + 1 - role) * LP + lcol];
+    const double o_ld = xch[(1 * 2 + 1 - role) * LP + lcol];
+    const double o_sh = xch[(2 * 2 + 1 - role) * LP + lcol];
+    const double o_pq = xch[(3 * 2 + 1 - role) * LP + lcol];
+    __syncthreads();
     const double tr_ = role == 0 ? trace : o_trace_or_mahal;
     const double mh_ = role == 0 ? o_trace_or_mahal : mahal;
     const double ld_ = role == 0 ? ld_sum : o_ld;
@@ -642,16 +651,16 @@ select_step_v3_kernel(const __grid_constant__ Args a) {
     int r_res[L], r_on[L], r_fail[L];
 #pragma unroll
     for (int q = 0; q < L; ++q) {
-      r_kl[q] = __shfl_sync(gmask, klv, 2 * q, GW);
-      r_res[q] = __shfl_sync(gmask, res, 2 * q, GW);
-      r_on[q] = __shfl_sync(gmask, (int)lane_on, 2 * q, GW);
-      r_beta[q] = __shfl_sync(gmask, beta, 2 * q, GW);
-      r_fail[q] = __shfl_sync(gmask, fail_knot, 2 * q, GW);
+      r_kl[q] = __shfl_sync(gmask, klv, q, GW);
+      r_res[q] = __shfl_sync(gmask, res, q, GW);
+      r_on[q] = __shfl_sync(gmask, (int)lane_on, q, GW);
+      r_beta[q] = __shfl_sync(gmask, beta, q, GW);
+      r_fail[q] = __shfl_sync(gmask, fail_knot, q, GW);
     }
     if (phase >= 4) continue;
     auto feasible = [&](int q) { return r_res[q] == 0 && !(r_kl[q] > a.kl_bound); };
     auto fail = [&](int code, int w) {
-      if (tid % GW == 0) {
+      if (leader) {
         a.status[b] = code;
         a.where[b] = w;
         if (a.nprobes) a.nprobes[b] = nprobe;
@@ -792,9 +801,10 @@ int launch_select_step_v2(const V2Launch& q, cudaStream_t s) {
   }
   // threads per CTA: 2 per lane; enough CTAs to cover the SMs. Plans per CTA
   // must be even: a TMA box's first plan column must sit on a 16-byte boundary.
-  int TB = ((int64_t)q.nplans * L * 2 <= 148 * 64) ? 32 : 64;
-  if (4 * L > TB) TB = 4 * L;
-  const int P = TB / (2 * L);
+  // two warps per 32 lane slots (warp-specialised roles); 32 / L plans per CTA
+  // (even for L <= 16, so every TMA box starts on a 16-byte plan boundary)
+  const int TB = 64;
+  const int P = 32 / L;
   const int Pb = round_up(P, 2);
   const int Kb = q.kshared ? 2 : Pb;
   const int n = q.n;
@@ -856,7 +866,7 @@ int launch_select_step_v2(const V2Launch& q, cudaStream_t s) {
   a.off_psiy = a.off_phi + round_up(T * LPb, 16);
   a.stage_doubles = a.off_psiy + round_up((T + n) * LPb, 16);
   a.bm_off = v3::kStages * a.stage_doubles;
-  a.bar_off = a.bm_off + round_up(P * L * N2, 16);
+  a.bar_off = a.bm_off + round_up(8 * P * L, 16);  // role exchange: 4 doubles x 2 roles per slot
   a.bytes_B = (uint32_t)(((2 * T + 3 * n + N2) * Pb + (T + N2) * Kb) * 8);
   a.bytes_F = (uint32_t)(((2 * T + 2 * n + N2) * Pb + (T + N2) * Kb + (2 * T + n) * LPb) * 8);
   (void)SE;
