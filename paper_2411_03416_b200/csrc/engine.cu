@@ -234,7 +234,7 @@ struct gvp_engine {
   int iteration_body() {
     int r = launch_select_step_v2(step_args(), stream);
     if (r) return r;
-    ++launches;
+    launches += 2;  // bisection + commit
     if ((r = factors())) return r;
     return control();
   }
@@ -242,9 +242,11 @@ struct gvp_engine {
 
 static int pick_lanes(const gvp_plan_config* cfg, int B) {
   if (cfg->spec_lanes > 0) return cfg->spec_lanes;
-  // fill the GPU: ~2 warps per SM of candidate lanes, at most 32 per plan
+  // Speculative lanes only pay while the GPU has idle SMs: measured on B200
+  // (C5, 4096 plans x 1001 knots) one lane per plan beats 4/8/16 lanes, while
+  // a single plan gains ~2x from 16 lanes. Aim at <= ~2 CTAs (4 warps) per SM.
   int L = 1;
-  while (L < 16 && (int64_t)B * L * 2 < 148 * 64) L *= 2;
+  while (L < 16 && (int64_t)B * L < 148 * 16) L *= 2;
   if (L == 2) L = 4;
   return L;
 }
@@ -434,7 +436,7 @@ extern "C" int gvp_engine_step(gvp_engine* e, int32_t iters, int32_t sync) {
       e->launches = before;  // counted per replay below
     }
     GVP_CUDA(cudaGraphLaunch(e->graph, s));
-    e->launches += 2 + (e->K > 2);
+    e->launches += 3 + (e->K > 2);
     ++e->iters_launched;
   }
   if (sync) GVP_CUDA(cudaStreamSynchronize(s));
@@ -450,7 +452,7 @@ extern "C" int gvp_engine_step_profiled(gvp_engine* e, int32_t iters, double* ms
     GVP_CUDA(cudaEventRecord(ev[0], s));
     int r = launch_select_step_v2(e->step_args(), s);
     if (r) return r;
-    ++e->launches;
+    e->launches += 2;
     GVP_CUDA(cudaEventRecord(ev[1], s));
     if ((r = e->factors())) return r;
     GVP_CUDA(cudaEventRecord(ev[2], s));

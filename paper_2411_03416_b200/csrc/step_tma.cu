@@ -157,8 +157,13 @@ struct Args {
   uint32_t bytes_B, bytes_F;
 };
 
-template <int N, int L>
-__global__ void __launch_bounds__(128)
+// COMMIT = false: the bisection; the accepted beta goes to a.beta[b].
+// COMMIT = true (L = 1): one write-mode probe at a.beta[b] producing the next
+// iterate, its marginals, KL, log det, prior cost and Lambda' mu'. Keeping the
+// write path out of the bisection kernel keeps its loop bodies small enough
+// for the instruction cache.
+template <int N, int L, bool COMMIT>
+__global__ void __launch_bounds__(64)
 select_step_v3_kernel(const __grid_constant__ Args a) {
   using Y = Ly<N>;
   constexpr int T = Y::T, N2 = Y::N2, SE = Y::SE;
@@ -191,9 +196,10 @@ select_step_v3_kernel(const __grid_constant__ Args a) {
   uint32_t uses[kStages] = {0, 0, 0, 0};  // per-slot completed-phase counters (uniform)
 
   // ---- per-plan bisection state (identical in every thread of the group)
-  const bool plan_ok = (b < a.B) && (!a.active || a.active[b]);
-  int phase = plan_ok ? 0 : 4;  // 0 first round, 1 beta_min (L==1), 2 bisect, 3 commit, 4 done
-  double lo = a.beta_min, hi = a.beta_max, best = a.beta_max;
+  const bool plan_ok = (b < a.B) && (!a.active || a.active[b]) && (!COMMIT || a.status[b] == GVP_OK);
+  // 0 first round, 1 beta_min (L==1), 2 bisect, 3 commit, 4 done
+  int phase = plan_ok ? (COMMIT ? 3 : 0) : 4;
+  double lo = a.beta_min, hi = a.beta_max, best = (COMMIT && plan_ok) ? a.beta[b] : a.beta_max;
   const double temp = plan_ok ? a.temp[b] : 1.0;
   const double ldc = plan_ok ? a.ld_cur[b] : 0.0;
   int nprobe = 0;
@@ -257,7 +263,7 @@ select_step_v3_kernel(const __grid_constant__ Args a) {
     } else if (phase == 1 && lane == 0) {
       lane_on = true;
       beta = a.beta_min;
-    } else if (phase == 3 && lane == 0) {
+    } else if (COMMIT && phase == 3 && lane == 0) {
       lane_on = true;
       write = true;
       beta = best;
@@ -479,7 +485,7 @@ select_step_v3_kernel(const __grid_constant__ Args a) {
             for (int q = 0; q < N; ++q) t += dprev[r] * pvp(a.rF[4] + r * N + q) * dl[q];
           mahal += 2.0 * t;
         }
-        if (write) {
+        if (COMMIT && write) {
           double dp[N], Pn[T];
 #pragma unroll
           for (int q = 0; q < T; ++q)
@@ -546,7 +552,7 @@ select_step_v3_kernel(const __grid_constant__ Args a) {
 #pragma unroll
           for (int q = 0; q <= r; ++q)
             trace += ((q == r) ? 1.0 : 2.0) * pv(a.rF[0] + tri_idx(r, q)) * Sig[tri_idx(r, q)];
-        if (write) {
+        if (COMMIT && write) {
 #pragma unroll
           for (int q = 0; q < T; ++q) {
             a.o_ld[(i * T + q) * a.Bp + b] =
@@ -588,7 +594,7 @@ select_step_v3_kernel(const __grid_constant__ Args a) {
 #pragma unroll
           for (int q = 0; q < N2; ++q) tc += pv(a.rF[4] + q) * M[q];
           trace -= 2.0 * tc;  // 2 <Lambda_{i,i+1}, Sigma_{i,i+1}>
-          if (write) {
+          if (COMMIT && write) {
             double tk = 0.0;
 #pragma unroll
             for (int q = 0; q < N2; ++q) {
@@ -635,15 +641,12 @@ select_step_v3_kernel(const __grid_constant__ Args a) {
       const double x = 0.5 * ((((tr_ + mh_) - (double)(K * N)) + ld_) - ldc);
       klv = (0.0 > x) ? 0.0 : x;  // python max(x, 0.0): NaN stays NaN
     }
-    if (write && role == 0) {
+    if (COMMIT && write && role == 0) {
       a.beta[b] = best;
       a.kl[b] = klv;
       a.ld_next[b] = ld_;
       a.shift[b] = sqrt(sh_);
       if (a.prior_cost) a.prior_cost[b] = 0.5 * pq_ + 0.5 * ptr_;
-      a.status[b] = GVP_OK;
-      a.where[b] = -1;
-      if (a.nprobes) a.nprobes[b] = nprobe;
     }
 
     // ---------------- group decision (the reference's sequential logic)
@@ -733,6 +736,15 @@ select_step_v3_kernel(const __grid_constant__ Args a) {
     } else if (phase == 2) {
       if (walk(0, tree_depth(L))) phase = ((hi - lo) > 1e-3 * hi) ? 2 : 3;
     }
+    if (!COMMIT && phase == 3) {  // search finished: hand beta to the commit kernel
+      if (leader) {
+        a.beta[b] = best;
+        a.status[b] = GVP_OK;
+        a.where[b] = -1;
+        if (a.nprobes) a.nprobes[b] = nprobe;
+      }
+      phase = 4;
+    }
   }
 }
 
@@ -788,19 +800,7 @@ int64_t step_plan_stride(int nplans) { return std::max<int64_t>(2, ((int64_t)npl
 
 static int round_up(int x, int m) { return (x + m - 1) / m * m; }
 
-int launch_select_step_v2(const V2Launch& q, cudaStream_t s) {
-  if (q.nplans == 0 || q.K == 0) return GVP_OK;
-  const int L = q.lanes;
-  if (L != 1 && L != 4 && L != 8 && L != 16) {
-    set_error("lanes must be 1, 4, 8 or 16");
-    return GVP_ERR_ARG;
-  }
-  if (q.Bp % 2 || q.Bp < 2) {
-    set_error("plan stride must be even (step_plan_stride)");
-    return GVP_ERR_ARG;
-  }
-  // threads per CTA: 2 per lane; enough CTAs to cover the SMs. Plans per CTA
-  // must be even: a TMA box's first plan column must sit on a 16-byte boundary.
+static int launch_v3(const V2Launch& q, const int L, const bool commit, cudaStream_t s) {
   // two warps per 32 lane slots (warp-specialised roles); 32 / L plans per CTA
   // (even for L <= 16, so every TMA box starts on a 16-byte plan boundary)
   const int TB = 64;
@@ -872,18 +872,22 @@ int launch_select_step_v2(const V2Launch& q, cudaStream_t s) {
   (void)SE;
   const size_t bytes = (size_t)(a.bar_off + 2 * v3::kStages) * sizeof(double) + 1024;
   const unsigned grid = (unsigned)((q.nplans + P - 1) / P);
-#define GVP_V3(NN, LL)                                                                        \
+#define GVP_V3(NN, LL, CC)                                                                    \
   {                                                                                           \
-    GVP_CUDA(cudaFuncSetAttribute(v3::select_step_v3_kernel<NN, LL>,                          \
+    GVP_CUDA(cudaFuncSetAttribute(v3::select_step_v3_kernel<NN, LL, CC>,                      \
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));  \
-    v3::select_step_v3_kernel<NN, LL><<<grid, TB, bytes, s>>>(a);                             \
+    v3::select_step_v3_kernel<NN, LL, CC><<<grid, TB, bytes, s>>>(a);                         \
   }
-#define GVP_V3_L(NN)                  \
-  switch (L) {                        \
-    case 1: GVP_V3(NN, 1) break;      \
-    case 4: GVP_V3(NN, 4) break;      \
-    case 8: GVP_V3(NN, 8) break;      \
-    default: GVP_V3(NN, 16) break;    \
+#define GVP_V3_L(NN)                           \
+  if (commit) {                                \
+    GVP_V3(NN, 1, true)                        \
+  } else {                                     \
+    switch (L) {                               \
+      case 1: GVP_V3(NN, 1, false) break;      \
+      case 4: GVP_V3(NN, 4, false) break;      \
+      case 8: GVP_V3(NN, 8, false) break;      \
+      default: GVP_V3(NN, 16, false) break;    \
+    }                                          \
   }
   switch (n) {
     case 2: GVP_V3_L(2) break;
@@ -897,6 +901,23 @@ int launch_select_step_v2(const V2Launch& q, cudaStream_t s) {
 #undef GVP_V3
   GVP_CUDA(cudaGetLastError());
   return GVP_OK;
+}
+
+// bisection (L candidate lanes per plan), then the commit of the accepted beta
+int launch_select_step_v2(const V2Launch& q, cudaStream_t s) {
+  if (q.nplans == 0 || q.K == 0) return GVP_OK;
+  const int L = q.lanes;
+  if (L != 1 && L != 4 && L != 8 && L != 16) {
+    set_error("lanes must be 1, 4, 8 or 16");
+    return GVP_ERR_ARG;
+  }
+  if (q.Bp % 2 || q.Bp < 2) {
+    set_error("plan stride must be even (step_plan_stride)");
+    return GVP_ERR_ARG;
+  }
+  int r = launch_v3(q, L, false, s);
+  if (r) return r;
+  return launch_v3(q, 1, true, s);
 }
 
 }  // namespace gvp

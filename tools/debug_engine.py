@@ -1,17 +1,19 @@
-"""Engine smoke at a given batch size / lane count (debugging aid)."""
-import os, sys
+"""Engine timing at a given batch size / lane count on the C5 problem shape (debugging aid)."""
+import os, sys, time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
+import bench
 import paper_2411_03416_b200 as P
 
-B = int(sys.argv[1]); lanes = int(sys.argv[2]); iters = int(sys.argv[3]) if len(sys.argv) > 3 else 3
-sdf = P.rasterize([P.sdf.Disc(center=np.array([1.1, 0.55]), radius=0.45)], bounds=[[-2, 4], [-2, 4]], cell_size=0.05)
-env = P.Environment(sdf, P.CollisionModel(0.2, 8.0))
-sys_ltv = P.point_robot_lti(2)(50, 3.0 / 50)
-cfg = P.OptimizerConfig(k_q=3, kl_bound=10.0, beta_max=0.5, max_iters=iters)
-goals = np.tile(np.array([2.0, 1.5, 0, 0]), (B, 1))
-try:
-    r = P.run_pgvimp_batch(sys_ltv, env, cfg, np.zeros(4), goals, 1.0, 1e-3, spec_lanes=lanes)
-    print(f"B={B} lanes={lanes} ok iters={r.iterations[:4]} status={set(r.status.tolist())}")
-except Exception as e:
-    print(f"B={B} lanes={lanes} FAIL {str(e)[:120]}")
+B = int(sys.argv[1]); lanes = int(sys.argv[2]); iters = int(sys.argv[3]) if len(sys.argv) > 3 else 4
+goals = bench.c5_goals(B)
+prior, info, pmean, init = bench.build_problem(P, goals)
+K, n = bench.N_INTERVALS + 1, 4
+eng = P.PlanBatch(B, K, n, bench.c2_map(P), P.CollisionModel(0.2, 8.0), P.smolyak_rule(3, 4),
+                  bench.c5_cfg(P, iters + 2), shared_prior=True, spec_lanes=lanes)
+eng.load(prior.prec.diag_stack, prior.prec.off_stack, info, pmean, init)
+eng.step(1, sync=True)
+ms = eng.step_profiled(iters)
+s = eng.summary()
+print(f"B={B} lanes={eng.lanes()} ms/iter select={ms[0]/iters:.2f} factor={ms[1]/iters:.3f} control={ms[2]/iters:.3f} "
+      f"status={set(s['status'].tolist())} iters={s['iterations'][:3]}")
