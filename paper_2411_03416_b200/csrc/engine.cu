@@ -246,7 +246,7 @@ static int pick_lanes(const gvp_plan_config* cfg, int B) {
   // (C5, 4096 plans x 1001 knots) one lane per plan beats 4/8/16 lanes, while
   // a single plan gains ~2x from 16 lanes. Aim at <= ~2 CTAs (4 warps) per SM.
   int L = 1;
-  while (L < 16 && (int64_t)B * L < 148 * 16) L *= 2;
+  while (L < 16 && (int64_t)B * L < 148 * 64) L *= 2;
   if (L == 2) L = 4;
   return L;
 }

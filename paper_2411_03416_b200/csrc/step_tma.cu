@@ -134,6 +134,36 @@ struct Ly {
   static constexpr int SE = 2 * T + N, S_PHI = 0, S_LIPSI = T, S_Y = 2 * T;
 };
 
+// Compile-time shared-memory layout of one CTA (32 lane slots = P plans x L
+// lanes, two warps). Every TMA box lands on a 128-byte boundary: row starts
+// are rounded to a multiple of cx_gran(width) rows.
+constexpr int cx_round(int x, int m) { return (x + m - 1) / m * m; }
+constexpr int cx_gran(int w) { return w % 16 == 0 ? 1 : w % 8 == 0 ? 2 : w % 4 == 0 ? 4 : w % 2 == 0 ? 8 : 16; }
+template <int N, int L, bool KS>
+struct Lay {
+  static constexpr int T = N * (N + 1) / 2, N2 = N * N;
+  static constexpr int P = 32 / L, Pb = P, Kb = KS ? 2 : P, LPb = 32;
+  static constexpr int gP = cx_gran(Pb), gK = cx_gran(Kb);
+  // pass B plan rows: LD T | GD T | G N | ETA N | V N | LO N2
+  static constexpr int B0 = 0, B1 = cx_round(B0 + T, gP), B2 = cx_round(B1 + T, gP),
+                       B3 = cx_round(B2 + N, gP), B4 = cx_round(B3 + N, gP),
+                       B5 = cx_round(B4 + N, gP), BR = cx_round(B5 + N2, gP);
+  // pass F plan rows: LD T | GD T | MU N | PM N | LO N2
+  static constexpr int F0 = 0, F1 = cx_round(F0 + T, gP), F2 = cx_round(F1 + T, gP),
+                       F3 = cx_round(F2 + N, gP), F4 = cx_round(F3 + N, gP),
+                       FR = cx_round(F4 + N2, gP);
+  // prior rows: KD T | KO N2
+  static constexpr int K0 = 0, K1 = cx_round(T, gK), KR = cx_round(K1 + N2, gK);
+  static constexpr int OFF_PLAN = 0, OFF_PRIOR = cx_round((BR > FR ? BR : FR) * Pb, 16),
+                       OFF_PHI = OFF_PRIOR + cx_round(KR * Kb, 16),
+                       OFF_PSIY = OFF_PHI + cx_round(T * LPb, 16),
+                       STAGE = OFF_PSIY + cx_round((T + N) * LPb, 16);
+  static constexpr int XCH = kStages * STAGE, BAR = XCH + 8 * 32;
+  static constexpr size_t BYTES = (size_t)(BAR + 2 * kStages) * 8;
+  static constexpr uint32_t TX_B = ((2 * T + 3 * N + N2) * Pb + (T + N2) * Kb) * 8;
+  static constexpr uint32_t TX_F = ((2 * T + 2 * N + N2) * Pb + (T + N2) * Kb + (2 * T + N) * LPb) * 8;
+};
+
 struct Args {
   CUtensorMap m_ld, m_lo, m_kd, m_ko, m_gd, m_g, m_eta, m_v, m_mu, m_pm, m_phi, m_psiy;
   int B;
@@ -162,14 +192,17 @@ struct Args {
 // iterate, its marginals, KL, log det, prior cost and Lambda' mu'. Keeping the
 // write path out of the bisection kernel keeps its loop bodies small enough
 // for the instruction cache.
-template <int N, int L, bool COMMIT>
+template <int N, int L, bool COMMIT, bool KS>
 __global__ void __launch_bounds__(64)
 select_step_v3_kernel(const __grid_constant__ Args a) {
   using Y = Ly<N>;
+  using LO = Lay<N, L, KS>;
   constexpr int T = Y::T, N2 = Y::N2, SE = Y::SE;
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  double* smem = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + a.bar_off);
+  // dynamic shared memory only (no static __shared__): the window starts
+  // 1 KB-aligned, so the compile-time layout keeps every TMA box 128-B aligned
+  // and all stage reads are LDS with immediate offsets
+  extern __shared__ __align__(1024) double smem[];
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + LO::BAR);
   const int tid = threadIdx.x;
   // warp-specialised roles: even warps run chain A, odd warps chain B for the
   // same 32 lane slots, so neither chain diverges inside a warp
@@ -177,15 +210,15 @@ select_step_v3_kernel(const __grid_constant__ Args a) {
   const int lcol = ((tid >> 6) << 5) | (tid & 31);  // lane slot in the CTA
   const int lane = lcol % L;
   const int p = lcol / L;
-  const int P = a.P, Pb = a.Pbox, Kb = a.Kbox;
-  const int LP = P * L;                       // lanes per CTA
+  constexpr int P = LO::P, Pb = LO::Pb, Kb = LO::Kb;
+  constexpr int LP = P * L;                   // lanes per CTA (= 32)
   const int64_t b0 = (int64_t)blockIdx.x * P;
   const int64_t b = b0 + p;
   const int64_t K = a.K;
-  const int kcol = a.ksp ? p : 0;             // prior column in its box
+  const int kcol = KS ? 0 : p;                // prior column in its box
   constexpr int GW = L;                       // group width in threads (<= 16, inside a warp)
   const unsigned gmask = ((1u << GW) - 1u) << ((tid & 31) / GW * GW);
-  double* xch = smem + a.bm_off;              // per-slot exchange between the two roles
+  double* xch = smem + LO::XCH;              // per-slot exchange between the two roles
   const bool leader = role == 0 && lane == 0;
 
   if (tid == 0) {
@@ -196,7 +229,8 @@ select_step_v3_kernel(const __grid_constant__ Args a) {
   uint32_t uses[kStages] = {0, 0, 0, 0};  // per-slot completed-phase counters (uniform)
 
   // ---- per-plan bisection state (identical in every thread of the group)
-  const bool plan_ok = (b < a.B) && (!a.active || a.active[b]) && (!COMMIT || a.status[b] == GVP_OK);
+  const bool plan_ok = (p < P) && (b < a.B) && (!a.active || a.active[b]) &&
+                       (!COMMIT || a.status[b] == GVP_OK);
   // 0 first round, 1 beta_min (L==1), 2 bisect, 3 commit, 4 done
   int phase = plan_ok ? (COMMIT ? 3 : 0) : 4;
   double lo = a.beta_min, hi = a.beta_max, best = (COMMIT && plan_ok) ? a.beta[b] : a.beta_max;
@@ -215,32 +249,32 @@ select_step_v3_kernel(const __grid_constant__ Args a) {
   double* scr = a.scratch;
   const int64_t sc_col = b0 * L + lcol;  // global scratch column
 
-  auto slot = [&](int64_t s) { return smem + (s % kStages) * a.stage_doubles; };
+  auto slot = [&](int64_t s) { return smem + (s % kStages) * LO::STAGE; };
   // issue the TMA loads of one knot of a pass into slot s % kStages
   auto issue = [&](int64_t s, int64_t i, bool passB) {
     double* st = slot(s);
     uint64_t* bar = &bars[s % kStages];
-    mbar_expect_tx(bar, passB ? a.bytes_B : a.bytes_F);
-    const int ck = (int)(b0 * a.ksp);
-    double* pl = st + a.off_plan;
-    double* pr = st + a.off_prior;
-    tma3(pr + a.rK[0] * Kb, &a.m_kd, ck, 0, (int)i, bar);
-    tma3(pr + a.rK[1] * Kb, &a.m_ko, ck, 0, (int)i, bar);
+    mbar_expect_tx(bar, passB ? LO::TX_B : LO::TX_F);
+    const int ck = KS ? 0 : (int)b0;
+    double* pl = st + LO::OFF_PLAN;
+    double* pr = st + LO::OFF_PRIOR;
+    tma3(pr + LO::K0 * Kb, &a.m_kd, ck, 0, (int)i, bar);
+    tma3(pr + LO::K1 * Kb, &a.m_ko, ck, 0, (int)i, bar);
     if (passB) {
-      tma3(pl + a.rB[0] * Pb, &a.m_ld, (int)b0, 0, (int)i, bar);
-      tma3(pl + a.rB[1] * Pb, &a.m_gd, (int)b0, 0, (int)i, bar);
-      tma3(pl + a.rB[2]* Pb, &a.m_g, (int)b0, 0, (int)i, bar);
-      tma3(pl + a.rB[3] * Pb, &a.m_eta, (int)b0, 0, (int)i, bar);
-      tma3(pl + a.rB[4]* Pb, &a.m_v, (int)b0, 0, (int)i, bar);
-      tma3(pl + a.rB[5] * Pb, &a.m_lo, (int)b0, 0, (int)i, bar);
+      tma3(pl + LO::B0 * Pb, &a.m_ld, (int)b0, 0, (int)i, bar);
+      tma3(pl + LO::B1 * Pb, &a.m_gd, (int)b0, 0, (int)i, bar);
+      tma3(pl + LO::B2* Pb, &a.m_g, (int)b0, 0, (int)i, bar);
+      tma3(pl + LO::B3 * Pb, &a.m_eta, (int)b0, 0, (int)i, bar);
+      tma3(pl + LO::B4* Pb, &a.m_v, (int)b0, 0, (int)i, bar);
+      tma3(pl + LO::B5 * Pb, &a.m_lo, (int)b0, 0, (int)i, bar);
     } else {
-      tma3(pl + a.rF[0] * Pb, &a.m_ld, (int)b0, 0, (int)i, bar);
-      tma3(pl + a.rF[1] * Pb, &a.m_gd, (int)b0, 0, (int)i, bar);
-      tma3(pl + a.rF[2] * Pb, &a.m_mu, (int)b0, 0, (int)i, bar);
-      tma3(pl + a.rF[3] * Pb, &a.m_pm, (int)b0, 0, (int)i, bar);
-      tma3(pl + a.rF[4] * Pb, &a.m_lo, (int)b0, 0, (int)i, bar);
-      tma3(st + a.off_phi, &a.m_phi, (int)(b0 * L), 0, (int)(i + 1), bar);        // PHIINV of knot i+1
-      tma3(st + a.off_psiy, &a.m_psiy, (int)(b0 * L), Y::S_LIPSI, (int)i, bar);  // LIPSI | Y of knot i
+      tma3(pl + LO::F0 * Pb, &a.m_ld, (int)b0, 0, (int)i, bar);
+      tma3(pl + LO::F1 * Pb, &a.m_gd, (int)b0, 0, (int)i, bar);
+      tma3(pl + LO::F2 * Pb, &a.m_mu, (int)b0, 0, (int)i, bar);
+      tma3(pl + LO::F3 * Pb, &a.m_pm, (int)b0, 0, (int)i, bar);
+      tma3(pl + LO::F4 * Pb, &a.m_lo, (int)b0, 0, (int)i, bar);
+      tma3(st + LO::OFF_PHI, &a.m_phi, (int)(b0 * L), 0, (int)(i + 1), bar);        // PHIINV of knot i+1
+      tma3(st + LO::OFF_PSIY, &a.m_psiy, (int)(b0 * L), Y::S_LIPSI, (int)i, bar);  // LIPSI | Y of knot i
     }
   };
   auto wait_slot = [&](int64_t s) {
@@ -303,24 +337,24 @@ select_step_v3_kernel(const __grid_constant__ Args a) {
       const int64_t i = K - 1 - s;
       if (!(lane_on && res == 0)) continue;
       const double* st = slot(s);
-      const double* pl = st + a.off_plan;
-      const double* pr = st + a.off_prior;
+      const double* pl = st + LO::OFF_PLAN;
+      const double* pr = st + LO::OFF_PRIOR;
       auto pv = [&](int row) { return pl[row * Pb + p]; };
       auto kv = [&](int row) { return pr[row * Kb + kcol]; };
       double A_[T];
       if (role == 0) {  // Lambda' diag block (optimizer.py:151-153), already symmetric
 #pragma unroll
         for (int q = 0; q < T; ++q)
-          A_[q] = ((pv(a.rB[1] + q) * two_t + kv(a.rK[0] + q) * inv_t) + pv(a.rB[0] + q) * inv_b) * c;
+          A_[q] = ((pv(LO::B1 + q) * two_t + kv(LO::K0 + q) * inv_t) + pv(LO::B0 + q) * inv_b) * c;
       } else {          // S diag block (optimizer.py:155)
 #pragma unroll
-        for (int q = 0; q < T; ++q) A_[q] = kv(a.rK[0] + q) * inv_t + pv(a.rB[0] + q) * inv_b;
+        for (int q = 0; q < T; ++q) A_[q] = kv(LO::K0 + q) * inv_t + pv(LO::B0 + q) * inv_b;
       }
       double rhs[N];
       if (role == 1) {
 #pragma unroll
         for (int r = 0; r < N; ++r)
-          rhs[r] = ((-pv(a.rB[2]+ r)) * inv_t + pv(a.rB[3] + r) * inv_t) + pv(a.rB[4]+ r) * inv_b;
+          rhs[r] = ((-pv(LO::B2+ r)) * inv_t + pv(LO::B3 + r) * inv_t) + pv(LO::B4+ r) * inv_b;
       }
       if (i < K - 1) {
         // off block: S_off = K_off/T + Lambda_off/beta; role A uses U' = c * S_off
@@ -333,7 +367,7 @@ select_step_v3_kernel(const __grid_constant__ Args a) {
             double t = 0.0;
 #pragma unroll
             for (int k2 = 0; k2 <= r; ++k2)
-              t += LiN[tri_idx(r, k2)] * ((kv(a.rK[1] + q * N + k2) * inv_t + pv(a.rB[5] + q * N + k2) * inv_b) * sc_);
+              t += LiN[tri_idx(r, k2)] * ((kv(LO::K1 + q * N + k2) * inv_t + pv(LO::B5 + q * N + k2) * inv_b) * sc_);
             W[r * N + q] = t;
           }
 #pragma unroll
@@ -396,11 +430,11 @@ select_step_v3_kernel(const __grid_constant__ Args a) {
     // like proximal_update raising before gbp_marginals, optimizer.py:203-207)
     {
       int* xi = reinterpret_cast<int*>(xch);  // [role][slot] result codes, then fail knots
-      xi[role * LP + lcol] = res;
-      xi[2 * LP + role * LP + lcol] = fail_knot;
+      xi[role * 32 + lcol] = res;  // 32 lane slots per warp pair
+      xi[64 + role * 32 + lcol] = fail_knot;
       __syncthreads();
-      const int other = xi[(1 - role) * LP + lcol];
-      const int otherk = xi[2 * LP + (1 - role) * LP + lcol];
+      const int other = xi[(1 - role) * 32 + lcol];
+      const int otherk = xi[64 + (1 - role) * 32 + lcol];
       __syncthreads();
       const int rA = role == 0 ? res : other, rB = role == 0 ? other : res;
       const int kA = role == 0 ? fail_knot : otherk, kB = role == 0 ? otherk : fail_knot;
@@ -425,17 +459,17 @@ select_step_v3_kernel(const __grid_constant__ Args a) {
       __syncthreads();
       if (tid == 0 && i + kAhead < K) issue(s + kAhead, i + kAhead, false);
       const double* st = slot(s);
-      const double* pl = st + a.off_plan;
-      const double* pr = st + a.off_prior;
+      const double* pl = st + LO::OFF_PLAN;
+      const double* pr = st + LO::OFF_PRIOR;
       const double* stp = slot(s - 1);  // knot i-1 (valid when i > 0)
-      const double* plp = stp + a.off_plan;
-      const double* prp = stp + a.off_prior;
+      const double* plp = stp + LO::OFF_PLAN;
+      const double* prp = stp + LO::OFF_PRIOR;
       auto pv = [&](int row) { return pl[row * Pb + p]; };
       auto kv = [&](int row) { return pr[row * Kb + kcol]; };
       auto pvp = [&](int row) { return plp[row * Pb + p]; };
       auto kvp = [&](int row) { return prp[row * Kb + kcol]; };
-      auto phi = [&](int q) { return st[a.off_phi + q * LP + lcol]; };
-      auto psi = [&](int q) { return st[a.off_psiy + q * LP + lcol]; };  // LIPSI rows then Y rows
+      auto phi = [&](int q) { return st[LO::OFF_PHI + q * LP + lcol]; };
+      auto psi = [&](int q) { return st[LO::OFF_PSIY + q * LP + lcol]; };  // LIPSI rows then Y rows
       if (passF && role == 1) {
         // ---- mean: mu'_i = Li^T (y_i - Li S_{i-1,i}^T mu'_{i-1})
         double m[N];
@@ -447,7 +481,7 @@ select_step_v3_kernel(const __grid_constant__ Args a) {
             if (i > 0) {
 #pragma unroll
               for (int q = 0; q < N; ++q)
-                t += (kvp(a.rK[1] + q * N + r) * inv_t + pvp(a.rF[4] + q * N + r) * inv_b) * mprev[q];
+                t += (kvp(LO::K1 + q * N + r) * inv_t + pvp(LO::F4 + q * N + r) * inv_b) * mprev[q];
             }
             z[r] = t;
           }
@@ -469,37 +503,37 @@ select_step_v3_kernel(const __grid_constant__ Args a) {
         double dl[N];
 #pragma unroll
         for (int r = 0; r < N; ++r) {
-          dl[r] = pv(a.rF[2] + r) - m[r];  // delta = cur.mean - nxt.mean
+          dl[r] = pv(LO::F2 + r) - m[r];  // delta = cur.mean - nxt.mean
           sh2 += dl[r] * dl[r];
         }
 #pragma unroll
         for (int r = 0; r < N; ++r)
 #pragma unroll
           for (int q = 0; q <= r; ++q)
-            mahal += ((q == r) ? 1.0 : 2.0) * pv(a.rF[0] + tri_idx(r, q)) * dl[r] * dl[q];
+            mahal += ((q == r) ? 1.0 : 2.0) * pv(LO::F0 + tri_idx(r, q)) * dl[r] * dl[q];
         if (i > 0) {
           double t = 0.0;
 #pragma unroll
           for (int r = 0; r < N; ++r)
 #pragma unroll
-            for (int q = 0; q < N; ++q) t += dprev[r] * pvp(a.rF[4] + r * N + q) * dl[q];
+            for (int q = 0; q < N; ++q) t += dprev[r] * pvp(LO::F4 + r * N + q) * dl[q];
           mahal += 2.0 * t;
         }
         if (COMMIT && write) {
           double dp[N], Pn[T];
 #pragma unroll
           for (int q = 0; q < T; ++q)
-            Pn[q] = ((pv(a.rF[1] + q) * two_t + kv(a.rK[0] + q) * inv_t) + pv(a.rF[0] + q) * inv_b) * c;
+            Pn[q] = ((pv(LO::F1 + q) * two_t + kv(LO::K0 + q) * inv_t) + pv(LO::F0 + q) * inv_b) * c;
 #pragma unroll
           for (int r = 0; r < N; ++r) {
             a.o_mu[(i * N + r) * a.Bp + b] = m[r];
-            dp[r] = m[r] - pv(a.rF[3] + r);
+            dp[r] = m[r] - pv(LO::F3 + r);
           }
 #pragma unroll
           for (int r = 0; r < N; ++r)
 #pragma unroll
             for (int q = 0; q <= r; ++q)
-              pq_c += ((q == r) ? 1.0 : 2.0) * kv(a.rK[0] + tri_idx(r, q)) * dp[r] * dp[q];
+              pq_c += ((q == r) ? 1.0 : 2.0) * kv(LO::K0 + tri_idx(r, q)) * dp[r] * dp[q];
           double pt[N];
 #pragma unroll
           for (int r = 0; r < N; ++r) {
@@ -509,7 +543,7 @@ select_step_v3_kernel(const __grid_constant__ Args a) {
             if (i > 0) {
 #pragma unroll
               for (int q = 0; q < N; ++q)
-                t += ((kvp(a.rK[1] + q * N + r) * inv_t + pvp(a.rF[4] + q * N + r) * inv_b) * c) * mprev[q];
+                t += ((kvp(LO::K1 + q * N + r) * inv_t + pvp(LO::F4 + q * N + r) * inv_b) * c) * mprev[q];
             }
             pt[r] = t;
           }
@@ -518,14 +552,14 @@ select_step_v3_kernel(const __grid_constant__ Args a) {
 #pragma unroll
             for (int r = 0; r < N; ++r)
 #pragma unroll
-              for (int q = 0; q < N; ++q) t2 += dpprev[r] * kvp(a.rK[1] + r * N + q) * dp[q];
+              for (int q = 0; q < N; ++q) t2 += dpprev[r] * kvp(LO::K1 + r * N + q) * dp[q];
             pq_c += 2.0 * t2;
 #pragma unroll
             for (int r = 0; r < N; ++r) {
               double t = part[r];
 #pragma unroll
               for (int q = 0; q < N; ++q)
-                t += ((kvp(a.rK[1] + r * N + q) * inv_t + pvp(a.rF[4] + r * N + q) * inv_b) * c) * m[q];
+                t += ((kvp(LO::K1 + r * N + q) * inv_t + pvp(LO::F4 + r * N + q) * inv_b) * c) * m[q];
               a.o_v[((i - 1) * N + r) * a.Bp + b] = t;
             }
           }
@@ -551,25 +585,25 @@ select_step_v3_kernel(const __grid_constant__ Args a) {
         for (int r = 0; r < N; ++r)
 #pragma unroll
           for (int q = 0; q <= r; ++q)
-            trace += ((q == r) ? 1.0 : 2.0) * pv(a.rF[0] + tri_idx(r, q)) * Sig[tri_idx(r, q)];
+            trace += ((q == r) ? 1.0 : 2.0) * pv(LO::F0 + tri_idx(r, q)) * Sig[tri_idx(r, q)];
         if (COMMIT && write) {
 #pragma unroll
           for (int q = 0; q < T; ++q) {
             a.o_ld[(i * T + q) * a.Bp + b] =
-                ((pv(a.rF[1] + q) * two_t + kv(a.rK[0] + q) * inv_t) + pv(a.rF[0] + q) * inv_b) * c;
+                ((pv(LO::F1 + q) * two_t + kv(LO::K0 + q) * inv_t) + pv(LO::F0 + q) * inv_b) * c;
             a.o_cov[(i * T + q) * a.Bp + b] = Sig[q];
           }
 #pragma unroll
           for (int r = 0; r < N; ++r)
 #pragma unroll
             for (int q = 0; q <= r; ++q)
-              ptr_c += ((q == r) ? 1.0 : 2.0) * kv(a.rK[0] + tri_idx(r, q)) * Sig[tri_idx(r, q)];
+              ptr_c += ((q == r) ? 1.0 : 2.0) * kv(LO::K0 + tri_idx(r, q)) * Sig[tri_idx(r, q)];
         }
         if (i + 1 < K) {
           // M = Sigma_ii U' Phi^{-1} = -Sigma_{i,i+1};  Sigma_{i+1} = Phi^{-1} + (U' Phi^{-1})^T M
           double Up[N2], M[N2], bm[N2];
 #pragma unroll
-          for (int q = 0; q < N2; ++q) Up[q] = (kv(a.rK[1] + q) * inv_t + pv(a.rF[4] + q) * inv_b) * c;
+          for (int q = 0; q < N2; ++q) Up[q] = (kv(LO::K1 + q) * inv_t + pv(LO::F4 + q) * inv_b) * c;
           // U' Phi_{i+1}^{-1}
 #pragma unroll
           for (int r = 0; r < N; ++r)
@@ -592,7 +626,7 @@ select_step_v3_kernel(const __grid_constant__ Args a) {
             }
           double tc = 0.0;
 #pragma unroll
-          for (int q = 0; q < N2; ++q) tc += pv(a.rF[4] + q) * M[q];
+          for (int q = 0; q < N2; ++q) tc += pv(LO::F4 + q) * M[q];
           trace -= 2.0 * tc;  // 2 <Lambda_{i,i+1}, Sigma_{i,i+1}>
           if (COMMIT && write) {
             double tk = 0.0;
@@ -600,7 +634,7 @@ select_step_v3_kernel(const __grid_constant__ Args a) {
             for (int q = 0; q < N2; ++q) {
               a.o_cr[(i * N2 + q) * a.Bp + b] = -M[q];
               a.o_lo[(i * N2 + q) * a.Bp + b] = Up[q];
-              tk += kv(a.rK[1] + q) * M[q];
+              tk += kv(LO::K1 + q) * M[q];
             }
             ptr_c -= 2.0 * tk;
           }
@@ -621,15 +655,15 @@ select_step_v3_kernel(const __grid_constant__ Args a) {
 
     // ---------------- KL of each lane: role A holds trace + log det, role B mahal + shift
     // each role publishes its quantities: A -> trace, ptr, log det; B -> mahal, pq, shift
-    xch[(0 * 2 + role) * LP + lcol] = role == 0 ? trace : mahal;
-    xch[(1 * 2 + role) * LP + lcol] = ld_sum;
-    xch[(2 * 2 + role) * LP + lcol] = sh2;
-    xch[(3 * 2 + role) * LP + lcol] = role == 0 ? ptr_c : pq_c;
+    xch[(0 * 2 + role) * 32 + lcol] = role == 0 ? trace : mahal;
+    xch[(1 * 2 + role) * 32 + lcol] = ld_sum;
+    xch[(2 * 2 + role) * 32 + lcol] = sh2;
+    xch[(3 * 2 + role) * 32 + lcol] = role == 0 ? ptr_c : pq_c;
     __syncthreads();
-    const double o_trace_or_mahal = xch[(0 * 2 + 1 - role) * LP + lcol];
-    const double o_ld = xch[(1 * 2 + 1 - role) * LP + lcol];
-    const double o_sh = xch[(2 * 2 + 1 - role) * LP + lcol];
-    const double o_pq = xch[(3 * 2 + 1 - role) * LP + lcol];
+    const double o_trace_or_mahal = xch[(0 * 2 + 1 - role) * 32 + lcol];
+    const double o_ld = xch[(1 * 2 + 1 - role) * 32 + lcol];
+    const double o_sh = xch[(2 * 2 + 1 - role) * 32 + lcol];
+    const double o_pq = xch[(3 * 2 + 1 - role) * 32 + lcol];
     __syncthreads();
     const double tr_ = role == 0 ? trace : o_trace_or_mahal;
     const double mh_ = role == 0 ? o_trace_or_mahal : mahal;
@@ -804,6 +838,8 @@ static int launch_v3(const V2Launch& q, const int L, const bool commit, cudaStre
   // two warps per 32 lane slots (warp-specialised roles); 32 / L plans per CTA
   // (even for L <= 16, so every TMA box starts on a 16-byte plan boundary)
   const int TB = 64;
+  // Fill all 32 lane slots (B200, C5 at L = 1: 32 plans/CTA 47 ms vs 8 plans/CTA
+  // 104 ms — the per-knot TMA issue + barrier cost is paid per CTA).
   const int P = 32 / L;
   const int Pb = round_up(P, 2);
   const int Kb = q.kshared ? 2 : Pb;
@@ -866,18 +902,25 @@ static int launch_v3(const V2Launch& q, const int L, const bool commit, cudaStre
   a.off_psiy = a.off_phi + round_up(T * LPb, 16);
   a.stage_doubles = a.off_psiy + round_up((T + n) * LPb, 16);
   a.bm_off = v3::kStages * a.stage_doubles;
-  a.bar_off = a.bm_off + round_up(8 * P * L, 16);  // role exchange: 4 doubles x 2 roles per slot
+  a.bar_off = a.bm_off + 8 * 32;  // role exchange: 4 doubles x 2 roles x 32 lane slots
   a.bytes_B = (uint32_t)(((2 * T + 3 * n + N2) * Pb + (T + N2) * Kb) * 8);
   a.bytes_F = (uint32_t)(((2 * T + 2 * n + N2) * Pb + (T + N2) * Kb + (2 * T + n) * LPb) * 8);
   (void)SE;
   const size_t bytes = (size_t)(a.bar_off + 2 * v3::kStages) * sizeof(double) + 1024;
   const unsigned grid = (unsigned)((q.nplans + P - 1) / P);
-#define GVP_V3(NN, LL, CC)                                                                    \
-  {                                                                                           \
-    GVP_CUDA(cudaFuncSetAttribute(v3::select_step_v3_kernel<NN, LL, CC>,                      \
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));  \
-    v3::select_step_v3_kernel<NN, LL, CC><<<grid, TB, bytes, s>>>(a);                         \
+#define GVP_V3_KS(NN, LL, CC, KK)                                                               \
+  {                                                                                             \
+    using LOH = v3::Lay<NN, LL, KK>;                                                            \
+    if (LOH::TX_B != a.bytes_B || LOH::TX_F != a.bytes_F || LOH::STAGE != a.stage_doubles) {   \
+      set_error("internal: device/host stage layout mismatch");                                 \
+      return GVP_ERR_ARG;                                                                       \
+    }                                                                                           \
+    GVP_CUDA(cudaFuncSetAttribute(v3::select_step_v3_kernel<NN, LL, CC, KK>,                    \
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)LOH::BYTES)); \
+    v3::select_step_v3_kernel<NN, LL, CC, KK><<<grid, TB, LOH::BYTES, s>>>(a);                  \
   }
+#define GVP_V3(NN, LL, CC)                                 \
+  if (q.kshared) GVP_V3_KS(NN, LL, CC, true) else GVP_V3_KS(NN, LL, CC, false)
 #define GVP_V3_L(NN)                           \
   if (commit) {                                \
     GVP_V3(NN, 1, true)                        \
