@@ -53,6 +53,7 @@ int Field::build(const double* grid, int ndim, const int64_t* shape, const doubl
   f.oy = origin[1];
   f.oz = ndim == 3 ? origin[2] : 0.0;
   f.cell = cell;
+  f.inv_cell = 1.0 / cell;
   std::vector<double> packed;
   if (ndim == 2) {
     // corner-packed cells: (iy, ix) -> {g[iy][ix], g[iy][ix+1], g[iy+1][ix], g[iy+1][ix+1]}
@@ -155,6 +156,10 @@ int Rule::build(const double* points, const double* weights, int64_t npts, int n
                            cudaMemcpyHostToDevice, s));
   GVP_CUDA(cudaMemcpyAsync(d_cnt, cnt.data(), nproj * sizeof(int), cudaMemcpyHostToDevice, s));
   GVP_CUDA(cudaStreamSynchronize(s));
+  h_proj = proj;
+  h_mom = mom;
+  h_cnt = cnt;
+  dev.host = this;
   dev.n = n;
   dev.P = P;
   dev.npts = npts;
@@ -178,22 +183,17 @@ GVP_DEV double fadd(double a, double b) { return EXACT ? __dadd_rn(a, b) : a + b
 template <bool EXACT>
 GVP_DEV double fsub(double a, double b) { return EXACT ? __dsub_rn(a, b) : a - b; }
 
+// branch-free border clamp; same values as the reference's if/elif for finite u
 GVP_DEV double clamp_axis(double u, double top, bool& out) {
-  if (u < 0.0) {
-    out = true;
-    return 0.0;
-  }
-  if (u > top) {
-    out = true;
-    return top;
-  }
-  return u;
+  out = out || (u < 0.0) || (u > top);
+  return fmin(fmax(u, 0.0), top);
 }
 
 template <bool EXACT>
 GVP_DEV double interp2(const FieldDev& F, double px, double py, bool& out) {
-  double u = __ddiv_rn(__dsub_rn(px, F.ox), F.cell);
-  double v = __ddiv_rn(__dsub_rn(py, F.oy), F.cell);
+  // exact path divides like the reference; the fused path multiplies by 1/cell
+  double u = EXACT ? __ddiv_rn(__dsub_rn(px, F.ox), F.cell) : (px - F.ox) * F.inv_cell;
+  double v = EXACT ? __ddiv_rn(__dsub_rn(py, F.oy), F.cell) : (py - F.oy) * F.inv_cell;
   out = false;
   u = clamp_axis(u, (double)(F.nx - 1), out);
   v = clamp_axis(v, (double)(F.ny - 1), out);
@@ -218,9 +218,9 @@ GVP_DEV double interp2(const FieldDev& F, double px, double py, bool& out) {
 // trilinear (_kernels.pyx:48-90): two bilinear planes combined in z
 template <bool EXACT>
 GVP_DEV double interp3(const FieldDev& F, double px, double py, double pz, bool& out) {
-  double u = __ddiv_rn(__dsub_rn(px, F.ox), F.cell);
-  double v = __ddiv_rn(__dsub_rn(py, F.oy), F.cell);
-  double w = __ddiv_rn(__dsub_rn(pz, F.oz), F.cell);
+  double u = EXACT ? __ddiv_rn(__dsub_rn(px, F.ox), F.cell) : (px - F.ox) * F.inv_cell;
+  double v = EXACT ? __ddiv_rn(__dsub_rn(py, F.oy), F.cell) : (py - F.oy) * F.inv_cell;
+  double w = EXACT ? __ddiv_rn(__dsub_rn(pz, F.oz), F.cell) : (pz - F.oz) * F.inv_cell;
   out = false;
   u = clamp_axis(u, (double)(F.nx - 1), out);
   v = clamp_axis(v, (double)(F.ny - 1), out);
@@ -346,34 +346,58 @@ int launch_factor_moments(int64_t nfac, int n, const double* means, const double
 }
 
 // ===================================================== fused gradients kernel
-template <int N, int P>
-__global__ void __launch_bounds__(128)
+#ifndef GVP_FACTOR_MINBLOCKS
+#define GVP_FACTOR_MINBLOCKS 4
+#endif
+// projection tables of a rule with NP distinct projections, passed by value
+template <int NP, int P, int M>
+struct RuleConst {
+  double proj[NP * P];
+  double mom[NP * M];
+  int cnt[NP];
+};
+
+template <int N, int P, bool GRID2D, int NP>
+__global__ void __launch_bounds__(128, GVP_FACTOR_MINBLOCKS)
 factor_grads_kernel(int nplans, int64_t nfac, View mean, View covs, RuleDev R, FieldDev F,
                     double radius_eps, double sigma_obs, FactorOut out,
-                    const int* __restrict__ active) {
+                    const int* __restrict__ active,
+                    const __grid_constant__ RuleConst<(NP > 0 ? NP : 1), P, 1 + N + N * (N + 1) / 2> RC) {
   constexpr int T = N * (N + 1) / 2;
   constexpr int M = 1 + N + T;
-  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= nfac * nplans) return;
-  const int64_t b = t % nplans;
-  const int64_t f = t / nplans;
+  int64_t b, f;
+  if (GRID2D) {  // plans along x, factors along y: no integer division
+    b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    f = blockIdx.y;
+    if (b >= nplans) return;
+  } else {
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= nfac * nplans) return;
+    b = t % nplans;
+    f = t / nplans;
+  }
   const int64_t knot = f + 1;  // interior factors 1..N-1 (factors.py:159-164)
   if (active && !active[b]) return;
 
   double mu[N], S[N][N], L[N][N];
+  {
+    const double* mp = mean.p + knot * mean.sk + b * mean.sp;
+    const double* cp = covs.p + knot * covs.sk + b * covs.sp;
 #pragma unroll
-  for (int r = 0; r < N; ++r) mu[r] = mean(b, knot, r);
+    for (int r = 0; r < N; ++r) mu[r] = mp[r * mean.se];
 #pragma unroll
-  for (int r = 0; r < N; ++r)
+    for (int r = 0; r < N; ++r)
 #pragma unroll
-    for (int c = 0; c <= r; ++c) S[r][c] = covs(b, knot, tri_idx(r, c));  // packed lower
+      for (int c = 0; c <= r; ++c) S[r][c] = cp[tri_idx(r, c) * covs.se];  // packed lower
+  }
   // gaussian_sqrt (quadrature.py:164-177): Cholesky, then one 1e-10 jitter retry
   // np.linalg.cholesky has no 1e-300 pivot floor: FLOOR=false
-  bool ok = chol<N, false>(S, L);
+  double dinv[N];
+  bool ok = chol_fast<N, false>(S, L, dinv);
   if (!ok) {
 #pragma unroll
     for (int r = 0; r < N; ++r) S[r][r] += 1e-10;
-    ok = chol<N, false>(S, L);
+    ok = chol_fast<N, false>(S, L, dinv);
   }
   if (!ok) {  // the eigh root branch is not taken on device: report it
     atomicMax(out.status + b, GVP_ERR_SQRT);
@@ -388,35 +412,92 @@ factor_grads_kernel(int nplans, int64_t nfac, View mean, View covs, RuleDev R, F
 #pragma unroll
   for (int k = 0; k < T; ++k) E2[k] = 0.0;
   unsigned long long nout = 0;
-  for (int64_t j = 0; j < R.nproj; ++j) {
-    double pos[P];
+  if constexpr (NP > 0) {
+    // rule tables live in the kernel's parameter space: every projection
+    // coordinate and moment is a constant-bank operand of its DFMA (no loads),
+    // the loop is fully unrolled and the accumulation is branch-free
+    double psi[NP];
+    bool any_hit = false;
 #pragma unroll
-    for (int r = 0; r < P; ++r) {
-      double acc = 0.0;
+    for (int j = 0; j < NP; ++j) {
+      double pos[P];
 #pragma unroll
-      for (int k = 0; k <= r; ++k) acc += L[r][k] * __ldg(R.proj + j * P + k);
-      pos[r] = mu[r] + acc;
+      for (int r = 0; r < P; ++r) {
+        double acc = 0.0;
+#pragma unroll
+        for (int k = 0; k <= r; ++k) acc += L[r][k] * RC.proj[j * P + k];
+        pos[r] = mu[r] + acc;
+      }
+      bool o;
+      const double d = (P == 2) ? interp2<false>(F, pos[0], pos[1], o)
+                                : interp3<false>(F, pos[0], pos[1], pos[P - 1], o);
+      nout += o ? (unsigned long long)RC.cnt[j] : 0ull;
+      const double gap = radius_eps - d;
+      psi[j] = gap > 0.0 ? sigma_obs * gap * gap : 0.0;
+      any_hit = any_hit || (gap > 0.0);
     }
-    bool o;
-    const double d = (P == 2) ? interp2<false>(F, pos[0], pos[1], o)
-                              : interp3<false>(F, pos[0], pos[1], pos[P - 1], o);
-    if (o) nout += (unsigned long long)__ldg(R.cnt + j);
-    const double gap = radius_eps - d;
-    if (gap > 0.0) {
-      const double psi = sigma_obs * gap * gap;
-      const double* m = R.mom + j * M;
-      e0 += psi * __ldg(m);
+    if (!any_hit) {  // clear of every obstacle: all moments, gradients and e_psi are zero
+      if (nout) atomicAdd(out.oob + b, nout);
 #pragma unroll
-      for (int r = 0; r < N; ++r) E1[r] += psi * __ldg(m + 1 + r);
+      for (int r = 0; r < N; ++r) out.g_mu.p[knot * out.g_mu.sk + b * out.g_mu.sp + r * out.g_mu.se] = 0.0;
 #pragma unroll
-      for (int k = 0; k < T; ++k) E2[k] += psi * __ldg(m + 1 + N + k);
+      for (int k = 0; k < T; ++k)
+        out.g_diag.p[knot * out.g_diag.sk + b * out.g_diag.sp + k * out.g_diag.se] = 0.0;
+      out.e_psi(b, f, 0) = 0.0;
+      return;
     }
+#pragma unroll
+    for (int j = 0; j < NP; ++j) {
+      e0 += psi[j] * RC.mom[j * M];
+#pragma unroll
+      for (int r = 0; r < N; ++r) E1[r] += psi[j] * RC.mom[j * M + 1 + r];
+#pragma unroll
+      for (int k = 0; k < T; ++k) E2[k] += psi[j] * RC.mom[j * M + 1 + N + k];
+    }
+  } else {
+  // projections in chunks of CH: all CH cell gathers are issued before any
+  // hinge is evaluated, so their L1/L2 latencies overlap
+  constexpr int CH = 4;
+  for (int64_t j0 = 0; j0 < R.nproj; j0 += CH) {
+    double dist[CH];
+    bool o[CH];
+#pragma unroll
+    for (int u = 0; u < CH; ++u) {
+      const int64_t j = (j0 + u < R.nproj) ? j0 + u : R.nproj - 1;
+      double pos[P];
+#pragma unroll
+      for (int r = 0; r < P; ++r) {
+        double acc = 0.0;
+#pragma unroll
+        for (int k = 0; k <= r; ++k) acc += L[r][k] * __ldg(R.proj + j * P + k);
+        pos[r] = mu[r] + acc;
+      }
+      dist[u] = (P == 2) ? interp2<false>(F, pos[0], pos[1], o[u])
+                         : interp3<false>(F, pos[0], pos[1], pos[P - 1], o[u]);
+    }
+#pragma unroll
+    for (int u = 0; u < CH; ++u) {
+      const int64_t j = j0 + u;
+      if (j >= R.nproj) break;
+      if (o[u]) nout += (unsigned long long)__ldg(R.cnt + j);
+      const double gap = radius_eps - dist[u];
+      if (gap > 0.0) {
+        const double psi = sigma_obs * gap * gap;
+        const double* m = R.mom + j * M;
+        e0 += psi * __ldg(m);
+#pragma unroll
+        for (int r = 0; r < N; ++r) E1[r] += psi * __ldg(m + 1 + r);
+#pragma unroll
+        for (int k = 0; k < T; ++k) E2[k] += psi * __ldg(m + 1 + N + k);
+      }
+    }
+  }
   }
   if (nout) atomicAdd(out.oob + b, nout);
 
   // ---- moment-form gradients (factors.py:95-104) in the L^{-1} basis
   double Li[N][N];
-  tri_inv<N>(L, Li);
+  tri_inv_fast<N>(L, dinv, Li);
   bool finite = isfinite(e0);
 #pragma unroll
   for (int r = 0; r < N; ++r) finite = finite && isfinite(E1[r]);
@@ -433,7 +514,7 @@ factor_grads_kernel(int nplans, int64_t nfac, View mean, View covs, RuleDev R, F
     double acc = 0.0;
 #pragma unroll
     for (int k = r; k < N; ++k) acc += Li[k][r] * E1[k];
-    out.g_mu(b, knot, r) = acc;
+    out.g_mu.p[knot * out.g_mu.sk + b * out.g_mu.sp + r * out.g_mu.se] = acc;
   }
   // W = E2 L^{-1}  (E2 symmetric, packed)
   double W[N][N];
@@ -457,7 +538,8 @@ factor_grads_kernel(int nplans, int64_t nfac, View mean, View covs, RuleDev R, F
         hp += Li[k][r] * W[k][c];
         pp += Li[k][r] * Li[k][c];
       }
-      out.g_diag(b, knot, tri_idx(r, c)) = h0 * pp + 0.5 * hp;  // packed lower
+      out.g_diag.p[knot * out.g_diag.sk + b * out.g_diag.sp + tri_idx(r, c) * out.g_diag.se] =
+          h0 * pp + 0.5 * hp;  // packed lower
     }
   out.e_psi(b, f, 0) = e0 > 0.0 ? e0 : 0.0;  // e_psi = max(e0, 0) (factors.py:218-224)
 }
@@ -468,10 +550,35 @@ static int grads_impl(int nplans, int64_t K, const View& mean, const View& covs,
                       const int* active, cudaStream_t s) {
   const int64_t nfac = K - 2;
   if (nfac <= 0 || nplans == 0) return GVP_OK;
-  const int64_t total = nfac * nplans;
   const int tpb = 128;
-  factor_grads_kernel<N, P><<<(unsigned)((total + tpb - 1) / tpb), tpb, 0, s>>>(
-      nplans, nfac, mean, covs, R, F, re, so, out, active);
+  constexpr int M = 1 + N + N * (N + 1) / 2;
+  const Rule* host = static_cast<const Rule*>(R.host);
+  auto go = [&](auto np_tag) {
+    constexpr int NPc = decltype(np_tag)::value;
+    RuleConst<(NPc > 0 ? NPc : 1), P, M> rc{};
+    if (NPc > 0 && host) {
+      std::memcpy(rc.proj, host->h_proj.data(), sizeof(rc.proj));
+      std::memcpy(rc.mom, host->h_mom.data(), sizeof(rc.mom));
+      std::memcpy(rc.cnt, host->h_cnt.data(), sizeof(rc.cnt));
+    }
+    if (nplans >= 64 && nfac <= 65535) {
+      const dim3 grid((unsigned)((nplans + tpb - 1) / tpb), (unsigned)nfac);
+      factor_grads_kernel<N, P, true, NPc><<<grid, tpb, 0, s>>>(nplans, nfac, mean, covs, R, F, re,
+                                                                so, out, active, rc);
+    } else {
+      const int64_t total = nfac * nplans;
+      factor_grads_kernel<N, P, false, NPc><<<(unsigned)((total + tpb - 1) / tpb), tpb, 0, s>>>(
+          nplans, nfac, mean, covs, R, F, re, so, out, active, rc);
+    }
+  };
+  // specialisations for the configurations of SURVEY §8d: 13 projections
+  // (k_q = 3, P = 2) and 57 (k_q = 5, P = 2); anything else takes the loop
+  if (host && R.nproj == 13 && (int64_t)host->h_proj.size() == 13 * P)
+    go(std::integral_constant<int, 13>{});
+  else if (host && R.nproj == 57 && (int64_t)host->h_proj.size() == 57 * P)
+    go(std::integral_constant<int, 57>{});
+  else
+    go(std::integral_constant<int, 0>{});
   GVP_CUDA(cudaGetLastError());
   return GVP_OK;
 }

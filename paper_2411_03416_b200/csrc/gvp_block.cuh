@@ -95,6 +95,54 @@ GVP_DEV bool chol(const double (&a)[N][N], double (&L)[N][N]) {
   return ok;
 }
 
+// Multiplication-only variant for the fused kernels: one rsqrt per pivot,
+// inv[j] = 1 / L[j][j]; same SPD predicate.
+template <int N, bool FLOOR = true>
+GVP_DEV bool chol_fast(const double (&a)[N][N], double (&L)[N][N], double (&inv)[N]) {
+  bool ok = true;
+#pragma unroll
+  for (int j = 0; j < N; ++j) {
+#pragma unroll
+    for (int c = j + 1; c < N; ++c) L[j][c] = 0.0;
+    double s = a[j][j];
+#pragma unroll
+    for (int k = 0; k < j; ++k) s -= L[j][k] * L[j][k];
+    ok = ok && (s > 0.0);
+    const double r = rsqrt(s);
+    const double d = s * r;
+    if (FLOOR) ok = ok && (d > kPivotFloor);
+    L[j][j] = d;
+    inv[j] = r;
+#pragma unroll
+    for (int i = j + 1; i < N; ++i) {
+      double t = a[i][j];
+#pragma unroll
+      for (int k = 0; k < j; ++k) t -= L[i][k] * L[j][k];
+      L[i][j] = t * r;
+    }
+  }
+  return ok;
+}
+template <int N>
+GVP_DEV void tri_inv_fast(const double (&L)[N][N], const double (&inv)[N], double (&Li)[N][N]) {
+#pragma unroll
+  for (int c = 0; c < N; ++c) {
+#pragma unroll
+    for (int r = 0; r < N; ++r) {
+      if (r < c) {
+        Li[r][c] = 0.0;
+      } else if (r == c) {
+        Li[r][c] = inv[r];
+      } else {
+        double t = 0.0;
+#pragma unroll
+        for (int k = c; k < r; ++k) t += L[r][k] * Li[k][c];
+        Li[r][c] = -t * inv[r];
+      }
+    }
+  }
+}
+
 // X <- L^{-1} X  (L lower), X has M columns
 template <int N, int M>
 GVP_DEV void trsm_lower(const double (&L)[N][N], double (&X)[N][M]) {

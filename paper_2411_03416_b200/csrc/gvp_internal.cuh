@@ -30,7 +30,7 @@ int cuda_fail(cudaError_t err, const char* what);
 struct FieldDev {
   int ndim;
   int64_t nx, ny, nz;
-  double ox, oy, oz, cell;
+  double ox, oy, oz, cell, inv_cell;
   const double* corners;  // device
 };
 
@@ -57,12 +57,16 @@ struct RuleDev {
   const double* proj;     // (nproj, P)
   const double* mom;      // (nproj, 1 + n + n(n+1)/2)
   const int* cnt;         // (nproj)
+  const void* host;       // the owning host Rule (projection tables for by-value launch)
 };
 
 struct Rule {
   RuleDev dev{};
   double* d_buf = nullptr;
   int* d_cnt = nullptr;
+  // host copies of the projection tables (passed by value to the fused kernel)
+  std::vector<double> h_proj, h_mom;
+  std::vector<int> h_cnt;
   ~Rule();
   int build(const double* points, const double* weights, int64_t npts, int n, int P,
             cudaStream_t s);
