@@ -601,6 +601,8 @@ extern "C" int gvp_select_step_size(const double* mean, const double* diag, cons
     GVP_TRY(h2d(mu, w_mu.data(), w_mu.size(), s));
     const double tt[2] = {temp, temp};
     GVP_TRY(h2d(scal + 8, tt, 2, s));
+    const double nan2[2] = {NAN, NAN};  // no previous beta to aim the speculation at
+    GVP_TRY(h2d(scal, nan2, 2, s));
     GVP_CUDA(cudaStreamSynchronize(s));
   }
   // rhs piece Lambda mu, and log det of the current precision from the same

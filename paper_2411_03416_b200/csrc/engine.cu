@@ -41,6 +41,7 @@ __global__ void init_plans_kernel(int B, PlanState ps, double temp_low) {
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= B) return;
   ps.temp[b] = temp_low;
+  ps.beta[b] = NAN;        // no previous step: no speculation target in the first search
   ps.prev_total[b] = NAN;  // NaN encodes python None
   ps.prev_temp[b] = NAN;
   ps.active[b] = 1;

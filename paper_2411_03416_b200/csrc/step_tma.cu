@@ -234,6 +234,10 @@ select_step_v3_kernel(const __grid_constant__ Args a) {
   // 0 first round, 1 beta_min (L==1), 2 bisect, 3 commit, 4 done
   int phase = plan_ok ? (COMMIT ? 3 : 0) : 4;
   double lo = a.beta_min, hi = a.beta_max, best = (COMMIT && plan_ok) ? a.beta[b] : a.beta_max;
+  // KL at the bracket ends and the previous iteration's beta (a.beta holds it
+  // on entry; NaN / out of range = no prediction) drive the speculation
+  double kl_lo = 0.0, kl_hi = INFINITY;
+  const double prev_beta = (!COMMIT && plan_ok && L > 1) ? a.beta[b] : -1.0;
   const double temp = plan_ok ? a.temp[b] : 1.0;
   const double ldc = plan_ok ? a.ld_cur[b] : 0.0;
   int nprobe = 0;
@@ -302,16 +306,50 @@ select_step_v3_kernel(const __grid_constant__ Args a) {
       write = true;
       beta = best;
     } else if (tree_phase) {
-      const int k = (phase == 2) ? lane + 1 : lane - 1;
+      const int q = (phase == 2) ? lane : lane - 2;  // speculative slot
       double l = (phase == 2) ? lo : a.beta_min, h = (phase == 2) ? hi : a.beta_max;
-      const int depth = 31 - __clz(k);
-      bool valid = true;
-      for (int lev = depth - 1; lev >= 0 && valid; --lev) {
-        if (!((h - l) > 1e-3 * h)) valid = false;
-        const double mid = 0.5 * (l + h);
-        if ((k >> lev) & 1) l = mid; else h = mid;
+      // Predicted crossing beta* (KL(beta*) = bound): in the first round the
+      // previous iteration's accepted beta, later a log-log interpolation of
+      // the bracket's KL values. With a prediction the lanes take the next
+      // nodes of the bisection path towards beta*; without one, the BFS nodes
+      // of the subtree. Any choice is exact: the walk below only uses lanes
+      // whose beta equals the reference's next midpoint.
+      double target = -1.0;
+      if (phase == 0) {
+        target = prev_beta;
+      } else if (kl_lo > 0.0 && isfinite(kl_hi) && kl_hi > kl_lo && kl_lo < a.kl_bound &&
+                 a.kl_bound < kl_hi) {
+        const double t = (log(a.kl_bound) - log(kl_lo)) / (log(kl_hi) - log(kl_lo));
+        target = exp(log(l) + t * (log(h) - log(l)));
       }
-      valid = valid && ((h - l) > 1e-3 * h);
+      // slots: a complete subtree of depth dt on (up to) half of them — always
+      // resolves dt levels — and the rest follow the predicted path below it
+      const int nslots = (phase == 2) ? L : L - 2;
+      int dt = 0;
+      while ((2 << dt) - 1 <= nslots / 2) ++dt;
+      const int ntree = (1 << dt) - 1;
+      bool valid = true;
+      if (q >= ntree && target > l && target < h) {  // path node at depth dt + (q - ntree)
+        const int depth = dt + (q - ntree);
+        for (int s = 0;; ++s) {
+          if (!((h - l) > 1e-3 * h)) {
+            valid = false;
+            break;
+          }
+          const double mid = 0.5 * (l + h);
+          if (s == depth) break;
+          if (mid <= target) l = mid; else h = mid;
+        }
+      } else {  // BFS node k = q + 1 of the subtree
+        const int k = q + 1;
+        const int depth = 31 - __clz(k);
+        for (int lev = depth - 1; lev >= 0 && valid; --lev) {
+          if (!((h - l) > 1e-3 * h)) valid = false;
+          const double mid = 0.5 * (l + h);
+          if ((k >> lev) & 1) l = mid; else h = mid;
+        }
+        valid = valid && ((h - l) > 1e-3 * h);
+      }
       if (valid) {
         lane_on = true;
         beta = 0.5 * (l + h);
@@ -704,32 +742,34 @@ select_step_v3_kernel(const __grid_constant__ Args a) {
       }
       phase = 4;
     };
-    auto walk = [&](int off, int depth_avail) -> bool {
-      int k = 1;
-      for (int lev = 0; lev < depth_avail; ++lev) {
+    // Replay the reference's bisection (optimizer.py:223-230) as far as this
+    // round's probes reach: at each step the reference evaluates
+    // mid = 0.5 * (lo + hi); if some lane probed exactly that beta (bitwise),
+    // take its verdict, otherwise stop and probe it next round.
+    auto walk = [&]() -> bool {
+      for (int lev = 0; lev <= L; ++lev) {
         if (!((hi - lo) > 1e-3 * hi)) return true;
-        const int q = k - 1 + off;
-        if (q >= L || !r_on[q]) return true;
+        const double mid = 0.5 * (lo + hi);
+        int q = -1;
+#pragma unroll
+        for (int qq = L - 1; qq >= 0; --qq)
+          if (r_on[qq] && r_beta[qq] == mid) q = qq;
+        if (q < 0) return true;
         log_probe(r_beta[q], r_res[q] != 1, r_kl[q]);
         if (r_res[q] == 2) {
           fail(GVP_ERR_NOT_SPD, r_fail[q] | GVP_WHERE_MEAN_SOLVE_BIAS);
           return false;
         }
         if (feasible(q)) {
-          lo = r_beta[q];
-          best = r_beta[q];
-          k = 2 * k + 1;
+          lo = mid;
+          best = mid;
+          kl_lo = r_kl[q];
         } else {
-          hi = r_beta[q];
-          k = 2 * k;
+          hi = mid;
+          kl_hi = r_res[q] == 1 ? INFINITY : r_kl[q];
         }
       }
       return true;
-    };
-    auto tree_depth = [](int nodes) {
-      int d = 0;
-      while ((2 << d) - 1 <= nodes) ++d;
-      return d;
     };
     if (phase == 3) {
       phase = 4;
@@ -752,7 +792,9 @@ select_step_v3_kernel(const __grid_constant__ Args a) {
           best = a.beta_min;
           lo = a.beta_min;
           hi = a.beta_max;
-          if (walk(2, tree_depth(L - 2))) phase = ((hi - lo) > 1e-3 * hi) ? 2 : 3;
+          kl_lo = r_kl[1];
+          kl_hi = r_res[0] == 1 ? INFINITY : r_kl[0];
+          if (walk()) phase = ((hi - lo) > 1e-3 * hi) ? 2 : 3;
         }
       }
     } else if (phase == 1) {
@@ -768,7 +810,7 @@ select_step_v3_kernel(const __grid_constant__ Args a) {
         phase = ((hi - lo) > 1e-3 * hi) ? 2 : 3;
       }
     } else if (phase == 2) {
-      if (walk(0, tree_depth(L))) phase = ((hi - lo) > 1e-3 * hi) ? 2 : 3;
+      if (walk()) phase = ((hi - lo) > 1e-3 * hi) ? 2 : 3;
     }
     if (!COMMIT && phase == 3) {  // search finished: hand beta to the commit kernel
       if (leader) {
