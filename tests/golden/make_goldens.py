@@ -308,8 +308,38 @@ def maps():
     np.savez_compressed(os.path.join(HERE, "maps.npz"), **out)
 
 
+def slr():
+    """iP-GVIMP (slr.py): one SLR linearisation of the quadrotor and a short
+    outer loop on a C4-like scene (SURVEY §8d C4 parity variant, shortened)."""
+    from gvplan import NominalTrajectory, OuterConfig, planar_quadrotor, run_ipgvimp, slr_linearize
+    out = {}
+    rng = np.random.default_rng(11)
+    sys_nl = planar_quadrotor()
+    means = rng.normal(size=(8, 6)) * np.array([2, 2, 0.3, 1, 1, 0.5])
+    covs = []
+    for _ in range(8):
+        a = rng.normal(size=(6, 6))
+        covs.append(0.05 * (a @ a.T + 6 * np.eye(6)) / 6)
+    covs = np.stack(covs)
+    ltv = slr_linearize(sys_nl, NominalTrajectory(means=means, covs=covs), 0.1, smolyak_rule(3, 6))
+    out["lin_means"], out["lin_covs"] = means, covs
+    out["lin_A"] = np.stack([s.A for s in ltv.steps])
+    out["lin_a"] = np.stack([s.a for s in ltv.steps])
+    sdf = rasterize([Disc(center=np.array([5.0, 4.5]), radius=0.8)], bounds=[[-5, 15], [-5, 10]], cell_size=0.05)
+    env = Environment(sdf=sdf, model=CollisionModel(radius_eps=1.5, sigma_obs=6.0))
+    cfg = OptimizerConfig(k_q=3, kl_bound=10.0, temp_low=1.0, temp_high=5.0, max_iters=15)
+    res, log = run_ipgvimp(sys_nl, env, cfg, OuterConfig(max_outer=2), np.zeros(6),
+                           np.array([10.0, 5.0, 0, 0, 0, 0]), dt=0.25, num_steps=20, q_c=0.5, sigma_b=1e-3)
+    keys = ["beta", "temperature", "prior_cost", "collision_cost", "entropy_cost", "total_cost", "kl_step",
+            "mean_shift"]
+    out["ip_norm_diff"] = np.array([r["norm_diff"] for r in log])
+    out["ip_records"] = np.array([[r[k] for k in keys] for r in res.records])
+    out["ip_final_mean"] = res.final.mean.reshape(21, 6)
+    np.savez_compressed(os.path.join(HERE, "slr.npz"), **out)
+
+
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["rules", "factors", "chain", "steps", "priors", "maps", "runs"]
+    which = sys.argv[1:] or ["rules", "factors", "chain", "steps", "priors", "maps", "runs", "slr"]
     for name in which:
         globals()[name]()
         print("wrote", name)

@@ -1,0 +1,39 @@
+"""iP-GVIMP (slr.py): host SLR linearisation vs the reference, and the outer
+loop with GPU inner runs vs the reference's recorded run."""
+
+import numpy as np
+import pytest
+
+from conftest import golden, rel_err
+
+
+def test_slr_linearize_matches_reference():
+    import paper_2411_03416_b200 as P
+
+    g = golden("slr")
+    ltv = P.slr_linearize(P.planar_quadrotor(), P.NominalTrajectory(g["lin_means"], g["lin_covs"]), 0.1,
+                          P.smolyak_rule(3, 6))
+    assert rel_err(np.stack([s.A for s in ltv.steps]), g["lin_A"]) <= 1e-12
+    assert rel_err(np.stack([s.a for s in ltv.steps]), g["lin_a"]) <= 1e-12
+
+
+@pytest.mark.gpu
+def test_ipgvimp_matches_reference(gpu):
+    import paper_2411_03416_b200 as P
+
+    g = golden("slr")
+    sdf = P.rasterize([P.sdf.Disc(center=np.array([5.0, 4.5]), radius=0.8)], bounds=[[-5, 15], [-5, 10]],
+                      cell_size=0.05)
+    env = P.Environment(sdf=sdf, model=P.CollisionModel(radius_eps=1.5, sigma_obs=6.0))
+    cfg = P.OptimizerConfig(k_q=3, kl_bound=10.0, temp_low=1.0, temp_high=5.0, max_iters=15)
+    res, log = P.run_ipgvimp(P.planar_quadrotor(), env, cfg, P.OuterConfig(max_outer=2), np.zeros(6),
+                             np.array([10.0, 5.0, 0, 0, 0, 0]), dt=0.25, num_steps=20, q_c=0.5, sigma_b=1e-3)
+    nd = np.array([r["norm_diff"] for r in log])
+    assert nd.shape == g["ip_norm_diff"].shape
+    assert rel_err(nd, g["ip_norm_diff"]) <= 1e-9
+    keys = ["beta", "temperature", "prior_cost", "collision_cost", "entropy_cost", "total_cost", "kl_step",
+            "mean_shift"]
+    got = np.array([[r[k] for k in keys] for r in res.records])
+    assert np.array_equal(got[:, 0], g["ip_records"][:, 0])  # identical beta sequence (last outer iteration)
+    assert rel_err(got[:, 2:6], g["ip_records"][:, 2:6]) <= 1e-9
+    assert rel_err(res.final.mean.reshape(21, 6), g["ip_final_mean"]) <= 1e-9
