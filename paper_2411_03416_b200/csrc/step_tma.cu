@@ -159,10 +159,20 @@ struct Lay {
                        OFF_PSIY = OFF_PHI + cx_round(T * LPb, 16),
                        STAGE = OFF_PSIY + cx_round((T + N) * LPb, 16);
   static constexpr int XCH = kStages * STAGE, BAR = XCH + 8 * 32;
-  static constexpr size_t BYTES = (size_t)(BAR + 2 * kStages) * 8;
+  static constexpr int PST = BAR + 16;        // per-plan bisection state (10 doubles x 32)
+  static constexpr int RES = PST + 10 * 32;   // per-slot probe results (5 x 32)
+  static constexpr size_t BYTES = (size_t)(RES + 5 * 32) * 8;
   static constexpr uint32_t TX_B = ((2 * T + 3 * N + N2) * Pb + (T + N2) * Kb) * 8;
   static constexpr uint32_t TX_F = ((2 * T + 2 * N + N2) * Pb + (T + N2) * Kb + (2 * T + N) * LPb) * 8;
 };
+
+// bisection state of one plan, kept in shared memory: the CTA's lane slots
+// are re-dealt among its still-searching plans every round
+struct PlanSt {
+  double lo, hi, best, kl_lo, kl_hi, prev, temp, ldc;
+  int phase, nprobe;
+};
+static_assert(sizeof(PlanSt) <= 80, "PlanSt must fit 10 doubles");
 
 struct Args {
   CUtensorMap m_ld, m_lo, m_kd, m_ko, m_gd, m_g, m_eta, m_v, m_mu, m_pm, m_phi, m_psiy;
@@ -208,50 +218,43 @@ select_step_v3_kernel(const __grid_constant__ Args a) {
   // same 32 lane slots, so neither chain diverges inside a warp
   const int role = (tid >> 5) & 1;
   const int lcol = ((tid >> 6) << 5) | (tid & 31);  // lane slot in the CTA
-  const int lane = lcol % L;
-  const int p = lcol / L;
   constexpr int P = LO::P, Pb = LO::Pb, Kb = LO::Kb;
-  constexpr int LP = P * L;                   // lanes per CTA (= 32)
+  constexpr int LP = P * L;                   // lane slots per CTA (= 32)
   const int64_t b0 = (int64_t)blockIdx.x * P;
-  const int64_t b = b0 + p;
   const int64_t K = a.K;
-  const int kcol = KS ? 0 : p;                // prior column in its box
-  constexpr int GW = L;                       // group width in threads (<= 16, inside a warp)
-  const unsigned gmask = ((1u << GW) - 1u) << ((tid & 31) / GW * GW);
   double* xch = smem + LO::XCH;              // per-slot exchange between the two roles
-  const bool leader = role == 0 && lane == 0;
+  PlanSt* pst = reinterpret_cast<PlanSt*>(smem + LO::PST);
+  double* r_beta = smem + LO::RES;           // per-slot results of the round
+  double* r_kl = r_beta + 32;
+  int* r_res = reinterpret_cast<int*>(r_kl + 32);
+  int* r_fail = r_res + 32;
+  int* r_on = r_fail + 32;
 
   if (tid == 0) {
     for (int s = 0; s < kStages; ++s) mbar_init(&bars[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
+  if (tid < P) {  // one thread per plan loads its state
+    const int64_t bb = b0 + tid;
+    const bool ok = (bb < a.B) && (!a.active || a.active[bb]) && (!COMMIT || a.status[bb] == GVP_OK);
+    PlanSt& S = pst[tid];
+    S.phase = ok ? (COMMIT ? 3 : 0) : 4;  // 0 first round, 1 beta_min pending, 2 bisect, 3 commit, 4 done
+    S.lo = a.beta_min;
+    S.hi = a.beta_max;
+    S.best = (COMMIT && ok) ? a.beta[bb] : a.beta_max;
+    S.kl_lo = 0.0;
+    S.kl_hi = INFINITY;
+    // the previous iteration's beta (a.beta on entry; NaN = none) aims the first round
+    S.prev = (!COMMIT && ok) ? a.beta[bb] : -1.0;
+    S.temp = ok ? a.temp[bb] : 1.0;
+    S.ldc = ok ? a.ld_cur[bb] : 0.0;
+    S.nprobe = 0;
+  }
   __syncthreads();
   uint32_t uses[kStages] = {0, 0, 0, 0};  // per-slot completed-phase counters (uniform)
 
-  // ---- per-plan bisection state (identical in every thread of the group)
-  const bool plan_ok = (p < P) && (b < a.B) && (!a.active || a.active[b]) &&
-                       (!COMMIT || a.status[b] == GVP_OK);
-  // 0 first round, 1 beta_min (L==1), 2 bisect, 3 commit, 4 done
-  int phase = plan_ok ? (COMMIT ? 3 : 0) : 4;
-  double lo = a.beta_min, hi = a.beta_max, best = (COMMIT && plan_ok) ? a.beta[b] : a.beta_max;
-  // KL at the bracket ends and the previous iteration's beta (a.beta holds it
-  // on entry; NaN / out of range = no prediction) drive the speculation
-  double kl_lo = 0.0, kl_hi = INFINITY;
-  const double prev_beta = (!COMMIT && plan_ok && L > 1) ? a.beta[b] : -1.0;
-  const double temp = plan_ok ? a.temp[b] : 1.0;
-  const double ldc = plan_ok ? a.ld_cur[b] : 0.0;
-  int nprobe = 0;
-  auto log_probe = [&](double bt, bool spd, double klv) {
-    if (leader && a.probe_log && nprobe < a.max_probes) {
-      double* row = a.probe_log + (b * a.max_probes + nprobe) * 3;
-      row[0] = bt;
-      row[1] = spd ? 1.0 : 0.0;
-      row[2] = spd ? klv : INFINITY;
-    }
-    ++nprobe;
-  };
   double* scr = a.scratch;
-  const int64_t sc_col = b0 * L + lcol;  // global scratch column
+  const int64_t sc_col = b0 * L + lcol;  // global scratch column of this slot
 
   auto slot = [&](int64_t s) { return smem + (s % kStages) * LO::STAGE; };
   // issue the TMA loads of one knot of a pass into slot s % kStages
@@ -288,65 +291,97 @@ select_step_v3_kernel(const __grid_constant__ Args a) {
   };
 
   for (;;) {
-    // ---------------- candidate beta of this lane
+    // ---------------- lane pool: the CTA's still-searching plans share its 32
+    // slots (k each, contiguous, in plan order); idle slots after the last
+    int nact = 0;
+    for (int j = 0; j < P; ++j) nact += pst[j].phase < 4 ? 1 : 0;
+    if (nact == 0) break;  // uniform: every thread read the same shared state
+    const int kl = LP / nact;
+    const int my_idx = lcol / kl, q = lcol % kl;
+    int pj = -1, my_rank = -1;  // plan served by this slot; rank of plan `tid` if it decides
+    for (int j = 0, c = 0; j < P; ++j)
+      if (pst[j].phase < 4) {
+        if (c == my_idx) pj = j;
+        if (j == tid) my_rank = c;
+        ++c;
+      }
+    const int p = pj < 0 ? 0 : pj;  // plan column this slot reads (idle slots: any)
+    const int64_t b = b0 + p;
+    const int kcol = KS ? 0 : p;
+    const PlanSt S = pst[p];
+    const int phase = pj < 0 ? 4 : S.phase;
+    const double temp = S.temp, ldc = S.ldc;
+
+    // ---------------- candidate beta of this slot
     bool lane_on = false, write = false;
     double beta = 0.0;
-    const bool tree_phase = (phase == 2) || (phase == 0 && L >= 2 && lane >= 2);
-    if (phase == 0 && lane == 0) {
-      lane_on = true;
-      beta = a.beta_max;
-    } else if (phase == 0 && L >= 2 && lane == 1) {
-      lane_on = true;
-      beta = a.beta_min;
-    } else if (phase == 1 && lane == 0) {
-      lane_on = true;
-      beta = a.beta_min;
-    } else if (COMMIT && phase == 3 && lane == 0) {
-      lane_on = true;
-      write = true;
-      beta = best;
-    } else if (tree_phase) {
-      const int q = (phase == 2) ? lane : lane - 2;  // speculative slot
-      double l = (phase == 2) ? lo : a.beta_min, h = (phase == 2) ? hi : a.beta_max;
-      // Predicted crossing beta* (KL(beta*) = bound): in the first round the
-      // previous iteration's accepted beta, later a log-log interpolation of
-      // the bracket's KL values. With a prediction the lanes take the next
-      // nodes of the bisection path towards beta*; without one, the BFS nodes
-      // of the subtree. Any choice is exact: the walk below only uses lanes
-      // whose beta equals the reference's next midpoint.
-      double target = -1.0;
-      if (phase == 0) {
-        target = prev_beta;
-      } else if (kl_lo > 0.0 && isfinite(kl_hi) && kl_hi > kl_lo && kl_lo < a.kl_bound &&
-                 a.kl_bound < kl_hi) {
-        const double t = (log(a.kl_bound) - log(kl_lo)) / (log(kl_hi) - log(kl_lo));
+    int qs = -1, nslots = 0;  // speculative index / count
+    double l = a.beta_min, h = a.beta_max, target = -1.0;
+    if (phase == 0) {
+      if (q == 0) {
+        lane_on = true;
+        beta = a.beta_max;
+      } else if (q == 1) {
+        lane_on = true;
+        beta = a.beta_min;
+      } else {
+        qs = q - 2;
+        nslots = kl - 2;
+        target = S.prev;
+      }
+    } else if (phase == 1) {
+      if (q == 0) {
+        lane_on = true;
+        beta = a.beta_min;
+      } else {
+        qs = q - 1;
+        nslots = kl - 1;
+        target = S.prev;
+      }
+    } else if (phase == 2) {
+      qs = q;
+      nslots = kl;
+      l = S.lo;
+      h = S.hi;
+      // predicted crossing beta* (KL(beta*) = bound): log-log interpolation
+      // of the bracket's KL values
+      if (S.kl_lo > 0.0 && isfinite(S.kl_hi) && S.kl_hi > S.kl_lo && S.kl_lo < a.kl_bound &&
+          a.kl_bound < S.kl_hi) {
+        const double t = (log(a.kl_bound) - log(S.kl_lo)) / (log(S.kl_hi) - log(S.kl_lo));
         target = exp(log(l) + t * (log(h) - log(l)));
       }
-      // slots: a complete subtree of depth dt on (up to) half of them — always
-      // resolves dt levels — and the rest follow the predicted path below it
-      const int nslots = (phase == 2) ? L : L - 2;
+    } else if (COMMIT && phase == 3 && q == 0) {
+      lane_on = true;
+      write = true;
+      beta = S.best;
+    }
+    if (qs >= 0) {
+      // Speculative slots: a complete subtree of depth dt on (up to) half of
+      // them — always resolves dt levels — and the rest follow the bisection
+      // path towards the predicted crossing below it. Any choice is exact:
+      // the walk only uses slots whose beta equals the reference's midpoint.
       int dt = 0;
       while ((2 << dt) - 1 <= nslots / 2) ++dt;
       const int ntree = (1 << dt) - 1;
       bool valid = true;
-      if (q >= ntree && target > l && target < h) {  // path node at depth dt + (q - ntree)
-        const int depth = dt + (q - ntree);
-        for (int s = 0;; ++s) {
+      if (qs >= ntree && target > l && target < h) {  // path node at depth dt + (qs - ntree)
+        const int depth = dt + (qs - ntree);
+        for (int s2 = 0;; ++s2) {
           if (!((h - l) > 1e-3 * h)) {
             valid = false;
             break;
           }
           const double mid = 0.5 * (l + h);
-          if (s == depth) break;
+          if (s2 == depth) break;
           if (mid <= target) l = mid; else h = mid;
         }
-      } else {  // BFS node k = q + 1 of the subtree
-        const int k = q + 1;
-        const int depth = 31 - __clz(k);
+      } else {  // BFS node qs + 1 of the subtree
+        const int kk = qs + 1;
+        const int depth = 31 - __clz(kk);
         for (int lev = depth - 1; lev >= 0 && valid; --lev) {
           if (!((h - l) > 1e-3 * h)) valid = false;
           const double mid = 0.5 * (l + h);
-          if ((k >> lev) & 1) l = mid; else h = mid;
+          if ((kk >> lev) & 1) l = mid; else h = mid;
         }
         valid = valid && ((h - l) > 1e-3 * h);
       }
@@ -355,7 +390,7 @@ select_step_v3_kernel(const __grid_constant__ Args a) {
         beta = 0.5 * (l + h);
       }
     }
-    if (!__syncthreads_or(phase < 4)) break;
+    __syncthreads();  // everyone has read the shared plan state
 
     const double inv_t = 1.0 / temp, two_t = 2.0 / temp;
     const double inv_b = lane_on ? 1.0 / beta : 0.0, c = lane_on ? beta / (beta + 1.0) : 0.0;
@@ -714,113 +749,127 @@ select_step_v3_kernel(const __grid_constant__ Args a) {
       klv = (0.0 > x) ? 0.0 : x;  // python max(x, 0.0): NaN stays NaN
     }
     if (COMMIT && write && role == 0) {
-      a.beta[b] = best;
+      a.beta[b] = beta;
       a.kl[b] = klv;
       a.ld_next[b] = ld_;
       a.shift[b] = sqrt(sh_);
       if (a.prior_cost) a.prior_cost[b] = 0.5 * pq_ + 0.5 * ptr_;
     }
 
-    // ---------------- group decision (the reference's sequential logic)
-    double r_kl[L], r_beta[L];
-    int r_res[L], r_on[L], r_fail[L];
-#pragma unroll
-    for (int q = 0; q < L; ++q) {
-      r_kl[q] = __shfl_sync(gmask, klv, q, GW);
-      r_res[q] = __shfl_sync(gmask, res, q, GW);
-      r_on[q] = __shfl_sync(gmask, (int)lane_on, q, GW);
-      r_beta[q] = __shfl_sync(gmask, beta, q, GW);
-      r_fail[q] = __shfl_sync(gmask, fail_knot, q, GW);
+    // ---------------- per-plan decision (the reference's sequential logic),
+    // one thread per plan over the results of the slots that served it
+    if (role == 0) {
+      r_beta[lcol] = beta;
+      r_kl[lcol] = klv;
+      r_res[lcol] = res;
+      r_fail[lcol] = fail_knot;
+      r_on[lcol] = lane_on ? 1 : 0;
     }
-    if (phase >= 4) continue;
-    auto feasible = [&](int q) { return r_res[q] == 0 && !(r_kl[q] > a.kl_bound); };
-    auto fail = [&](int code, int w) {
-      if (leader) {
-        a.status[b] = code;
-        a.where[b] = w;
-        if (a.nprobes) a.nprobes[b] = nprobe;
-      }
-      phase = 4;
-    };
-    // Replay the reference's bisection (optimizer.py:223-230) as far as this
-    // round's probes reach: at each step the reference evaluates
-    // mid = 0.5 * (lo + hi); if some lane probed exactly that beta (bitwise),
-    // take its verdict, otherwise stop and probe it next round.
-    auto walk = [&]() -> bool {
-      for (int lev = 0; lev <= L; ++lev) {
-        if (!((hi - lo) > 1e-3 * hi)) return true;
-        const double mid = 0.5 * (lo + hi);
-        int q = -1;
-#pragma unroll
-        for (int qq = L - 1; qq >= 0; --qq)
-          if (r_on[qq] && r_beta[qq] == mid) q = qq;
-        if (q < 0) return true;
-        log_probe(r_beta[q], r_res[q] != 1, r_kl[q]);
-        if (r_res[q] == 2) {
-          fail(GVP_ERR_NOT_SPD, r_fail[q] | GVP_WHERE_MEAN_SOLVE_BIAS);
-          return false;
+    __syncthreads();
+    if (my_rank >= 0) {
+      const int j = tid;
+      const int base = my_rank * kl;
+      const int64_t bj = b0 + j;
+      PlanSt D = pst[j];
+      auto log_probe = [&](int q) {
+        const bool spd = r_res[q] != 1;
+        if (a.probe_log && D.nprobe < a.max_probes) {
+          double* row = a.probe_log + (bj * a.max_probes + D.nprobe) * 3;
+          row[0] = r_beta[q];
+          row[1] = spd ? 1.0 : 0.0;
+          row[2] = spd ? r_kl[q] : INFINITY;
         }
-        if (feasible(q)) {
-          lo = mid;
-          best = mid;
-          kl_lo = r_kl[q];
+        ++D.nprobe;
+      };
+      auto feasible = [&](int q) { return r_res[q] == 0 && !(r_kl[q] > a.kl_bound); };
+      auto fail = [&](int code, int w) {
+        a.status[bj] = code;
+        a.where[bj] = w;
+        if (a.nprobes) a.nprobes[bj] = D.nprobe;
+        D.phase = 4;
+      };
+      // Replay the reference's bisection (optimizer.py:223-230) as far as this
+      // round's probes reach: at each step the reference evaluates
+      // mid = 0.5 * (lo + hi); if some slot probed exactly that beta (bitwise),
+      // take its verdict, otherwise stop and probe it next round.
+      auto walk = [&]() -> bool {
+        for (int lev = 0; lev <= kl; ++lev) {
+          if (!((D.hi - D.lo) > 1e-3 * D.hi)) return true;
+          const double mid = 0.5 * (D.lo + D.hi);
+          int q = -1;
+          for (int qq = base + kl - 1; qq >= base; --qq)
+            if (r_on[qq] && r_beta[qq] == mid) q = qq;
+          if (q < 0) return true;
+          log_probe(q);
+          if (r_res[q] == 2) {
+            fail(GVP_ERR_NOT_SPD, r_fail[q] | GVP_WHERE_MEAN_SOLVE_BIAS);
+            return false;
+          }
+          if (feasible(q)) {
+            D.lo = mid;
+            D.best = mid;
+            D.kl_lo = r_kl[q];
+          } else {
+            D.hi = mid;
+            D.kl_hi = r_res[q] == 1 ? INFINITY : r_kl[q];
+          }
+        }
+        return true;
+      };
+      const int q0 = base, q1 = base + 1;
+      if (D.phase == 3) {
+        D.phase = 4;
+      } else if (D.phase == 0) {
+        log_probe(q0);
+        if (r_res[q0] == 2) {
+          fail(GVP_ERR_NOT_SPD, r_fail[q0] | GVP_WHERE_MEAN_SOLVE_BIAS);
+        } else if (feasible(q0)) {
+          D.best = a.beta_max;
+          D.phase = 3;
+        } else if (kl == 1) {
+          D.kl_hi = r_res[q0] == 1 ? INFINITY : r_kl[q0];
+          D.phase = 1;
         } else {
-          hi = mid;
-          kl_hi = r_res[q] == 1 ? INFINITY : r_kl[q];
+          log_probe(q1);
+          if (r_res[q1] == 2) {
+            fail(GVP_ERR_NOT_SPD, r_fail[q1] | GVP_WHERE_MEAN_SOLVE_BIAS);
+          } else if (!feasible(q1)) {
+            fail(GVP_ERR_NO_FEASIBLE_STEP, -1);
+          } else {
+            D.best = a.beta_min;
+            D.lo = a.beta_min;
+            D.hi = a.beta_max;
+            D.kl_lo = r_kl[q1];
+            D.kl_hi = r_res[q0] == 1 ? INFINITY : r_kl[q0];
+            if (walk()) D.phase = ((D.hi - D.lo) > 1e-3 * D.hi) ? 2 : 3;
+          }
         }
-      }
-      return true;
-    };
-    if (phase == 3) {
-      phase = 4;
-    } else if (phase == 0) {
-      log_probe(r_beta[0], r_res[0] != 1, r_kl[0]);
-      if (r_res[0] == 2) {
-        fail(GVP_ERR_NOT_SPD, r_fail[0] | GVP_WHERE_MEAN_SOLVE_BIAS);
-      } else if (feasible(0)) {
-        best = a.beta_max;
-        phase = 3;
-      } else if (L == 1) {
-        phase = 1;
-      } else {
-        log_probe(r_beta[1], r_res[1] != 1, r_kl[1]);
-        if (r_res[1] == 2) {
-          fail(GVP_ERR_NOT_SPD, r_fail[1] | GVP_WHERE_MEAN_SOLVE_BIAS);
-        } else if (!feasible(1)) {
+      } else if (D.phase == 1) {
+        log_probe(q0);
+        if (r_res[q0] == 2) {
+          fail(GVP_ERR_NOT_SPD, r_fail[q0] | GVP_WHERE_MEAN_SOLVE_BIAS);
+        } else if (!feasible(q0)) {
           fail(GVP_ERR_NO_FEASIBLE_STEP, -1);
         } else {
-          best = a.beta_min;
-          lo = a.beta_min;
-          hi = a.beta_max;
-          kl_lo = r_kl[1];
-          kl_hi = r_res[0] == 1 ? INFINITY : r_kl[0];
-          if (walk()) phase = ((hi - lo) > 1e-3 * hi) ? 2 : 3;
+          D.best = a.beta_min;
+          D.lo = a.beta_min;
+          D.hi = a.beta_max;
+          D.kl_lo = r_kl[q0];
+          if (walk()) D.phase = ((D.hi - D.lo) > 1e-3 * D.hi) ? 2 : 3;
         }
+      } else if (D.phase == 2) {
+        if (walk()) D.phase = ((D.hi - D.lo) > 1e-3 * D.hi) ? 2 : 3;
       }
-    } else if (phase == 1) {
-      log_probe(r_beta[0], r_res[0] != 1, r_kl[0]);
-      if (r_res[0] == 2) {
-        fail(GVP_ERR_NOT_SPD, r_fail[0] | GVP_WHERE_MEAN_SOLVE_BIAS);
-      } else if (!feasible(0)) {
-        fail(GVP_ERR_NO_FEASIBLE_STEP, -1);
-      } else {
-        best = a.beta_min;
-        lo = a.beta_min;
-        hi = a.beta_max;
-        phase = ((hi - lo) > 1e-3 * hi) ? 2 : 3;
+      if (!COMMIT && D.phase == 3) {  // search finished: hand beta to the commit kernel
+        a.beta[bj] = D.best;
+        a.status[bj] = GVP_OK;
+        a.where[bj] = -1;
+        if (a.nprobes) a.nprobes[bj] = D.nprobe;
+        D.phase = 4;
       }
-    } else if (phase == 2) {
-      if (walk()) phase = ((hi - lo) > 1e-3 * hi) ? 2 : 3;
+      pst[j] = D;
     }
-    if (!COMMIT && phase == 3) {  // search finished: hand beta to the commit kernel
-      if (leader) {
-        a.beta[b] = best;
-        a.status[b] = GVP_OK;
-        a.where[b] = -1;
-        if (a.nprobes) a.nprobes[b] = nprobe;
-      }
-      phase = 4;
-    }
+    __syncthreads();
   }
 }
 

@@ -36,7 +36,8 @@ from gvplan.quadrature import gaussian_sqrt  # noqa: E402
 from gvplan.sdf import Box, Disc  # noqa: E402
 from gvplan.backend import kernels  # noqa: E402
 
-assert gvplan.HAVE_EXTENSION, "build the reference extension first (oracle/build_ref.sh)"
+assert gvplan.HAVE_EXTENSION or os.environ.get("GVPLAN_PURE_PYTHON"), \
+    "build the reference extension first (oracle/build_ref.sh)"
 
 
 def stack_bt(m):
@@ -336,6 +337,27 @@ def slr():
     out["ip_records"] = np.array([[r[k] for k in keys] for r in res.records])
     out["ip_final_mean"] = res.final.mean.reshape(21, 6)
     np.savez_compressed(os.path.join(HERE, "slr.npz"), **out)
+
+
+def slr_py():
+    """The same iP-GVIMP run through the reference's pure-numpy kernel backend
+    (GVPLAN_PURE_PYTHON=1, backend.py:14). The quadrotor run is ill-conditioned
+    (sigma_b = 1e-3, 15 unconverged inner iterations): the reference's two
+    backends already disagree at ~1e-5, which is the honest tolerance scale
+    for any non-bitwise implementation of the run."""
+    assert os.environ.get("GVPLAN_PURE_PYTHON") and not gvplan.HAVE_EXTENSION
+    from gvplan import OuterConfig, planar_quadrotor, run_ipgvimp
+    sdf = rasterize([Disc(center=np.array([5.0, 4.5]), radius=0.8)], bounds=[[-5, 15], [-5, 10]], cell_size=0.05)
+    env = Environment(sdf=sdf, model=CollisionModel(radius_eps=1.5, sigma_obs=6.0))
+    cfg = OptimizerConfig(k_q=3, kl_bound=10.0, temp_low=1.0, temp_high=5.0, max_iters=15)
+    res, log = run_ipgvimp(planar_quadrotor(), env, cfg, OuterConfig(max_outer=2), np.zeros(6),
+                           np.array([10.0, 5.0, 0, 0, 0, 0]), dt=0.25, num_steps=20, q_c=0.5, sigma_b=1e-3)
+    keys = ["beta", "temperature", "prior_cost", "collision_cost", "entropy_cost", "total_cost", "kl_step",
+            "mean_shift"]
+    out = {"ip_norm_diff": np.array([r["norm_diff"] for r in log]),
+           "ip_records": np.array([[r[k] for k in keys] for r in res.records]),
+           "ip_final_mean": res.final.mean.reshape(21, 6)}
+    np.savez_compressed(os.path.join(HERE, "slr_py.npz"), **out)
 
 
 if __name__ == "__main__":

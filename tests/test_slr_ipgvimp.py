@@ -17,11 +17,25 @@ def test_slr_linearize_matches_reference():
     assert rel_err(np.stack([s.a for s in ltv.steps]), g["lin_a"]) <= 1e-12
 
 
+def _spread(g, gp, key, cols=slice(None)):
+    """Tolerance for the ill-conditioned quadrotor run: 4x the disagreement
+    between the reference's own two kernel backends (compiled vs pure numpy,
+    tests/golden/make_goldens.py slr_py), never tighter than 1e-9."""
+    return max(1e-9, 4.0 * rel_err(gp[key][..., cols], g[key][..., cols]))
+
+
+def test_ipgvimp_spread_is_reference_property():
+    """The golden spread comes from the reference alone, not from this code."""
+    g, gp = golden("slr"), golden("slr_py")
+    assert np.array_equal(gp["ip_records"][:, 0], g["ip_records"][:, 0])
+    assert _spread(g, gp, "ip_norm_diff") < 1e-4
+
+
 @pytest.mark.gpu
 def test_ipgvimp_matches_reference(gpu):
     import paper_2411_03416_b200 as P
 
-    g = golden("slr")
+    g, gp = golden("slr"), golden("slr_py")
     sdf = P.rasterize([P.sdf.Disc(center=np.array([5.0, 4.5]), radius=0.8)], bounds=[[-5, 15], [-5, 10]],
                       cell_size=0.05)
     env = P.Environment(sdf=sdf, model=P.CollisionModel(radius_eps=1.5, sigma_obs=6.0))
@@ -30,10 +44,12 @@ def test_ipgvimp_matches_reference(gpu):
                              np.array([10.0, 5.0, 0, 0, 0, 0]), dt=0.25, num_steps=20, q_c=0.5, sigma_b=1e-3)
     nd = np.array([r["norm_diff"] for r in log])
     assert nd.shape == g["ip_norm_diff"].shape
-    assert rel_err(nd, g["ip_norm_diff"]) <= 1e-9
+    assert rel_err(nd, g["ip_norm_diff"]) <= _spread(g, gp, "ip_norm_diff")
     keys = ["beta", "temperature", "prior_cost", "collision_cost", "entropy_cost", "total_cost", "kl_step",
             "mean_shift"]
     got = np.array([[r[k] for k in keys] for r in res.records])
     assert np.array_equal(got[:, 0], g["ip_records"][:, 0])  # identical beta sequence (last outer iteration)
-    assert rel_err(got[:, 2:6], g["ip_records"][:, 2:6]) <= 1e-9
-    assert rel_err(res.final.mean.reshape(21, 6), g["ip_final_mean"]) <= 1e-9
+    assert np.array_equal(got[:, 1], g["ip_records"][:, 1])  # identical temperature schedule
+    for c in range(2, 6):
+        assert rel_err(got[:, c], g["ip_records"][:, c]) <= _spread(g, gp, "ip_records", c), keys[c]
+    assert rel_err(res.final.mean.reshape(21, 6), g["ip_final_mean"]) <= _spread(g, gp, "ip_final_mean")
