@@ -86,26 +86,44 @@ def build_problem(P, goals):
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons during the timed region."""
+    """nvidia-smi clocks + throttle reasons sampled every 20 ms; summary() keeps
+    the samples taken inside the timed window (mark_start / mark_end)."""
+
+    FIELDS = ("timestamp,clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
     def __init__(self, index: int):
         self.index = index
         self.proc = None
+        self.t0 = self.t1 = None
         self.path = os.path.join(REPO, "gpurun_out", f"clocks_r{index}.csv")
 
     def __enter__(self):
         os.makedirs(os.path.dirname(self.path), exist_ok=True)
         try:
             self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.index), "--query-gpu=clocks.sm,clocks.max.sm,"
-                 "clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
-                 "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-                 "clocks_event_reasons.sw_power_cap", "--format=csv,noheader,nounits", "-lms", "100"],
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "20"],
                 stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
         except OSError:
             self.proc = None
-        time.sleep(0.3)
+        deadline = time.time() + 5.0  # nvidia-smi start-up: wait for its first sample
+        while self.proc is not None and time.time() < deadline:
+            try:
+                if os.path.getsize(self.path) > 0:
+                    break
+            except OSError:
+                pass
+            time.sleep(0.02)
         return self
+
+    def mark_start(self):
+        self.t0 = time.time()
+
+    def mark_end(self):
+        self.t1 = time.time()
+        time.sleep(0.05)
 
     def __exit__(self, *exc):
         if self.proc is not None:
@@ -113,21 +131,49 @@ class ClockSampler:
             self.proc.wait()
 
     def summary(self):
+        import datetime
         rows = []
         try:
             for line in open(self.path):
                 parts = [p.strip() for p in line.split(",")]
-                if len(parts) >= 7 and parts[0].isdigit():
-                    rows.append(parts)
+                if len(parts) >= 8 and parts[1].isdigit():
+                    try:
+                        ts = datetime.datetime.strptime(parts[0], "%Y/%m/%d %H:%M:%S.%f").timestamp()
+                    except ValueError:
+                        ts = None
+                    rows.append((ts, parts[1:]))
         except OSError:
             pass
         if not rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = sorted(int(r[0]) for r in rows)
+        inside = [r for ts, r in rows if ts is not None and self.t0 is not None and self.t1 is not None
+                  and self.t0 - 0.03 <= ts <= self.t1 + 0.03]
+        sel = inside or [r for _, r in rows]
+        sm = sorted(int(r[0]) for r in sel)
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({nm for r in rows for nm, v in zip(names, r[3:7]) if v.lower() == "active"})
-        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": int(rows[0][1]), "reasons": reasons,
-                "samples": len(rows)}
+        reasons = sorted({nm for r in sel for nm, v in zip(names, r[3:7]) if v.lower() == "active"})
+        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": int(sel[0][1]), "reasons": reasons,
+                "samples": len(sel), "window": "timed region" if inside else "whole run (no sample inside)"}
+
+
+def probe_flops_per_knot(n: int) -> dict:
+    """Algorithmic fp64 flops of one bisection probe at one knot (both chains
+    of the one-pass probe, csrc/step_probe.cu; FMA = 2, rsqrt = 1), counted
+    from its loop nests. Returns {"A", "B", "total"}."""
+    T, N2 = n * (n + 1) // 2, n * n
+    fma = lambda k: 2 * k  # noqa: E731
+    chol = fma(T - n) + n + n + n + sum((n - 1 - j) * (1 + fma(j)) for j in range(n)) \
+        + sum(fma(r - c) + 1 for c in range(n) for r in range(c + 1, n))
+    common = (4 * N2                      # off block scaled: (K/T + Lambda/beta) (* c)
+              + fma(n * T) * 2            # W = Li M_o, G = Li Lambda_o
+              + fma(N2 * n)               # Z = Psi W - G
+              + fma(T * n) + fma(T * 2 * n)  # Phi -= W'W, Phi' += W'Z - G'W
+              + chol
+              + fma(n * T) + fma(sum(q + 1 for r in range(n) for q in range(r + 1)))  # Psi = Li Phi' Li'
+              + n)                        # trace / accumulate
+    a = 6 * T + common + 1
+    b = 3 * T + common + n + fma(N2) + n + fma(3 * N2) + fma(2 * T) + fma(N2) + 3 * n
+    return {"A": a, "B": b, "total": a + b}
 
 
 def measured_peaks():
@@ -249,7 +295,7 @@ def _ref_worker_step(arg):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--plans", type=int, default=4096, help="plans per GPU")
@@ -288,6 +334,7 @@ def main():
     rule = P.smolyak_rule(K_Q, n)
     max_iters = args.warmup + 2 * args.steps + 4
     eng = P.PlanBatch(B, K, n, sdf, model, rule, c5_cfg(P, max_iters), shared_prior=True)
+    eng.trace_probes(64)  # per-plan probe counts (the useful work of the bisection)
 
     # problem resident in HBM (plan-minor torch tensors), loaded device-to-device
     from paper_2411_03416_b200.engine import to_plan_minor
@@ -319,11 +366,13 @@ def main():
     with ClockSampler(local) as clk:
         barrier()
         torch.cuda.synchronize()
+        clk.mark_start()
         ev0.record(stream)
         eng.step(args.steps)
         ev1.record(stream)
         ev1.synchronize()
         torch.cuda.synchronize()
+        clk.mark_end()
         barrier()
     ms = ev0.elapsed_time(ev1)
     launches = eng.launches() - launches_before
@@ -333,10 +382,18 @@ def main():
     evals_all = sum_over_ranks(evals)
     value = evals_all / (ms_max / 1e3)
 
-    # ---------------- per-kernel device times (events around each kernel)
-    kms = eng.step_profiled(args.steps)
-    it_prof = eng.summary()["iterations"].astype(np.int64)
-    plans_prof = float((it_prof - it_after).sum())
+    # ---------------- per-kernel device times (events around each kernel) and
+    # the bisection's useful work: the reference's probe count of each plan
+    kms = np.zeros(4)
+    probes = 0
+    it_prev = it_after
+    for _ in range(args.steps):
+        kms += eng.step_profiled(1)
+        it_now = eng.summary()["iterations"].astype(np.int64)
+        moved = (it_now - it_prev) > 0
+        counts = [len(p) for p in eng.probes()]
+        probes += int(sum(c for c, m in zip(counts, moved) if m))
+        it_prev = it_now
     # ---------------- e2e: through the C ABI from pinned host buffers
     pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()  # noqa: E731
     h_kd, h_ko = pin(prior.prec.diag_stack), pin(prior.prec.off_stack)
@@ -365,21 +422,23 @@ def main():
         peaks = measured_peaks()
         hbm = float(peaks.get("hbm_gbs", 6650.0))
         steps_prof = max(args.steps, 1)
-        sel_ms = kms[0] / steps_prof
-        fac_ms = kms[1] / steps_prof
-        ctl_ms = kms[2] / steps_prof
-        # algorithmic bytes per launch:
-        #  select_step: per plan per knot, read mu, Lambda (diag+off), info, g_mu, G_diag, prior
-        #  mean (64 doubles) + write mu', Lambda', Sigma_ii, Sigma_i,i+1 (68 doubles); the
-        #  shared prior precision once per launch.
-        sel_bytes = B * K * 132 * 8 + K * 32 * 8
+        bis_ms, com_ms, fac_ms, ctl_ms = (float(x) / steps_prof for x in kms)
+        # Dominant kernel: the bisection (one-pass probes), fp64-pipe bound.
+        # achieved = useful probes (the reference's own probe sequence, counted
+        # on device) x knots x algorithmic flops per probe-knot / kernel time;
+        # speculative probes that the reference would not make are not counted.
+        fl = probe_flops_per_knot(n)
+        sm_mhz = float(peaks.get("sm_max_mhz", 1965.0))
+        fp64_peak = 148 * 64 * 2 * sm_mhz * 1e6 / 1e12  # 64 DFMA/clk/SM (ncu peak_sustained)
+        bis_flops = probes / steps_prof * K * fl["total"]
+        ach = bis_flops / (bis_ms / 1e3) / 1e12
+        traffic = None
+        tpath = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "ncu_traffic.json")
+        if os.path.exists(tpath):
+            with open(tpath) as fh:
+                traffic = json.load(fh).get("probe_fused_kernel")
         #  factor stage: 8 (n^2 + 3n + 1) = 232 B per factor
         fac_bytes = B * F * 232
-        dominant = "select_step" if sel_ms >= fac_ms else "factor_grads"
-        if dominant == "select_step":
-            ach = sel_bytes / (sel_ms / 1e3) / 1e9
-        else:
-            ach = fac_bytes / (fac_ms / 1e3) / 1e9
         fac_ach = fac_bytes / (fac_ms / 1e3) / 1e9 if fac_ms > 0 else None
         result = {
             "metric": "factor-expectation evals/s",
@@ -404,12 +463,17 @@ def main():
             "sigma_point_evals_per_s": value * rule.npoints,
             "plan_iterations_per_s": value / F,
             "gpu_launches": int(launches),
-            "kernel_ms_per_step": {"select_step": sel_ms, "factor_grads": fac_ms, "control": ctl_ms},
-            "roofline": {"kernel": dominant, "bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s",
-                         "frac": ach / hbm, "traffic": None,
-                         "peak_source": "MEASURED_PEAKS.json hbm_gbs" + (" (fallback)" if peaks.get("fallback") else ""),
-                         "factor_grads_achieved_gbs": fac_ach,
-                         "factor_grads_frac": (fac_ach / hbm) if fac_ach else None},
+            "kernel_ms_per_step": {"bisection": bis_ms, "commit": com_ms, "factor_grads": fac_ms,
+                                   "control": ctl_ms},
+            "roofline": {"kernel": "bisection (probe_fused_kernel)", "bound": "fp64", "achieved": ach,
+                         "peak": fp64_peak, "unit": "TFLOP/s", "frac": ach / fp64_peak, "traffic": traffic,
+                         "traffic_unit": "bytes/launch (ncu dram read+write)",
+                         "flops_per_probe_knot": fl["total"], "probes_per_plan_iter": probes / max(1, B * steps_prof),
+                         "peak_source": "148 SMs x 64 DFMA/clk (ncu sm__sass_thread_inst_executed_op_dfma"
+                                        "_pred_on.sum.peak_sustained) x 2 x sm_max_mhz (MEASURED_PEAKS.json)",
+                         "factor_grads": {"bound": "hbm", "achieved": fac_ach, "peak": hbm, "unit": "GB/s",
+                                          "frac": (fac_ach / hbm) if fac_ach else None,
+                                          "bytes_per_factor": 232}},
             "e2e": {"value": e2e_value, "unit": "factor-evals/s", "h2d_bytes_per_step": h2d // max(args.steps, 1),
                     "d2h_bytes_per_step": d2h // max(args.steps, 1),
                     "what": "gvp_engine_load from pinned host + steps + records D2H, one C-ABI call chain"},

@@ -177,8 +177,8 @@ int gvp_engine_load_dev(gvp_engine* e, const double* kdiag, const double* koff,
  * (asynchronous on the engine stream unless sync != 0). */
 int gvp_engine_step(gvp_engine* e, int32_t iters, int32_t sync);
 /* Same as gvp_engine_step but kernel by kernel with CUDA events on the
- * engine stream; adds the device time of each kernel over the iterations to
- * ms[0..2] = {select_step, factor_grads, control} (synchronous). */
+ * engine stream; the device time of each stage summed over the iterations
+ * goes to ms[0..3] = {bisection, commit, factor_grads, control} (synchronous). */
 int gvp_engine_step_profiled(gvp_engine* e, int32_t iters, double* ms);
 /* The engine's cudaStream_t (as void*), for events/interop. */
 void* gvp_engine_stream(gvp_engine* e);
@@ -209,6 +209,11 @@ int gvp_engine_device_state(gvp_engine* e, double** mean, double** diag, double*
                             double** covs, double** crosses);
 /* Launch counters: kernels launched by this engine since create. */
 int64_t gvp_engine_launches(gvp_engine* e);
+/* Probe trace of the step-size search (optimizer.py:188-231 `trace`): per
+ * plan the last iteration's probes as (beta, spd, kl) rows, at most
+ * max_probes each. Enable before the first step. */
+int gvp_engine_trace_probes(gvp_engine* e, int32_t max_probes);
+int gvp_engine_get_probes(gvp_engine* e, double* log, int32_t* counts);
 
 /* ------------------------------------------------ batched device kernels (tests) */
 /* All pointers device memory, plan-minor layout with nplans plans, async on

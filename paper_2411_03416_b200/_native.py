@@ -86,6 +86,8 @@ _SIGS = {
     "gvp_engine_device_state": (C.c_int, [C.c_void_p] + [C.POINTER(C.c_void_p)] * 5),
     "gvp_engine_launches": (C.c_int64, [C.c_void_p]),
     "gvp_engine_lanes": (C.c_int32, [C.c_void_p]),
+    "gvp_engine_trace_probes": (C.c_int, [C.c_void_p, C.c_int32]),
+    "gvp_engine_get_probes": (C.c_int, [C.c_void_p, _dp, _i32p]),
     "gvp_set_step_lanes": (C.c_int, [C.c_int32]),
     "gvp_chain_scratch_doubles": (C.c_int64, [C.c_int32, C.c_int64, C.c_int32, C.c_int32]),
     "gvp_gbp_marginals_dev": (C.c_int, [C.c_int32, C.c_int64, C.c_int32, C.c_void_p, C.c_void_p,

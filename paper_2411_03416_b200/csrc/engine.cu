@@ -172,6 +172,10 @@ struct gvp_engine {
   unsigned long long* oob = nullptr;
   PlanState ps{};
   cudaGraphExec_t graph = nullptr;
+  // optional per-iteration probe trace (the reference's select_step trace)
+  double* plog = nullptr;
+  int* pcount = nullptr;
+  int max_probes = 0;
   int iters_launched = 0;
   int64_t launches = 0;
   std::vector<void*> allocs;
@@ -216,7 +220,7 @@ struct gvp_engine {
     q.temp = ps.temp; q.ld_cur = ps.logdet;
     q.kl_bound = cfg.kl_bound; q.beta_min = cfg.beta_min; q.beta_max = cfg.beta_max;
     q.status = ps.status; q.where = ps.where;
-    q.probe_log = nullptr; q.max_probes = 0; q.nprobes = nullptr;
+    q.probe_log = plog; q.max_probes = max_probes; q.nprobes = pcount;
     q.scratch = scratch;
     q.active = ps.active;
     return q;
@@ -446,21 +450,23 @@ extern "C" int gvp_engine_step(gvp_engine* e, int32_t iters, int32_t sync) {
 
 extern "C" int gvp_engine_step_profiled(gvp_engine* e, int32_t iters, double* ms) {
   cudaStream_t s = e->stream;
-  cudaEvent_t ev[4];
+  cudaEvent_t ev[5];
   for (auto& x : ev) GVP_CUDA(cudaEventCreate(&x));
-  double acc[3] = {0, 0, 0};
+  double acc[4] = {0, 0, 0, 0};
   for (int k = 0; k < iters && e->iters_launched < e->cfg.max_iters; ++k) {
     GVP_CUDA(cudaEventRecord(ev[0], s));
-    int r = launch_select_step_v2(e->step_args(), s);
+    int r = launch_select_bisect(e->step_args(), s);
     if (r) return r;
-    e->launches += 2;
     GVP_CUDA(cudaEventRecord(ev[1], s));
-    if ((r = e->factors())) return r;
+    if ((r = launch_select_commit(e->step_args(), s))) return r;
+    e->launches += 2;
     GVP_CUDA(cudaEventRecord(ev[2], s));
-    if ((r = e->control())) return r;
+    if ((r = e->factors())) return r;
     GVP_CUDA(cudaEventRecord(ev[3], s));
-    GVP_CUDA(cudaEventSynchronize(ev[3]));
-    for (int j = 0; j < 3; ++j) {
+    if ((r = e->control())) return r;
+    GVP_CUDA(cudaEventRecord(ev[4], s));
+    GVP_CUDA(cudaEventSynchronize(ev[4]));
+    for (int j = 0; j < 4; ++j) {
       float t = 0.f;
       GVP_CUDA(cudaEventElapsedTime(&t, ev[j], ev[j + 1]));
       acc[j] += t;
@@ -468,7 +474,7 @@ extern "C" int gvp_engine_step_profiled(gvp_engine* e, int32_t iters, double* ms
     ++e->iters_launched;
   }
   for (auto& x : ev) cudaEventDestroy(x);
-  for (int j = 0; j < 3; ++j) ms[j] = acc[j];
+  for (int j = 0; j < 4; ++j) ms[j] = acc[j];
   return GVP_OK;
 }
 
@@ -559,4 +565,33 @@ extern "C" int gvp_engine_device_state(gvp_engine* e, double** mean, double** di
 }
 
 extern "C" int64_t gvp_engine_launches(gvp_engine* e) { return e->launches; }
+
+// Record every probe (beta, spd, kl) of each plan's step-size search; the log
+// holds the last iteration. Must be enabled before the first step.
+extern "C" int gvp_engine_trace_probes(gvp_engine* e, int32_t max_probes) {
+  if (!e || max_probes <= 0) return GVP_ERR_ARG;
+  if (e->iters_launched > 0) {
+    set_error("enable the probe trace before the first step");
+    return GVP_ERR_ARG;
+  }
+  int r;
+  if ((r = e->alloc(&e->plog, (size_t)e->B * max_probes * 3)) || (r = e->alloc(&e->pcount, (size_t)e->B)))
+    return r;
+  GVP_CUDA(cudaMemsetAsync(e->pcount, 0, sizeof(int) * e->B, e->stream));
+  e->max_probes = max_probes;
+  if (e->graph) {
+    cudaGraphExecDestroy(e->graph);
+    e->graph = nullptr;
+  }
+  return GVP_OK;
+}
+
+extern "C" int gvp_engine_get_probes(gvp_engine* e, double* log, int32_t* counts) {
+  if (!e || !e->plog) return GVP_ERR_ARG;
+  GVP_CUDA(cudaMemcpyAsync(log, e->plog, sizeof(double) * e->nreal * e->max_probes * 3,
+                           cudaMemcpyDeviceToHost, e->stream));
+  GVP_CUDA(cudaMemcpyAsync(counts, e->pcount, sizeof(int) * e->nreal, cudaMemcpyDeviceToHost, e->stream));
+  GVP_CUDA(cudaStreamSynchronize(e->stream));
+  return GVP_OK;
+}
 extern "C" int32_t gvp_engine_lanes(gvp_engine* e) { return e->lanes; }

@@ -158,6 +158,8 @@ struct V2Launch {
   const int* active;
 };
 int launch_select_step_v2(const V2Launch& q, cudaStream_t s);
+int launch_select_bisect(const V2Launch& q, cudaStream_t s);  // bisection only
+int launch_select_commit(const V2Launch& q, cudaStream_t s);  // commit of q.beta
 // even plan stride >= 2 required by the TMA-staged step kernel
 int64_t step_plan_stride(int nplans);
 int64_t step_scratch_doubles(int nplans, int64_t K, int n, int lanes);

@@ -31,91 +31,14 @@
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 
 #include "gvp_internal.cuh"
+#include "step_common.cuh"
 
 namespace gvp {
 namespace v3 {
-
-constexpr int kStages = 4;  // prefetch distance 2; slot of knot i-1 stays valid during knot i
-constexpr int kAhead = 2;
-
-template <int N> constexpr int T_ = N * (N + 1) / 2;
-
-GVP_DEV uint32_t saddr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
-GVP_DEV void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(saddr(bar)), "r"(count) : "memory");
-}
-GVP_DEV void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(saddr(bar)), "r"(bytes)
-               : "memory");
-}
-GVP_DEV bool mbar_try(uint64_t* bar, uint32_t parity) {
-  uint32_t ok;
-  asm volatile(
-      "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
-      : "=r"(ok)
-      : "r"(saddr(bar)), "r"(parity)
-      : "memory");
-  return ok != 0;
-}
-GVP_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
-  while (!mbar_try(bar, parity)) {
-  }
-}
-GVP_DEV void tma3(double* dst, const CUtensorMap* map, int c0, int c1, int c2, uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];\n" ::"r"(
-          saddr(dst)),
-      "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(saddr(bar))
-      : "memory");
-}
-GVP_DEV void fence_proxy_async() { asm volatile("fence.proxy.async.global;\n" ::: "memory"); }
-
-// ------------------------------------------------------------ packed algebra
-template <int N>
-GVP_DEV bool chol_inv(const double (&A)[T_<N>], double (&Li)[T_<N>], double& pivprod) {
-  double L[T_<N>], inv[N];
-  bool ok = true;
-  pivprod = 1.0;
-#pragma unroll
-  for (int j = 0; j < N; ++j) {
-    double s = A[tri_idx(j, j)];
-#pragma unroll
-    for (int k = 0; k < j; ++k) s -= L[tri_idx(j, k)] * L[tri_idx(j, k)];
-    ok = ok && (s > 0.0);
-    const double r = rsqrt(s);
-    const double d = s * r;
-    ok = ok && (d > kPivotFloor);
-    L[tri_idx(j, j)] = d;
-    inv[j] = r;
-    pivprod *= d;
-#pragma unroll
-    for (int i = j + 1; i < N; ++i) {
-      double t = A[tri_idx(i, j)];
-#pragma unroll
-      for (int k = 0; k < j; ++k) t -= L[tri_idx(i, k)] * L[tri_idx(j, k)];
-      L[tri_idx(i, j)] = t * r;
-    }
-  }
-#pragma unroll
-  for (int c = 0; c < N; ++c) {
-    Li[tri_idx(c, c)] = inv[c];
-#pragma unroll
-    for (int r = c + 1; r < N; ++r) {
-      double t = 0.0;
-#pragma unroll
-      for (int k = c; k < r; ++k) t += L[tri_idx(r, k)] * Li[tri_idx(k, c)];
-      Li[tri_idx(r, c)] = -t * inv[r];
-    }
-  }
-  return ok;
-}
-template <int N>
-GVP_DEV double sym_at(const double (&A)[T_<N>], int r, int c) {
-  return r >= c ? A[tri_idx(r, c)] : A[tri_idx(c, r)];
-}
 
 // ------------------------------------------------------------ stage layout
 // rows per plan (pass B / pass F), and per lane (pass F scratch)
@@ -137,8 +60,6 @@ struct Ly {
 // Compile-time shared-memory layout of one CTA (32 lane slots = P plans x L
 // lanes, two warps). Every TMA box lands on a 128-byte boundary: row starts
 // are rounded to a multiple of cx_gran(width) rows.
-constexpr int cx_round(int x, int m) { return (x + m - 1) / m * m; }
-constexpr int cx_gran(int w) { return w % 16 == 0 ? 1 : w % 8 == 0 ? 2 : w % 4 == 0 ? 4 : w % 2 == 0 ? 8 : 16; }
 template <int N, int L, bool KS>
 struct Lay {
   static constexpr int T = N * (N + 1) / 2, N2 = N * N;
@@ -158,21 +79,14 @@ struct Lay {
                        OFF_PHI = OFF_PRIOR + cx_round(KR * Kb, 16),
                        OFF_PSIY = OFF_PHI + cx_round(T * LPb, 16),
                        STAGE = OFF_PSIY + cx_round((T + N) * LPb, 16);
-  static constexpr int XCH = kStages * STAGE, BAR = XCH + 8 * 32;
+  static constexpr int NS = ring_stages(STAGE), AH = NS - 2;  // slot of knot i-1 stays valid at knot i
+  static constexpr int XCH = NS * STAGE, BAR = XCH + 8 * 32;
   static constexpr int PST = BAR + 16;        // per-plan bisection state (10 doubles x 32)
   static constexpr int RES = PST + 10 * 32;   // per-slot probe results (5 x 32)
   static constexpr size_t BYTES = (size_t)(RES + 5 * 32) * 8;
   static constexpr uint32_t TX_B = ((2 * T + 3 * N + N2) * Pb + (T + N2) * Kb) * 8;
   static constexpr uint32_t TX_F = ((2 * T + 2 * N + N2) * Pb + (T + N2) * Kb + (2 * T + N) * LPb) * 8;
 };
-
-// bisection state of one plan, kept in shared memory: the CTA's lane slots
-// are re-dealt among its still-searching plans every round
-struct PlanSt {
-  double lo, hi, best, kl_lo, kl_hi, prev, temp, ldc;
-  int phase, nprobe;
-};
-static_assert(sizeof(PlanSt) <= 80, "PlanSt must fit 10 doubles");
 
 struct Args {
   CUtensorMap m_ld, m_lo, m_kd, m_ko, m_gd, m_g, m_eta, m_v, m_mu, m_pm, m_phi, m_psiy;
@@ -231,36 +145,20 @@ select_step_v3_kernel(const __grid_constant__ Args a) {
   int* r_on = r_fail + 32;
 
   if (tid == 0) {
-    for (int s = 0; s < kStages; ++s) mbar_init(&bars[s], 1);
+    for (int s = 0; s < LO::NS; ++s) mbar_init(&bars[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
-  if (tid < P) {  // one thread per plan loads its state
-    const int64_t bb = b0 + tid;
-    const bool ok = (bb < a.B) && (!a.active || a.active[bb]) && (!COMMIT || a.status[bb] == GVP_OK);
-    PlanSt& S = pst[tid];
-    S.phase = ok ? (COMMIT ? 3 : 0) : 4;  // 0 first round, 1 beta_min pending, 2 bisect, 3 commit, 4 done
-    S.lo = a.beta_min;
-    S.hi = a.beta_max;
-    S.best = (COMMIT && ok) ? a.beta[bb] : a.beta_max;
-    S.kl_lo = 0.0;
-    S.kl_hi = INFINITY;
-    // the previous iteration's beta (a.beta on entry; NaN = none) aims the first round
-    S.prev = (!COMMIT && ok) ? a.beta[bb] : -1.0;
-    S.temp = ok ? a.temp[bb] : 1.0;
-    S.ldc = ok ? a.ld_cur[bb] : 0.0;
-    S.nprobe = 0;
-  }
+  search_init(a, pst, P, b0, COMMIT, tid);
   __syncthreads();
-  uint32_t uses[kStages] = {0, 0, 0, 0};  // per-slot completed-phase counters (uniform)
 
   double* scr = a.scratch;
   const int64_t sc_col = b0 * L + lcol;  // global scratch column of this slot
 
-  auto slot = [&](int64_t s) { return smem + (s % kStages) * LO::STAGE; };
-  // issue the TMA loads of one knot of a pass into slot s % kStages
+  auto slot = [&](int64_t s) { return smem + (s % LO::NS) * LO::STAGE; };
+  // issue the TMA loads of one knot of a pass into slot s % NS
   auto issue = [&](int64_t s, int64_t i, bool passB) {
     double* st = slot(s);
-    uint64_t* bar = &bars[s % kStages];
+    uint64_t* bar = &bars[s % LO::NS];
     mbar_expect_tx(bar, passB ? LO::TX_B : LO::TX_F);
     const int ck = KS ? 0 : (int)b0;
     double* pl = st + LO::OFF_PLAN;
@@ -285,111 +183,18 @@ select_step_v3_kernel(const __grid_constant__ Args a) {
     }
   };
   auto wait_slot = [&](int64_t s) {
-    const int k = (int)(s % kStages);
-    mbar_wait(&bars[k], uses[k] & 1u);
-    ++uses[k];
+    mbar_wait(&bars[s % LO::NS], (uint32_t)((s / LO::NS) & 1));
   };
 
   for (;;) {
-    // ---------------- lane pool: the CTA's still-searching plans share its 32
-    // slots (k each, contiguous, in plan order); idle slots after the last
-    int nact = 0;
-    for (int j = 0; j < P; ++j) nact += pst[j].phase < 4 ? 1 : 0;
-    if (nact == 0) break;  // uniform: every thread read the same shared state
-    const int kl = LP / nact;
-    const int my_idx = lcol / kl, q = lcol % kl;
-    int pj = -1, my_rank = -1;  // plan served by this slot; rank of plan `tid` if it decides
-    for (int j = 0, c = 0; j < P; ++j)
-      if (pst[j].phase < 4) {
-        if (c == my_idx) pj = j;
-        if (j == tid) my_rank = c;
-        ++c;
-      }
-    const int p = pj < 0 ? 0 : pj;  // plan column this slot reads (idle slots: any)
+    const Pick pk = search_pick(a, pst, P, LP, lcol, tid, COMMIT);
+    if (pk.kl == 0) break;  // uniform: every thread read the same shared state
+    const int p = pk.p, kl = pk.kl, my_rank = pk.my_rank;
     const int64_t b = b0 + p;
     const int kcol = KS ? 0 : p;
-    const PlanSt S = pst[p];
-    const int phase = pj < 0 ? 4 : S.phase;
-    const double temp = S.temp, ldc = S.ldc;
-
-    // ---------------- candidate beta of this slot
-    bool lane_on = false, write = false;
-    double beta = 0.0;
-    int qs = -1, nslots = 0;  // speculative index / count
-    double l = a.beta_min, h = a.beta_max, target = -1.0;
-    if (phase == 0) {
-      if (q == 0) {
-        lane_on = true;
-        beta = a.beta_max;
-      } else if (q == 1) {
-        lane_on = true;
-        beta = a.beta_min;
-      } else {
-        qs = q - 2;
-        nslots = kl - 2;
-        target = S.prev;
-      }
-    } else if (phase == 1) {
-      if (q == 0) {
-        lane_on = true;
-        beta = a.beta_min;
-      } else {
-        qs = q - 1;
-        nslots = kl - 1;
-        target = S.prev;
-      }
-    } else if (phase == 2) {
-      qs = q;
-      nslots = kl;
-      l = S.lo;
-      h = S.hi;
-      // predicted crossing beta* (KL(beta*) = bound): log-log interpolation
-      // of the bracket's KL values
-      if (S.kl_lo > 0.0 && isfinite(S.kl_hi) && S.kl_hi > S.kl_lo && S.kl_lo < a.kl_bound &&
-          a.kl_bound < S.kl_hi) {
-        const double t = (log(a.kl_bound) - log(S.kl_lo)) / (log(S.kl_hi) - log(S.kl_lo));
-        target = exp(log(l) + t * (log(h) - log(l)));
-      }
-    } else if (COMMIT && phase == 3 && q == 0) {
-      lane_on = true;
-      write = true;
-      beta = S.best;
-    }
-    if (qs >= 0) {
-      // Speculative slots: a complete subtree of depth dt on (up to) half of
-      // them — always resolves dt levels — and the rest follow the bisection
-      // path towards the predicted crossing below it. Any choice is exact:
-      // the walk only uses slots whose beta equals the reference's midpoint.
-      int dt = 0;
-      while ((2 << dt) - 1 <= nslots / 2) ++dt;
-      const int ntree = (1 << dt) - 1;
-      bool valid = true;
-      if (qs >= ntree && target > l && target < h) {  // path node at depth dt + (qs - ntree)
-        const int depth = dt + (qs - ntree);
-        for (int s2 = 0;; ++s2) {
-          if (!((h - l) > 1e-3 * h)) {
-            valid = false;
-            break;
-          }
-          const double mid = 0.5 * (l + h);
-          if (s2 == depth) break;
-          if (mid <= target) l = mid; else h = mid;
-        }
-      } else {  // BFS node qs + 1 of the subtree
-        const int kk = qs + 1;
-        const int depth = 31 - __clz(kk);
-        for (int lev = depth - 1; lev >= 0 && valid; --lev) {
-          if (!((h - l) > 1e-3 * h)) valid = false;
-          const double mid = 0.5 * (l + h);
-          if ((kk >> lev) & 1) l = mid; else h = mid;
-        }
-        valid = valid && ((h - l) > 1e-3 * h);
-      }
-      if (valid) {
-        lane_on = true;
-        beta = 0.5 * (l + h);
-      }
-    }
+    const double temp = pst[p].temp, ldc = pst[p].ldc;
+    const bool lane_on = pk.on, write = pk.on && pk.write;
+    const double beta = pk.beta;
     __syncthreads();  // everyone has read the shared plan state
 
     const double inv_t = 1.0 / temp, two_t = 2.0 / temp;
@@ -402,11 +207,11 @@ select_step_v3_kernel(const __grid_constant__ Args a) {
     double LiN[T], yN[N];
     int64_t sbase = 0;
     if (tid == 0)
-      for (int s = 0; s < kAhead && s < K; ++s) issue(s, K - 1 - s, true);
+      for (int s = 0; s < LO::AH && s < K; ++s) issue(s, K - 1 - s, true);
     for (int64_t s = 0; s < K; ++s) {
       wait_slot(s);
       __syncthreads();  // everyone past knot s-1: its slot may be refilled
-      if (tid == 0 && s + kAhead < K) issue(s + kAhead, K - 1 - (s + kAhead), true);
+      if (tid == 0 && s + LO::AH < K) issue(s + LO::AH, K - 1 - (s + LO::AH), true);
       const int64_t i = K - 1 - s;
       if (!(lane_on && res == 0)) continue;
       const double* st = slot(s);
@@ -525,12 +330,12 @@ select_step_v3_kernel(const __grid_constant__ Args a) {
       for (int q = 0; q < T; ++q) Sig[q] = sc[(Y::S_PHI + q) * a.BLp];
     }
     if (tid == 0)
-      for (int s = 0; s < kAhead && s < K; ++s) issue(sbase + s, s, false);
+      for (int s = 0; s < LO::AH && s < K; ++s) issue(sbase + s, s, false);
     for (int64_t i = 0; i < K; ++i) {
       const int64_t s = sbase + i;
       wait_slot(s);
       __syncthreads();
-      if (tid == 0 && i + kAhead < K) issue(s + kAhead, i + kAhead, false);
+      if (tid == 0 && i + LO::AH < K) issue(s + LO::AH, i + LO::AH, false);
       const double* st = slot(s);
       const double* pl = st + LO::OFF_PLAN;
       const double* pr = st + LO::OFF_PRIOR;
@@ -766,151 +571,10 @@ select_step_v3_kernel(const __grid_constant__ Args a) {
       r_on[lcol] = lane_on ? 1 : 0;
     }
     __syncthreads();
-    if (my_rank >= 0) {
-      const int j = tid;
-      const int base = my_rank * kl;
-      const int64_t bj = b0 + j;
-      PlanSt D = pst[j];
-      auto log_probe = [&](int q) {
-        const bool spd = r_res[q] != 1;
-        if (a.probe_log && D.nprobe < a.max_probes) {
-          double* row = a.probe_log + (bj * a.max_probes + D.nprobe) * 3;
-          row[0] = r_beta[q];
-          row[1] = spd ? 1.0 : 0.0;
-          row[2] = spd ? r_kl[q] : INFINITY;
-        }
-        ++D.nprobe;
-      };
-      auto feasible = [&](int q) { return r_res[q] == 0 && !(r_kl[q] > a.kl_bound); };
-      auto fail = [&](int code, int w) {
-        a.status[bj] = code;
-        a.where[bj] = w;
-        if (a.nprobes) a.nprobes[bj] = D.nprobe;
-        D.phase = 4;
-      };
-      // Replay the reference's bisection (optimizer.py:223-230) as far as this
-      // round's probes reach: at each step the reference evaluates
-      // mid = 0.5 * (lo + hi); if some slot probed exactly that beta (bitwise),
-      // take its verdict, otherwise stop and probe it next round.
-      auto walk = [&]() -> bool {
-        for (int lev = 0; lev <= kl; ++lev) {
-          if (!((D.hi - D.lo) > 1e-3 * D.hi)) return true;
-          const double mid = 0.5 * (D.lo + D.hi);
-          int q = -1;
-          for (int qq = base + kl - 1; qq >= base; --qq)
-            if (r_on[qq] && r_beta[qq] == mid) q = qq;
-          if (q < 0) return true;
-          log_probe(q);
-          if (r_res[q] == 2) {
-            fail(GVP_ERR_NOT_SPD, r_fail[q] | GVP_WHERE_MEAN_SOLVE_BIAS);
-            return false;
-          }
-          if (feasible(q)) {
-            D.lo = mid;
-            D.best = mid;
-            D.kl_lo = r_kl[q];
-          } else {
-            D.hi = mid;
-            D.kl_hi = r_res[q] == 1 ? INFINITY : r_kl[q];
-          }
-        }
-        return true;
-      };
-      const int q0 = base, q1 = base + 1;
-      if (D.phase == 3) {
-        D.phase = 4;
-      } else if (D.phase == 0) {
-        log_probe(q0);
-        if (r_res[q0] == 2) {
-          fail(GVP_ERR_NOT_SPD, r_fail[q0] | GVP_WHERE_MEAN_SOLVE_BIAS);
-        } else if (feasible(q0)) {
-          D.best = a.beta_max;
-          D.phase = 3;
-        } else if (kl == 1) {
-          D.kl_hi = r_res[q0] == 1 ? INFINITY : r_kl[q0];
-          D.phase = 1;
-        } else {
-          log_probe(q1);
-          if (r_res[q1] == 2) {
-            fail(GVP_ERR_NOT_SPD, r_fail[q1] | GVP_WHERE_MEAN_SOLVE_BIAS);
-          } else if (!feasible(q1)) {
-            fail(GVP_ERR_NO_FEASIBLE_STEP, -1);
-          } else {
-            D.best = a.beta_min;
-            D.lo = a.beta_min;
-            D.hi = a.beta_max;
-            D.kl_lo = r_kl[q1];
-            D.kl_hi = r_res[q0] == 1 ? INFINITY : r_kl[q0];
-            if (walk()) D.phase = ((D.hi - D.lo) > 1e-3 * D.hi) ? 2 : 3;
-          }
-        }
-      } else if (D.phase == 1) {
-        log_probe(q0);
-        if (r_res[q0] == 2) {
-          fail(GVP_ERR_NOT_SPD, r_fail[q0] | GVP_WHERE_MEAN_SOLVE_BIAS);
-        } else if (!feasible(q0)) {
-          fail(GVP_ERR_NO_FEASIBLE_STEP, -1);
-        } else {
-          D.best = a.beta_min;
-          D.lo = a.beta_min;
-          D.hi = a.beta_max;
-          D.kl_lo = r_kl[q0];
-          if (walk()) D.phase = ((D.hi - D.lo) > 1e-3 * D.hi) ? 2 : 3;
-        }
-      } else if (D.phase == 2) {
-        if (walk()) D.phase = ((D.hi - D.lo) > 1e-3 * D.hi) ? 2 : 3;
-      }
-      if (!COMMIT && D.phase == 3) {  // search finished: hand beta to the commit kernel
-        a.beta[bj] = D.best;
-        a.status[bj] = GVP_OK;
-        a.where[bj] = -1;
-        if (a.nprobes) a.nprobes[bj] = D.nprobe;
-        D.phase = 4;
-      }
-      pst[j] = D;
-    }
+    if (my_rank >= 0)
+      search_decide(a, pst, tid, my_rank * kl, kl, b0, COMMIT, r_beta, r_kl, r_res, r_fail, r_on);
     __syncthreads();
   }
-}
-
-// ------------------------------------------------------------ host side
-typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
-                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
-                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
-                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-
-static EncodeTiledFn encode_fn() {
-  static EncodeTiledFn fn = nullptr;
-  if (!fn) {
-    void* p = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
-        q == cudaDriverEntryPointSuccess)
-      fn = (EncodeTiledFn)p;
-  }
-  return fn;
-}
-
-// 3D map over a plan-minor array [K][E][W] (W = plan stride), box [bw, rows, 1]
-static int make_map(CUtensorMap* m, const double* base, int64_t W, int64_t E, int64_t K, int bw,
-                    int rows) {
-  EncodeTiledFn fn = encode_fn();
-  if (!fn) {
-    set_error("cuTensorMapEncodeTiled unavailable");
-    return GVP_ERR_CUDA;
-  }
-  cuuint64_t dims[3] = {(cuuint64_t)W, (cuuint64_t)E, (cuuint64_t)std::max<int64_t>(K, 1)};
-  cuuint64_t strides[2] = {(cuuint64_t)(W * 8), (cuuint64_t)(W * E * 8)};
-  cuuint32_t box[3] = {(cuuint32_t)bw, (cuuint32_t)rows, 1};
-  cuuint32_t es[3] = {1, 1, 1};
-  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, (void*)base, dims, strides, box, es,
-                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                  CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r != CUDA_SUCCESS) {
-    set_error("cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
-    return GVP_ERR_CUDA;
-  }
-  return GVP_OK;
 }
 
 }  // namespace v3
@@ -918,7 +582,10 @@ static int make_map(CUtensorMap* m, const double* base, int64_t W, int64_t E, in
 int64_t step_scratch_doubles(int nplans, int64_t K, int n, int lanes) {
   const int64_t T = (int64_t)n * (n + 1) / 2;
   const int64_t BL = (((int64_t)nplans + 1) & ~1LL) * lanes + 64;  // padded columns
-  return std::max<int64_t>(1, K * (2 * T + n) * BL);
+  // two-pass bisection scratch, or commit scratch + the one-pass probe's residual
+  const int64_t two_pass = K * (2 * T + n) * BL;
+  const int64_t one_pass = probe_residual_offset(nplans, K, n) + K * n * step_plan_stride(nplans);
+  return std::max<int64_t>(1, std::max(two_pass, one_pass));
 }
 
 int64_t step_plan_stride(int nplans) { return std::max<int64_t>(2, ((int64_t)nplans + 1) & ~1LL); }
@@ -992,12 +659,11 @@ static int launch_v3(const V2Launch& q, const int L, const bool commit, cudaStre
   a.off_phi = a.off_prior + round_up(rowsK * Kb, 16);
   a.off_psiy = a.off_phi + round_up(T * LPb, 16);
   a.stage_doubles = a.off_psiy + round_up((T + n) * LPb, 16);
-  a.bm_off = v3::kStages * a.stage_doubles;
+  a.bm_off = 0;
   a.bar_off = a.bm_off + 8 * 32;  // role exchange: 4 doubles x 2 roles x 32 lane slots
   a.bytes_B = (uint32_t)(((2 * T + 3 * n + N2) * Pb + (T + N2) * Kb) * 8);
   a.bytes_F = (uint32_t)(((2 * T + 2 * n + N2) * Pb + (T + N2) * Kb + (2 * T + n) * LPb) * 8);
   (void)SE;
-  const size_t bytes = (size_t)(a.bar_off + 2 * v3::kStages) * sizeof(double) + 1024;
   const unsigned grid = (unsigned)((q.nplans + P - 1) / P);
 #define GVP_V3_KS(NN, LL, CC, KK)                                                               \
   {                                                                                             \
@@ -1037,8 +703,8 @@ static int launch_v3(const V2Launch& q, const int L, const bool commit, cudaStre
   return GVP_OK;
 }
 
-// bisection (L candidate lanes per plan), then the commit of the accepted beta
-int launch_select_step_v2(const V2Launch& q, cudaStream_t s) {
+// bisection (L candidate lanes per plan): the accepted beta of each plan -> q.beta
+int launch_select_bisect(const V2Launch& q, cudaStream_t s) {
   if (q.nplans == 0 || q.K == 0) return GVP_OK;
   const int L = q.lanes;
   if (L != 1 && L != 4 && L != 8 && L != 16) {
@@ -1049,9 +715,24 @@ int launch_select_step_v2(const V2Launch& q, cudaStream_t s) {
     set_error("plan stride must be even (step_plan_stride)");
     return GVP_ERR_ARG;
   }
-  int r = launch_v3(q, L, false, s);
-  if (r) return r;
+  // GVP_TWO_PASS=1 selects the two-pass bisection kernel (A/B comparisons)
+  static const bool two_pass = [] {
+    const char* e = std::getenv("GVP_TWO_PASS");
+    return e && e[0] == '1';
+  }();
+  return two_pass ? launch_v3(q, L, false, s) : launch_probe(q, L, s);
+}
+
+// the commit of the accepted beta: next iterate, marginals, KL, log det, costs
+int launch_select_commit(const V2Launch& q, cudaStream_t s) {
+  if (q.nplans == 0 || q.K == 0) return GVP_OK;
   return launch_v3(q, 1, true, s);
+}
+
+int launch_select_step_v2(const V2Launch& q, cudaStream_t s) {
+  int r = launch_select_bisect(q, s);
+  if (r) return r;
+  return launch_select_commit(q, s);
 }
 
 }  // namespace gvp

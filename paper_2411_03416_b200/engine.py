@@ -109,8 +109,8 @@ class PlanBatch:
 
     def step_profiled(self, iters: int = 1) -> np.ndarray:
         """Kernel-by-kernel iterations with CUDA events; returns summed device
-        ms of (select_step, factor_grads, control)."""
-        ms = np.zeros(3)
+        ms of (bisection, commit, factor_grads, control)."""
+        ms = np.zeros(4)
         self._ok(self.lib.gvp_engine_step_profiled(self.handle, int(iters), N.ptr(ms)),
                  "gvp_engine_step_profiled")
         return ms
@@ -143,6 +143,20 @@ class PlanBatch:
 
     def launches(self) -> int:
         return int(self.lib.gvp_engine_launches(self.handle))
+
+    def trace_probes(self, max_probes: int = 64):
+        """Record each plan's step-size probes (optimizer.py:188-231 `trace`);
+        call before the first step."""
+        self._ok(self.lib.gvp_engine_trace_probes(self.handle, int(max_probes)), "gvp_engine_trace_probes")
+        self._max_probes = int(max_probes)
+
+    def probes(self):
+        """Last iteration's probes per plan: list of (n_i, 3) arrays of
+        (beta, spd, kl) in the reference's probe order."""
+        log = np.empty((self.B, self._max_probes, 3))
+        cnt = np.zeros(self.B, dtype=np.int32)
+        self._ok(self.lib.gvp_engine_get_probes(self.handle, N.ptr(log), N.ptr(cnt)), "gvp_engine_get_probes")
+        return [log[b, :min(int(cnt[b]), self._max_probes)] for b in range(self.B)]
 
     # ------------------------------------------------------------ results
     def state(self):

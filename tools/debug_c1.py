@@ -18,4 +18,4 @@ ms = eng.step_profiled(iters)
 t0 = time.perf_counter(); eng.load(pr.prec.diag_stack, pr.prec.off_stack, pr.info.reshape(1, 51, 4), pr.mean.reshape(1, 51, 4),
          np.linspace(0, 1, 51)[None, :, None] * np.array([2.0, 1.5, 0, 0])[None, None, :]); eng.step(iters, sync=True)
 wall = (time.perf_counter() - t0) * 1e3
-print(f"C1 lanes={eng.lanes()} per-iter select={ms[0]/iters:.3f} factor={ms[1]/iters:.3f} control={ms[2]/iters:.3f} ms; graph wall {wall/iters:.3f} ms/iter")
+print(f"C1 lanes={eng.lanes()} per-iter bisect={ms[0]/iters:.3f} commit={ms[1]/iters:.3f} factor={ms[2]/iters:.3f} control={ms[3]/iters:.3f} ms; graph wall {wall/iters:.3f} ms/iter")

@@ -15,5 +15,5 @@ eng.load(prior.prec.diag_stack, prior.prec.off_stack, info, pmean, init)
 eng.step(1, sync=True)
 ms = eng.step_profiled(iters)
 s = eng.summary()
-print(f"B={B} lanes={eng.lanes()} ms/iter select={ms[0]/iters:.2f} factor={ms[1]/iters:.3f} control={ms[2]/iters:.3f} "
+print(f"B={B} lanes={eng.lanes()} ms/iter bisect={ms[0]/iters:.2f} commit={ms[1]/iters:.2f} factor={ms[2]/iters:.3f} control={ms[3]/iters:.3f} "
       f"status={set(s['status'].tolist())} iters={s['iterations'][:3]}")
