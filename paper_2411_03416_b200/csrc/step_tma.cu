@@ -60,10 +60,12 @@ struct Ly {
 // Compile-time shared-memory layout of one CTA (32 lane slots = P plans x L
 // lanes, two warps). Every TMA box lands on a 128-byte boundary: row starts
 // are rounded to a multiple of cx_gran(width) rows.
-template <int N, int L, bool KS>
+template <int N, int L, bool KS, bool CM>
 struct Lay {
   static constexpr int T = N * (N + 1) / 2, N2 = N * N;
-  static constexpr int P = 32 / L, Pb = P, Kb = KS ? 2 : P, LPb = 32;
+  // LPb: scratch columns per CTA — one per lane slot in the bisection, one per
+  // plan in the commit (only its write slot runs)
+  static constexpr int P = 32 / L, Pb = P, Kb = KS ? 2 : P, LPb = CM ? P : 32;
   static constexpr int gP = cx_gran(Pb), gK = cx_gran(Kb);
   // pass B plan rows: LD T | GD T | G N | ETA N | V N | LO N2
   static constexpr int B0 = 0, B1 = cx_round(B0 + T, gP), B2 = cx_round(B1 + T, gP),
@@ -120,7 +122,7 @@ template <int N, int L, bool COMMIT, bool KS>
 __global__ void __launch_bounds__(64)
 select_step_v3_kernel(const __grid_constant__ Args a) {
   using Y = Ly<N>;
-  using LO = Lay<N, L, KS>;
+  using LO = Lay<N, L, KS, COMMIT>;
   constexpr int T = Y::T, N2 = Y::N2, SE = Y::SE;
   // dynamic shared memory only (no static __shared__): the window starts
   // 1 KB-aligned, so the compile-time layout keeps every TMA box 128-B aligned
@@ -152,7 +154,8 @@ select_step_v3_kernel(const __grid_constant__ Args a) {
   __syncthreads();
 
   double* scr = a.scratch;
-  const int64_t sc_col = b0 * L + lcol;  // global scratch column of this slot
+  // global scratch column: per lane slot (bisection) / per plan (commit)
+  auto sc_column = [&](int p_) -> int64_t { return COMMIT ? b0 + p_ : b0 * L + lcol; };
 
   auto slot = [&](int64_t s) { return smem + (s % LO::NS) * LO::STAGE; };
   // issue the TMA loads of one knot of a pass into slot s % NS
@@ -178,8 +181,9 @@ select_step_v3_kernel(const __grid_constant__ Args a) {
       tma3(pl + LO::F2 * Pb, &a.m_mu, (int)b0, 0, (int)i, bar);
       tma3(pl + LO::F3 * Pb, &a.m_pm, (int)b0, 0, (int)i, bar);
       tma3(pl + LO::F4 * Pb, &a.m_lo, (int)b0, 0, (int)i, bar);
-      tma3(st + LO::OFF_PHI, &a.m_phi, (int)(b0 * L), 0, (int)(i + 1), bar);        // PHIINV of knot i+1
-      tma3(st + LO::OFF_PSIY, &a.m_psiy, (int)(b0 * L), Y::S_LIPSI, (int)i, bar);  // LIPSI | Y of knot i
+      const int sc0 = (int)(COMMIT ? b0 : b0 * L);
+      tma3(st + LO::OFF_PHI, &a.m_phi, sc0, 0, (int)(i + 1), bar);        // PHIINV of knot i+1
+      tma3(st + LO::OFF_PSIY, &a.m_psiy, sc0, Y::S_LIPSI, (int)i, bar);  // LIPSI | Y of knot i
     }
   };
   auto wait_slot = [&](int64_t s) {
@@ -273,7 +277,7 @@ select_step_v3_kernel(const __grid_constant__ Args a) {
         fail_knot = (int)i;
         continue;
       }
-      double* sc = scr + (i * SE) * a.BLp + sc_col;
+      double* sc = scr + (i * SE) * a.BLp + sc_column(p);
       if (role == 0) {
         ld_sum += 2.0 * log(pp);
         // Phi^{-1} = Li^T Li -> scratch for the covariance sweep
@@ -325,7 +329,7 @@ select_step_v3_kernel(const __grid_constant__ Args a) {
     double Sig[T], mprev[N], dprev[N], dpprev[N], part[N];
     double trace = 0.0, mahal = 0.0, sh2 = 0.0, pq_c = 0.0, ptr_c = 0.0;
     if (passF && role == 0) {
-      const double* sc = scr + sc_col;  // Sigma_00 = Phi_0^{-1}
+      const double* sc = scr + sc_column(p);  // Sigma_00 = Phi_0^{-1}
 #pragma unroll
       for (int q = 0; q < T; ++q) Sig[q] = sc[(Y::S_PHI + q) * a.BLp];
     }
@@ -346,8 +350,9 @@ select_step_v3_kernel(const __grid_constant__ Args a) {
       auto kv = [&](int row) { return pr[row * Kb + kcol]; };
       auto pvp = [&](int row) { return plp[row * Pb + p]; };
       auto kvp = [&](int row) { return prp[row * Kb + kcol]; };
-      auto phi = [&](int q) { return st[LO::OFF_PHI + q * LP + lcol]; };
-      auto psi = [&](int q) { return st[LO::OFF_PSIY + q * LP + lcol]; };  // LIPSI rows then Y rows
+      const int scs = COMMIT ? p : lcol;  // this slot's scratch column in the stage
+      auto phi = [&](int q) { return st[LO::OFF_PHI + q * LO::LPb + scs]; };
+      auto psi = [&](int q) { return st[LO::OFF_PSIY + q * LO::LPb + scs]; };  // LIPSI rows then Y rows
       if (passF && role == 1) {
         // ---- mean: mu'_i = Li^T (y_i - Li S_{i-1,i}^T mu'_{i-1})
         double m[N];
@@ -614,15 +619,17 @@ static int launch_v3(const V2Launch& q, const int L, const bool commit, cudaStre
   a.ksp = q.kshared ? 0 : 1;
   const int64_t K = q.K, K1 = std::max<int64_t>(K - 1, 1);
   const int64_t KW = q.kshared ? 2 : q.Bp;
-  const int64_t BLp = (q.Bp * L) + 64;
+  // scratch columns: one per lane slot (bisection) or one per plan (commit)
+  const int SW = commit ? Pb : (P * L < 2 ? 2 : P * L);
+  const int64_t BLp = (commit ? q.Bp : q.Bp * L) + 64;
   int r;
   if ((r = v3::make_map(&a.m_ld, q.ld, q.Bp, T, K, Pb, T)) || (r = v3::make_map(&a.m_lo, q.lo, q.Bp, N2, K1, Pb, N2)) ||
       (r = v3::make_map(&a.m_kd, q.kd, KW, T, K, Kb, T)) || (r = v3::make_map(&a.m_ko, q.ko, KW, N2, K1, Kb, N2)) ||
       (r = v3::make_map(&a.m_gd, q.gd, q.Bp, T, K, Pb, T)) || (r = v3::make_map(&a.m_g, q.g, q.Bp, n, K, Pb, n)) ||
       (r = v3::make_map(&a.m_eta, q.eta, q.Bp, n, K, Pb, n)) || (r = v3::make_map(&a.m_v, q.v, q.Bp, n, K, Pb, n)) ||
       (r = v3::make_map(&a.m_mu, q.mu, q.Bp, n, K, Pb, n)) || (r = v3::make_map(&a.m_pm, q.pmean, q.Bp, n, K, Pb, n)) ||
-      (r = v3::make_map(&a.m_phi, q.scratch, BLp, SE, K, P * L < 2 ? 2 : P * L, T)) ||
-      (r = v3::make_map(&a.m_psiy, q.scratch, BLp, SE, K, P * L < 2 ? 2 : P * L, T + n)))
+      (r = v3::make_map(&a.m_phi, q.scratch, BLp, SE, K, SW, T)) ||
+      (r = v3::make_map(&a.m_psiy, q.scratch, BLp, SE, K, SW, T + n)))
     return r;
   a.o_mu = q.o_mu; a.o_ld = q.o_ld; a.o_lo = q.o_lo; a.o_cov = q.o_cov; a.o_cr = q.o_cr; a.o_v = q.o_v;
   a.beta = q.beta; a.kl = q.kl; a.ld_next = q.ld_next; a.shift = q.shift; a.prior_cost = q.prior_cost;
@@ -636,7 +643,7 @@ static int launch_v3(const V2Launch& q, const int L, const bool commit, cudaStre
   // one stage: plan rows | prior rows | PHI rows (lanes) | LIPSI+Y rows (lanes).
   // Every array's box starts on a 128-byte boundary (TMA destination rule):
   // row starts are rounded to a multiple of 16 / gcd(width, 16) rows.
-  const int LPb = P * L < 2 ? 2 : P * L;
+  const int LPb = SW;
   auto gran = [](int width) {
     int g = 16;
     while (g > 1 && (width * g) % 16 == 0 && (width * (g / 2)) % 16 == 0) g /= 2;
@@ -667,7 +674,7 @@ static int launch_v3(const V2Launch& q, const int L, const bool commit, cudaStre
   const unsigned grid = (unsigned)((q.nplans + P - 1) / P);
 #define GVP_V3_KS(NN, LL, CC, KK)                                                               \
   {                                                                                             \
-    using LOH = v3::Lay<NN, LL, KK>;                                                            \
+    using LOH = v3::Lay<NN, LL, KK, CC>;                                                            \
     if (LOH::TX_B != a.bytes_B || LOH::TX_F != a.bytes_F || LOH::STAGE != a.stage_doubles) {   \
       set_error("internal: device/host stage layout mismatch");                                 \
       return GVP_ERR_ARG;                                                                       \
@@ -680,7 +687,11 @@ static int launch_v3(const V2Launch& q, const int L, const bool commit, cudaStre
   if (q.kshared) GVP_V3_KS(NN, LL, CC, true) else GVP_V3_KS(NN, LL, CC, false)
 #define GVP_V3_L(NN)                           \
   if (commit) {                                \
-    GVP_V3(NN, 1, true)                        \
+    switch (L) {                               \
+      case 1: GVP_V3(NN, 1, true) break;       \
+      case 4: GVP_V3(NN, 4, true) break;       \
+      default: GVP_V3(NN, 16, true) break;     \
+    }                                          \
   } else {                                     \
     switch (L) {                               \
       case 1: GVP_V3(NN, 1, false) break;      \
@@ -726,7 +737,16 @@ int launch_select_bisect(const V2Launch& q, cudaStream_t s) {
 // the commit of the accepted beta: next iterate, marginals, KL, log det, costs
 int launch_select_commit(const V2Launch& q, cudaStream_t s) {
   if (q.nplans == 0 || q.K == 0) return GVP_OK;
-  return launch_v3(q, 1, true, s);
+  // One write-mode probe per plan. The commit is bound by each warp's serial
+  // per-knot latency (and TMA latency), not by lanes: few plans per CTA keep
+  // the stage small (deep prefetch ring) and spread plans over more SMs.
+  // GVP_COMMIT_LANES overrides (A/B measurements).
+  static const int forced = [] {
+    const char* e = std::getenv("GVP_COMMIT_LANES");
+    return e ? std::atoi(e) : 0;
+  }();
+  const int L = forced == 1 || forced == 4 || forced == 16 ? forced : (q.nplans <= 2 ? 16 : 1);
+  return launch_v3(q, L, true, s);
 }
 
 int launch_select_step_v2(const V2Launch& q, cudaStream_t s) {
