@@ -631,25 +631,49 @@ __global__ void __launch_bounds__(64) probe_fused_kernel(const __grid_constant__
   }
 }
 
-// e = K mu + g - eta per knot (plan-minor, the probe's beta-free residual)
-__global__ void residual_kernel(int B, int64_t K, int n, int64_t Bp, const double* kd, const double* ko,
-                                int64_t KW, bool kshared, const double* mu, const double* g,
-                                const double* eta, double* e) {
+// e = K mu + g - eta per knot (plan-minor, the probe's beta-free residual).
+// One thread per (plan, run of kRun knots): the mean window slides through
+// registers, so every mean block is read about once and all loads are
+// coalesced across plans.
+constexpr int kRun = 8;
+template <int N>
+__global__ void __launch_bounds__(128, 4) residual_kernel(int B, int64_t K, int64_t Bp, const double* kd, const double* ko, int64_t KW,
+                                bool kshared, const double* mu, const double* g, const double* eta, double* e) {
+  constexpr int T = N * (N + 1) / 2, N2 = N * N;
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= K * Bp) return;
-  const int64_t i = t / Bp, b = t % Bp;
+  const int64_t runs = (K + kRun - 1) / kRun;
+  if (t >= runs * Bp) return;
+  const int64_t b = t % Bp, i0 = (t / Bp) * kRun;
   if (b >= B) return;
-  const int T = n * (n + 1) / 2, N2 = n * n;
   const int64_t kc = kshared ? 0 : b;
-  for (int r = 0; r < n; ++r) {
-    double acc = 0.0;
-    for (int q = 0; q < n; ++q) {
-      const int tq = r >= q ? r * (r + 1) / 2 + q : q * (q + 1) / 2 + r;
-      acc += kd[(i * T + tq) * KW + kc] * mu[(i * n + q) * Bp + b];
-      if (i > 0) acc += ko[((i - 1) * N2 + q * n + r) * KW + kc] * mu[((i - 1) * n + q) * Bp + b];
-      if (i + 1 < K) acc += ko[(i * N2 + r * n + q) * KW + kc] * mu[((i + 1) * n + q) * Bp + b];
+  auto ld_mu = [&](int64_t i, double (&m)[N]) {
+#pragma unroll
+    for (int r = 0; r < N; ++r) m[r] = (i >= 0 && i < K) ? mu[(i * N + r) * Bp + b] : 0.0;
+  };
+  double mp[N], mc[N], mn[N];
+  ld_mu(i0 - 1, mp);
+  ld_mu(i0, mc);
+  const int64_t i1 = i0 + kRun < K ? i0 + kRun : K;
+#pragma unroll 1
+  for (int64_t i = i0; i < i1; ++i) {
+    ld_mu(i + 1, mn);
+#pragma unroll 1
+    for (int r = 0; r < N; ++r) {
+      double acc = 0.0;
+#pragma unroll
+      for (int q = 0; q < N; ++q) {
+        const int tq = r >= q ? r * (r + 1) / 2 + q : q * (q + 1) / 2 + r;
+        acc += kd[(i * T + tq) * KW + kc] * mc[q];
+        if (i > 0) acc += ko[((i - 1) * N2 + q * N + r) * KW + kc] * mp[q];
+        if (i + 1 < K) acc += ko[(i * N2 + r * N + q) * KW + kc] * mn[q];
+      }
+      e[(i * N + r) * Bp + b] = (acc + g[(i * N + r) * Bp + b]) - eta[(i * N + r) * Bp + b];
     }
-    e[(i * n + r) * Bp + b] = (acc + g[(i * n + r) * Bp + b]) - eta[(i * n + r) * Bp + b];
+#pragma unroll
+    for (int r = 0; r < N; ++r) {
+      mp[r] = mc[r];
+      mc[r] = mn[r];
+    }
   }
 }
 
@@ -669,10 +693,17 @@ int launch_probe(const V2Launch& q, const int L, cudaStream_t s) {
   const int64_t KW = q.kshared ? 2 : q.Bp;
   double* e = q.scratch + probe_residual_offset(q.nplans, K, n);
   {
-    const int64_t total = K * q.Bp;
-    const int tb = 256;
-    v4::residual_kernel<<<(unsigned)((total + tb - 1) / tb), tb, 0, s>>>(
-        q.nplans, K, n, q.Bp, q.kd, q.ko, KW, q.kshared, q.mu, q.g, q.eta, e);
+    const int64_t total = (K + v4::kRun - 1) / v4::kRun * q.Bp;
+    const int tb = 128;
+    const unsigned nb = (unsigned)((total + tb - 1) / tb);
+    switch (n) {
+      case 2: v4::residual_kernel<2><<<nb, tb, 0, s>>>(q.nplans, K, q.Bp, q.kd, q.ko, KW, q.kshared, q.mu, q.g, q.eta, e); break;
+      case 4: v4::residual_kernel<4><<<nb, tb, 0, s>>>(q.nplans, K, q.Bp, q.kd, q.ko, KW, q.kshared, q.mu, q.g, q.eta, e); break;
+      case 6: v4::residual_kernel<6><<<nb, tb, 0, s>>>(q.nplans, K, q.Bp, q.kd, q.ko, KW, q.kshared, q.mu, q.g, q.eta, e); break;
+      default:
+        set_error("step kernel supports n in {2, 4, 6}");
+        return GVP_ERR_UNSUPPORTED;
+    }
   }
   v4::Args a;
   std::memset(&a, 0, sizeof(a));
