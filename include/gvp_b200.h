@@ -215,6 +215,26 @@ int64_t gvp_engine_launches(gvp_engine* e);
 int gvp_engine_trace_probes(gvp_engine* e, int32_t max_probes);
 int gvp_engine_get_probes(gvp_engine* e, double* log, int32_t* counts);
 
+/* ------------------------------------------------ iP-GVIMP on the device */
+/* Statistical linearisation of the planar quadrotor (slr.py:69-92) for B
+ * nominal trajectories: host arrays means (B,K,6), covs (B,K,6,6), rule points
+ * (Q,6) / weights (Q), params = {1/mass, length/inertia, gravity}. Out: the
+ * LTV triples A (B,K,6,6), a (B,K,6) (B_i is the constant input matrix).
+ * status/where per plan: GVP_ERR_SQRT (covariance needs gaussian_sqrt's eigh
+ * root), GVP_ERR_NONFINITE (euler_step non-finite), GVP_ERR_NOT_SPD (P_xx). */
+int gvp_slr_quadrotor(int32_t nplans, int32_t K, const double* means, const double* covs, const double* points,
+                      const double* weights, int32_t Q, double dt, const double* params, double* A, double* a,
+                      int32_t* status, int32_t* where);
+/* Anchored LTV prior assembly (prior.py:56-170, transition_kernel + grammian +
+ * assemble_prior) for B plans of S steps, n = 6: A (B,S,6,6), a (B,S,6),
+ * B (B,S,6,m), Gauss-Legendre nodes/weights on [-1,1]. Out: Phi (B,S,6,6),
+ * offsets (B,S,6), Grammians (B,S,6,6), precision diag (B,S+1,6,6) / off
+ * (B,S,6,6) and information (B,S+1,6). The anchored mean is gvp_gbp_mean_solve. */
+int gvp_prior_assemble(int32_t nplans, int32_t S, int32_t n, int32_t m, const double* A, const double* a,
+                       const double* B, double dt, double q_c, double sigma_b, const double* x0, const double* goal,
+                       const double* gl_nodes, const double* gl_weights, int32_t nodes, double* phis, double* offs,
+                       double* grams, double* diag, double* off, double* info, int32_t* status, int32_t* where);
+
 /* ------------------------------------------------ batched device kernels (tests) */
 /* All pointers device memory, plan-minor layout with nplans plans, async on
  * `stream` (a cudaStream_t; NULL = legacy default stream). */

@@ -87,6 +87,11 @@ _SIGS = {
     "gvp_engine_launches": (C.c_int64, [C.c_void_p]),
     "gvp_engine_lanes": (C.c_int32, [C.c_void_p]),
     "gvp_engine_trace_probes": (C.c_int, [C.c_void_p, C.c_int32]),
+    "gvp_slr_quadrotor": (C.c_int, [C.c_int32, C.c_int32, _dp, _dp, _dp, _dp, C.c_int32, C.c_double, _dp, _dp,
+                                    _dp, _i32p, _i32p]),
+    "gvp_prior_assemble": (C.c_int, [C.c_int32, C.c_int32, C.c_int32, C.c_int32, _dp, _dp, _dp, C.c_double,
+                                     C.c_double, C.c_double, _dp, _dp, _dp, _dp, C.c_int32, _dp, _dp, _dp, _dp,
+                                     _dp, _dp, _i32p, _i32p]),
     "gvp_engine_get_probes": (C.c_int, [C.c_void_p, _dp, _i32p]),
     "gvp_set_step_lanes": (C.c_int, [C.c_int32]),
     "gvp_chain_scratch_doubles": (C.c_int64, [C.c_int32, C.c_int64, C.c_int32, C.c_int32]),
