@@ -401,4 +401,6 @@ static inline int make_map(CUtensorMap* m, const double* base, int64_t W, int64_
 // one-pass bisection (step_probe.cu); its residual buffer lives in the step scratch
 int launch_probe(const V2Launch& q, int L, cudaStream_t s);
 int64_t probe_residual_offset(int nplans, int64_t K, int n);
+// commit with the output work split off the two recursion warps (commit.cu)
+int launch_commit_split(const V2Launch& q, cudaStream_t s);
 }  // namespace gvp

@@ -745,6 +745,8 @@ int launch_select_commit(const V2Launch& q, cudaStream_t s) {
     const char* e = std::getenv("GVP_COMMIT_LANES");
     return e ? std::atoi(e) : 0;
   }();
+  // default: the 4-warp commit (commit.cu); GVP_COMMIT_LANES selects this file's kernel
+  if (forced == 0) return launch_commit_split(q, s);
   const int L = forced == 1 || forced == 4 || forced == 16 ? forced : (q.nplans <= 2 ? 16 : 1);
   return launch_v3(q, L, true, s);
 }
