@@ -550,7 +550,7 @@ extern "C" int gvp_select_step_size(const double* mean, const double* diag, cons
     return select_step_size_v1(mean, diag, off, kdiag, koff, info, g_mu, gdiag, goff, nblocks, n,
                                temp, kl_bound, beta_min, beta_max, beta, kl, out_mean, out_diag,
                                out_off, covs, crosses, probe_log, max_probes, nprobes, where);
-  // ---- packed layout, TMA-staged step kernel with speculative lanes (step_tma.cu).
+  // ---- packed layout, TMA-staged probe + commit kernels (step_select.cu).
   // The step kernel wants an even plan stride: the plan goes in column 0 of
   // 2-wide arrays (column 1 is a copy), the prior is the 2-wide shared prior.
   cudaStream_t s = C.stream;

