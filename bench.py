@@ -432,11 +432,14 @@ def main():
         fp64_peak = 148 * 64 * 2 * sm_mhz * 1e6 / 1e12  # 64 DFMA/clk/SM (ncu peak_sustained)
         bis_flops = probes / steps_prof * K * fl["total"]
         ach = bis_flops / (bis_ms / 1e3) / 1e12
+        # the engine runs the split probe kernel while the grid is below 2 CTAs per SM
+        lanes = eng.lanes()
+        probe_kernel = "probe_split_kernel" if (B + 1) // 2 * 2 * lanes // 32 < 2 * 148 else "probe_fused_kernel"
         traffic = None
         tpath = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "ncu_traffic.json")
         if os.path.exists(tpath):
             with open(tpath) as fh:
-                traffic = json.load(fh).get("probe_fused_kernel")
+                traffic = json.load(fh).get(probe_kernel)
         #  factor stage: 8 (n^2 + 3n + 1) = 232 B per factor
         fac_bytes = B * F * 232
         fac_ach = fac_bytes / (fac_ms / 1e3) / 1e9 if fac_ms > 0 else None
@@ -465,10 +468,11 @@ def main():
             "gpu_launches": int(launches),
             "kernel_ms_per_step": {"bisection": bis_ms, "commit": com_ms, "factor_grads": fac_ms,
                                    "control": ctl_ms},
-            "roofline": {"kernel": "bisection (probe_fused_kernel)", "bound": "fp64", "achieved": ach,
+            "roofline": {"kernel": f"bisection ({probe_kernel})", "bound": "fp64", "achieved": ach,
                          "peak": fp64_peak, "unit": "TFLOP/s", "frac": ach / fp64_peak, "traffic": traffic,
                          "traffic_unit": "bytes/launch (ncu dram read+write)",
                          "flops_per_probe_knot": fl["total"], "probes_per_plan_iter": probes / max(1, B * steps_prof),
+                         "lanes_per_plan": lanes,
                          "peak_source": "148 SMs x 64 DFMA/clk (ncu sm__sass_thread_inst_executed_op_dfma"
                                         "_pred_on.sum.peak_sustained) x 2 x sm_max_mhz (MEASURED_PEAKS.json)",
                          "factor_grads": {"bound": "hbm", "achieved": fac_ach, "peak": hbm, "unit": "GB/s",
@@ -488,12 +492,15 @@ def main():
         cfg1 = P.OptimizerConfig(k_q=3, kl_bound=10.0, beta_max=0.5, max_iters=600)
         pr1 = P.assemble_prior(sys1, np.zeros(4), np.array([2.0, 1.5, 0, 0]), 1.0, 1e-3)
         P.run_pgvimp(sys1, env1, cfg1, np.zeros(4), np.array([2.0, 1.5, 0, 0]), 1.0, 1e-3, prior=pr1)  # warm
-        t0 = time.perf_counter()
-        r1 = P.run_pgvimp(sys1, env1, cfg1, np.zeros(4), np.array([2.0, 1.5, 0, 0]), 1.0, 1e-3, prior=pr1)
-        c1_ms = (time.perf_counter() - t0) * 1e3
+        runs = []
+        for _ in range(3):  # wall clock of the whole call (engine setup, 94 iterations, fetch)
+            t0 = time.perf_counter()
+            r1 = P.run_pgvimp(sys1, env1, cfg1, np.zeros(4), np.array([2.0, 1.5, 0, 0]), 1.0, 1e-3, prior=pr1)
+            runs.append((time.perf_counter() - t0) * 1e3)
         result["time_to_converge"] = {"config": "C1 pinned: point2d N=50, k_q=3, kl_bound=10, beta_max=0.5",
-                                      "ms": c1_ms, "iterations": r1.iterations, "converged": r1.converged,
-                                      "reference_iterations": 94}
+                                      "ms": min(runs), "ms_runs": runs, "iterations": r1.iterations,
+                                      "converged": r1.converged, "reference_iterations": 94,
+                                      "ms_per_iteration": min(runs) / max(r1.iterations, 1)}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cb, err = cpu_baseline_reference(1)
         result["cpu_baseline"] = cb if cb else {"value": None, "error": err}

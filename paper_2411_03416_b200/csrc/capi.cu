@@ -522,8 +522,8 @@ static int select_step_size_v1(const double* mean, const double* diag, const dou
 }
 
 extern "C" int gvp_set_step_lanes(int32_t lanes) {
-  if (lanes != 1 && lanes != 4 && lanes != 8 && lanes != 16) {
-    set_error("lanes must be 1, 4, 8 or 16");
+  if (lanes != 1 && lanes != 2 && lanes != 4 && lanes != 8 && lanes != 16) {
+    set_error("lanes must be 1, 2, 4, 8 or 16");
     return GVP_ERR_ARG;
   }
   g_step_lanes = lanes;

@@ -247,12 +247,13 @@ struct gvp_engine {
 
 static int pick_lanes(const gvp_plan_config* cfg, int B) {
   if (cfg->spec_lanes > 0) return cfg->spec_lanes;
-  // Speculative lanes only pay while the GPU has idle SMs: measured on B200
-  // (C5, 4096 plans x 1001 knots) one lane per plan beats 4/8/16 lanes, while
-  // a single plan gains ~2x from 16 lanes. Aim at <= ~2 CTAs (4 warps) per SM.
+  // Speculative lanes only pay while the GPU would otherwise idle: take the
+  // fewest lanes that give ~6 probe warps per SM (the split probe kernel runs
+  // 4 warps per 32 lane slots). B200, C5 (4096 plans x 1001 knots): 2 lanes
+  // (split) 11.6 ms < 4 lanes (fused) 12.0 < 4 lanes (split) 14.0 per
+  // bisection; a single plan takes 16 lanes.
   int L = 1;
-  while (L < 16 && (int64_t)B * L < 148 * 64) L *= 2;
-  if (L == 2) L = 4;
+  while (L < 16 && (int64_t)B * L * 4 / 32 < 148 * 6) L *= 2;
   return L;
 }
 
@@ -277,8 +278,8 @@ extern "C" int gvp_engine_create(gvp_engine** out, int32_t nplans, int64_t nknot
     return GVP_ERR_ARG;
   }
   const int lanes = pick_lanes(cfg, nplans);
-  if (lanes != 1 && lanes != 4 && lanes != 8 && lanes != 16) {
-    set_error("spec_lanes must be 0 (auto), 1, 4, 8 or 16");
+  if (lanes != 1 && lanes != 2 && lanes != 4 && lanes != 8 && lanes != 16) {
+    set_error("spec_lanes must be 0 (auto), 1, 2, 4, 8 or 16");
     return GVP_ERR_ARG;
   }
   int ndev = 0;

@@ -755,6 +755,7 @@ int launch_probe(const V2Launch& q, const int L, cudaStream_t s) {
 #define GVP_V4_L(NN)                     \
   switch (L) {                           \
     case 1: GVP_V4(NN, 1) break;         \
+    case 2: GVP_V4(NN, 2) break;         \
     case 4: GVP_V4(NN, 4) break;         \
     case 8: GVP_V4(NN, 8) break;         \
     default: GVP_V4(NN, 16) break;       \

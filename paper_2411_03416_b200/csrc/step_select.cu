@@ -23,8 +23,8 @@ int64_t step_scratch_doubles(int nplans, int64_t K, int n, int lanes) {
 int launch_select_bisect(const V2Launch& q, cudaStream_t s) {
   if (q.nplans == 0 || q.K == 0) return GVP_OK;
   const int L = q.lanes;
-  if (L != 1 && L != 4 && L != 8 && L != 16) {
-    set_error("lanes must be 1, 4, 8 or 16");
+  if (L != 1 && L != 2 && L != 4 && L != 8 && L != 16) {
+    set_error("lanes must be 1, 2, 4, 8 or 16");
     return GVP_ERR_ARG;
   }
   if (q.Bp % 2 || q.Bp < 2) {
