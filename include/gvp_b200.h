@@ -209,6 +209,20 @@ int gvp_engine_device_state(gvp_engine* e, double** mean, double** diag, double*
                             double** covs, double** crosses);
 /* Launch counters: kernels launched by this engine since create. */
 int64_t gvp_engine_launches(gvp_engine* e);
+/* Map bank: nmaps signed-distance maps with the engine's grid
+ * geometry, plan b reading map plan_map[b] (nreal entries). set: host grids
+ * (nmaps x row-major (ny,nx) / (nz,ny,nx)); raster: rasterised on the device
+ * from primitive lists like rasterize (sdf.py:156-185) — map m owns primitives
+ * [prim_off[m], prim_off[m+1]), kind 0 disc/sphere (center, radius, pad) or
+ * 1 box (center, halfextents), 2*dim doubles each. Call before stepping. */
+int gvp_engine_set_map_bank(gvp_engine* e, int32_t nmaps, const double* grids, const int32_t* plan_map);
+int gvp_engine_raster_map_bank(gvp_engine* e, int32_t nmaps, const int32_t* prim_off, const int32_t* kinds,
+                               const double* params, const int32_t* plan_map);
+/* Drop-in rasterize (sdf.py:156-185), bit-identical values: counts per axis
+ * (x, y[, z]) as the reference derives them from bounds, out row-major
+ * (ny, nx) or (nz, ny, nx) in host memory. */
+int gvp_rasterize(int32_t dim, const int64_t* counts, const double* origin, double cell_size, int32_t nprim,
+                  const int32_t* kinds, const double* params, double* out);
 /* Probe trace of the step-size search (optimizer.py:188-231 `trace`): per
  * plan the last iteration's probes as (beta, spd, kl) rows, at most
  * max_probes each. Enable before the first step. */

@@ -87,6 +87,9 @@ _SIGS = {
     "gvp_engine_launches": (C.c_int64, [C.c_void_p]),
     "gvp_engine_lanes": (C.c_int32, [C.c_void_p]),
     "gvp_engine_trace_probes": (C.c_int, [C.c_void_p, C.c_int32]),
+    "gvp_engine_set_map_bank": (C.c_int, [C.c_void_p, C.c_int32, _dp, _i32p]),
+    "gvp_engine_raster_map_bank": (C.c_int, [C.c_void_p, C.c_int32, _i32p, _i32p, _dp, _i32p]),
+    "gvp_rasterize": (C.c_int, [C.c_int32, _i64p, _dp, C.c_double, C.c_int32, _i32p, _dp, _dp]),
     "gvp_slr_quadrotor": (C.c_int, [C.c_int32, C.c_int32, _dp, _dp, _dp, _dp, C.c_int32, C.c_double, _dp, _dp,
                                     _dp, _i32p, _i32p]),
     "gvp_prior_assemble": (C.c_int, [C.c_int32, C.c_int32, C.c_int32, C.c_int32, _dp, _dp, _dp, C.c_double,

@@ -567,6 +567,85 @@ extern "C" int gvp_engine_device_state(gvp_engine* e, double** mean, double** di
 
 extern "C" int64_t gvp_engine_launches(gvp_engine* e) { return e->launches; }
 
+// Map bank: nmaps signed-distance maps with the engine's grid
+// geometry; plan b reads map plan_map[b]. From host grids (nmaps x (ny, nx) or
+// (nz, ny, nx), row-major) or rasterised on the device from primitive lists.
+static int install_bank(gvp_engine* e, int nmaps, const double* raw_dev, const int32_t* plan_map) {
+  for (int b = 0; b < e->nreal; ++b)
+    if (plan_map[b] < 0 || plan_map[b] >= nmaps) {
+      set_error("plan_map entry outside [0, nmaps)");
+      return GVP_ERR_ARG;
+    }
+  FieldDev f = e->field.dev;
+  const int64_t stride = packed_field_doubles(f);
+  double* bank = nullptr;
+  int* pm = nullptr;
+  int r;
+  if ((r = e->alloc(&bank, (size_t)stride * nmaps)) || (r = e->alloc(&pm, (size_t)e->B))) return r;
+  if ((r = pack_field_maps(f, nmaps, raw_dev, bank, e->stream))) return r;
+  std::vector<int> h(e->B);
+  for (int b = 0; b < e->B; ++b) h[b] = plan_map[b < e->nreal ? b : 0];  // padding plan = plan 0
+  GVP_CUDA(cudaMemcpyAsync(pm, h.data(), sizeof(int) * e->B, cudaMemcpyHostToDevice, e->stream));
+  GVP_CUDA(cudaStreamSynchronize(e->stream));
+  f.corners = bank;
+  f.plan_map = pm;
+  f.map_stride = stride;
+  e->field.dev = f;
+  if (e->graph) {  // the captured factor launch holds the old field
+    cudaGraphExecDestroy(e->graph);
+    e->graph = nullptr;
+  }
+  return GVP_OK;
+}
+
+extern "C" int gvp_engine_set_map_bank(gvp_engine* e, int32_t nmaps, const double* grids,
+                                       const int32_t* plan_map) {
+  if (!e || nmaps < 1 || !grids || !plan_map) return GVP_ERR_ARG;
+  const FieldDev& f = e->field.dev;
+  const int64_t cells = f.nx * f.ny * f.nz;
+  double* raw = nullptr;
+  GVP_CUDA(cudaMalloc(&raw, sizeof(double) * cells * nmaps));
+  cudaError_t ce = cudaMemcpyAsync(raw, grids, sizeof(double) * cells * nmaps, cudaMemcpyHostToDevice, e->stream);
+  int r = ce == cudaSuccess ? install_bank(e, nmaps, raw, plan_map) : GVP_ERR_CUDA;
+  if (ce != cudaSuccess) set_error(cudaGetErrorString(ce));
+  cudaStreamSynchronize(e->stream);
+  cudaFree(raw);
+  return r;
+}
+
+extern "C" int gvp_engine_raster_map_bank(gvp_engine* e, int32_t nmaps, const int32_t* prim_off,
+                                          const int32_t* kinds, const double* params, const int32_t* plan_map) {
+  if (!e || nmaps < 1 || !prim_off || !plan_map) return GVP_ERR_ARG;
+  const FieldDev& f = e->field.dev;
+  const int dim = f.ndim;
+  const int nprim = prim_off[nmaps];
+  for (int m = 0; m < nmaps; ++m)
+    if (prim_off[m] > prim_off[m + 1] || prim_off[m] < 0) return GVP_ERR_ARG;
+  if (nprim > 0 && (!kinds || !params)) return GVP_ERR_ARG;
+  const int64_t cells = f.nx * f.ny * f.nz;
+  const int64_t counts[3] = {f.nx, f.ny, f.nz};
+  const double origin[3] = {f.ox, f.oy, f.oz};
+  double *raw = nullptr, *par = nullptr;
+  int *off = nullptr, *kd = nullptr;
+  GVP_CUDA(cudaMalloc(&raw, sizeof(double) * cells * nmaps));
+  GVP_CUDA(cudaMalloc(&par, sizeof(double) * (2 * dim * nprim + 1)));
+  GVP_CUDA(cudaMalloc(&off, sizeof(int) * (nmaps + 1)));
+  GVP_CUDA(cudaMalloc(&kd, sizeof(int) * (nprim + 1)));
+  GVP_CUDA(cudaMemcpyAsync(off, prim_off, sizeof(int) * (nmaps + 1), cudaMemcpyHostToDevice, e->stream));
+  if (nprim) {
+    GVP_CUDA(cudaMemcpyAsync(kd, kinds, sizeof(int) * nprim, cudaMemcpyHostToDevice, e->stream));
+    GVP_CUDA(cudaMemcpyAsync(par, params, sizeof(double) * 2 * dim * nprim, cudaMemcpyHostToDevice, e->stream));
+  }
+  int r = rasterize_maps(dim, counts, origin, f.cell, nmaps, off, kd, par, raw, e->stream);
+  if (!r) r = install_bank(e, nmaps, raw, plan_map);
+  cudaStreamSynchronize(e->stream);
+  cudaFree(raw);
+  cudaFree(par);
+  cudaFree(off);
+  cudaFree(kd);
+  return r;
+}
+
 // Record every probe (beta, spd, kl) of each plan's step-size search; the log
 // holds the last iteration. Must be enabled before the first step.
 extern "C" int gvp_engine_trace_probes(gvp_engine* e, int32_t max_probes) {

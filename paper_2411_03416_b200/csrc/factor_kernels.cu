@@ -378,6 +378,7 @@ factor_grads_kernel(int nplans, int64_t nfac, View mean, View covs, RuleDev R, F
   }
   const int64_t knot = f + 1;  // interior factors 1..N-1 (factors.py:159-164)
   if (active && !active[b]) return;
+  if (F.plan_map) F.corners += (int64_t)F.plan_map[b] * F.map_stride;  // this plan's map of the bank
 
   double mu[N], S[N][N], L[N][N];
   {

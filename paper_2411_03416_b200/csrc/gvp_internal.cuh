@@ -32,7 +32,20 @@ struct FieldDev {
   int64_t nx, ny, nz;
   double ox, oy, oz, cell, inv_cell;
   const double* corners;  // device
+  // map bank: plan b reads map plan_map[b] at corners + plan_map[b] * map_stride
+  const int* plan_map;    // device, nullptr = one map for every plan
+  int64_t map_stride;     // doubles per packed map
 };
+// corner-pack raw grids on the device (nmaps maps of the geometry in f) into dst
+int pack_field_maps(const FieldDev& f, int nmaps, const double* raw_dev, double* dst_dev, cudaStream_t s);
+int64_t packed_field_doubles(const FieldDev& f);
+// rasterize primitive unions on the device (sdf.py:134-185): per map m the
+// primitives [prim_off[m], prim_off[m+1]) of kinds (0 disc/sphere, 1 box) with
+// params [center(dim) | radius or halfextents(dim)] (2*dim doubles each);
+// raw row-major grids (nz, ny, nx) out
+int rasterize_maps(int dim, const int64_t* counts, const double* origin, double cell, int nmaps,
+                   const int* prim_off_dev, const int* kinds_dev, const double* params_dev, double* raw_dev,
+                   cudaStream_t s);
 
 struct Field {
   FieldDev dev{};

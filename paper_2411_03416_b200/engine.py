@@ -57,6 +57,7 @@ class PlanBatch:
         self._cfg = c
         h = C.c_void_p()
         grid = N.f64(sdf.values)
+        self._grid_dim = grid.ndim
         shape = np.asarray(grid.shape, dtype=np.int64)
         origin = N.f64(sdf.origin)
         code = self.lib.gvp_engine_create(C.byref(h), self.B, self.K, self.n, int(self.shared_prior),
@@ -143,6 +144,39 @@ class PlanBatch:
 
     def launches(self) -> int:
         return int(self.lib.gvp_engine_launches(self.handle))
+
+    def set_map_bank(self, maps, plan_map):
+        """Per-plan signed-distance maps: `maps` is a sequence of
+        SignedDistanceField (or raw value arrays) with the engine's grid
+        geometry; plan b reads maps[plan_map[b]]. Call before stepping."""
+        vals = [np.asarray(getattr(m, "values", m), dtype=np.float64) for m in maps]
+        grids = N.f64(np.stack(vals))
+        pm = np.ascontiguousarray(np.asarray(plan_map, dtype=np.int32))
+        if pm.shape != (self.B,):
+            raise ValueError(f"plan_map needs {self.B} entries")
+        self._ok(self.lib.gvp_engine_set_map_bank(self.handle, len(vals), N.ptr(grids), N.ptr(pm)),
+                 "gvp_engine_set_map_bank")
+
+    def raster_map_bank(self, primitive_lists, plan_map):
+        """Map bank rasterised on the device from primitive lists (one list of
+        Disc/Box per map, rasterize semantics on the engine's grid)."""
+        from .sdf import primitive_table
+
+        dim = self._grid_dim
+        off = np.zeros(len(primitive_lists) + 1, dtype=np.int32)
+        kinds, params = [], []
+        for m, prims in enumerate(primitive_lists):
+            k, p = primitive_table(list(prims), dim)
+            kinds.append(k)
+            params.append(p)
+            off[m + 1] = off[m] + len(prims)
+        kinds = np.ascontiguousarray(np.concatenate(kinds) if kinds else np.zeros(0, np.int32), dtype=np.int32)
+        params = N.f64(np.concatenate(params) if params else np.zeros((0, 2 * dim)))
+        pm = np.ascontiguousarray(np.asarray(plan_map, dtype=np.int32))
+        if pm.shape != (self.B,):
+            raise ValueError(f"plan_map needs {self.B} entries")
+        self._ok(self.lib.gvp_engine_raster_map_bank(self.handle, len(primitive_lists), N.ptr(off), N.ptr(kinds),
+                                                     N.ptr(params), N.ptr(pm)), "gvp_engine_raster_map_bank")
 
     def trace_probes(self, max_probes: int = 64):
         """Record each plan's step-size probes (optimizer.py:188-231 `trace`);
