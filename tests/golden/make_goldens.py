@@ -339,6 +339,42 @@ def slr():
     np.savez_compressed(os.path.join(HERE, "slr.npz"), **out)
 
 
+def configs():
+    """SURVEY §8d configurations the bench/engine specialise for, a few
+    iterations each: C2 (N=500, k_q=5: the 57-projection factor kernel) and
+    plan 0 of the C5 bench workload (N=1000, k_q=3, C2 map)."""
+    from gvplan.sdf import Box
+    out = {}
+    keys = ["beta", "temperature", "prior_cost", "collision_cost", "entropy_cost", "total_cost", "kl_step",
+            "mean_shift"]
+    c2map = rasterize([Box(center=np.array([5.0, 1.2]), halfextents=np.array([0.3, 3.4])),
+                       Box(center=np.array([5.0, 8.8]), halfextents=np.array([0.3, 3.4]))],
+                      bounds=[[-2, 12], [-2, 12]], cell_size=0.05)
+    env = Environment(sdf=c2map, model=CollisionModel(radius_eps=0.2, sigma_obs=8.0))
+    # C2: point2d N=500, T=10, k_q=5
+    cfg = OptimizerConfig(k_q=5, kl_bound=10.0, beta_max=0.5, max_iters=4)
+    res = run_pgvimp(point_robot_lti(2)(500, 10.0 / 500), env, cfg, np.zeros(4), np.array([10.0, 10.0, 0, 0]),
+                     1.0, 1e-3)
+    out["c2_records"] = np.array([[r[k] for k in keys] for r in res.records])
+    out["c2_final_mean"] = res.final.mean.reshape(501, 4)
+    # C5 plan 0: goal from the bench's generator (bench.c5_goals)
+    rng = np.random.default_rng(2411_03416)
+    goal = np.array([10.0, 10.0, 0.0, 0.0])
+    goal[:2] += rng.uniform(-0.5, 0.5, size=(1, 2))[0]
+    cfg = OptimizerConfig(k_q=3, kl_bound=10.0, beta_max=0.5, max_iters=3)
+    res = run_pgvimp(point_robot_lti(2)(1000, 10.0 / 1000), env, cfg, np.zeros(4), goal, 1.0, 1e-3)
+    out["c5p_goal"] = goal
+    out["c5p_records"] = np.array([[r[k] for k in keys] for r in res.records])
+    out["c5p_final_mean"] = res.final.mean.reshape(1001, 4)
+    # the reference's own probe log of the first iteration (beta, spd, KL)
+    log, restore = probe_log()
+    run_pgvimp(point_robot_lti(2)(1000, 10.0 / 1000), env, OptimizerConfig(k_q=3, kl_bound=10.0, beta_max=0.5,
+                                                                          max_iters=1), np.zeros(4), goal, 1.0, 1e-3)
+    restore()
+    out["c5p_probes1"] = np.array(log)
+    np.savez_compressed(os.path.join(HERE, "configs.npz"), **out)
+
+
 def slr_py():
     """The same iP-GVIMP run through the reference's pure-numpy kernel backend
     (GVPLAN_PURE_PYTHON=1, backend.py:14). The quadrotor run is ill-conditioned

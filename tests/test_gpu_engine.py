@@ -9,6 +9,7 @@ from conftest import golden, rel_err
 
 pytestmark = pytest.mark.gpu
 TOL = 1e-9
+MEAN_TOL_LONG = 2e-6  # iterate of an N >= 500 chain after several ill-conditioned mean solves
 
 
 @pytest.fixture(scope="module")
@@ -106,3 +107,66 @@ def test_engine_matches_oracle_driver(P):
     for a, b in zip(res.records, ref["records"]):
         for k in ("prior_cost", "collision_cost", "entropy_cost", "total_cost"):
             assert abs(a[k] - b[k]) <= TOL * max(1.0, abs(b[k])), (k, a[k], b[k])
+
+
+def _c2_env(P):
+    from paper_2411_03416_b200.sdf import Box
+    sdf = P.rasterize([Box(center=np.array([5.0, 1.2]), halfextents=np.array([0.3, 3.4])),
+                       Box(center=np.array([5.0, 8.8]), halfextents=np.array([0.3, 3.4]))],
+                      bounds=[[-2, 12], [-2, 12]], cell_size=0.05)
+    return P.Environment(sdf=sdf, model=P.CollisionModel(radius_eps=0.2, sigma_obs=8.0))
+
+
+def test_c2_config_matches_reference(P):
+    """C2: N=500, k_q=5 (57-projection factor kernel), 4 iterations."""
+    g = golden("configs")
+    cfg = P.OptimizerConfig(k_q=5, kl_bound=10.0, beta_max=0.5, max_iters=4)
+    res = P.run_pgvimp(P.point_robot_lti(2)(500, 10.0 / 500), _c2_env(P), cfg, np.zeros(4),
+                       np.array([10.0, 10.0, 0, 0]), 1.0, 1e-3)
+    keys = ["beta", "temperature", "prior_cost", "collision_cost", "entropy_cost", "total_cost", "kl_step",
+            "mean_shift"]
+    got = np.array([[r[k] for k in keys] for r in res.records])
+    assert np.array_equal(got[:, 0], g["c2_records"][:, 0])
+    assert rel_err(got[:, 2:7], g["c2_records"][:, 2:7]) <= TOL
+    # the mean solve S mu' = rhs has cond ~1e10 at N = 500 (sigma_b = 1e-3 anchors): two correct fp64
+    # solvers agree to ~cond * eps on the iterate (the p500 prior-mean test shows the reference itself
+    # 1.3e-9 from the exact solve after ONE solve); the records above stay within 1e-9
+    assert rel_err(res.final.mean.reshape(501, 4), g["c2_final_mean"]) <= MEAN_TOL_LONG
+
+
+def test_c5_bench_plan_matches_reference(P):
+    """Plan 0 of the bench workload (C5: N=1000, k_q=3, C2 map): the first
+    iteration's probe log against the reference's own (tests/golden configs).
+
+    At N=1000 the reference's KL is itself only good to ~1e-5 relative: its
+    trace_product (gbp.py:109-120) cancels terms ~1e4 down to ~4e3, so two
+    implementations of the same marginals sweep differ by 1e-4 in KL (and the
+    reference's Cython and numpy factor backends differ by 8e-6 on this very
+    probe). Decisions must agree outside that band; the probe right at the
+    bound (margin 3e-6) is the reference's coin flip. DESIGN.md §5."""
+    g = golden("configs")
+    ref = g["c5p_probes1"]
+    noise = 2e-4  # absolute KL noise of the reference here (2x its backend spread)
+    env = _c2_env(P)
+    sys_ltv = P.point_robot_lti(2)(1000, 10.0 / 1000)
+    prior = P.assemble_prior(sys_ltv, np.zeros(4), g["c5p_goal"], 1.0, 1e-3)
+    cfg = P.OptimizerConfig(k_q=3, kl_bound=10.0, beta_max=0.5, max_iters=2)
+    K = 1001
+    eng = P.PlanBatch(1, K, 4, env.sdf, env.model, P.smolyak_rule(3, 4), cfg)
+    eng.trace_probes(64)
+    init = np.linspace(0, 1, K)[None, :, None] * g["c5p_goal"][None, None, :]
+    eng.load(prior.prec.diag_stack, prior.prec.off_stack, prior.info.reshape(1, K, 4), prior.mean.reshape(1, K, 4),
+             init)
+    eng.step(1, sync=True)
+    got = eng.probes()[0]
+    eng.close()
+    for j, (rb, rs, rk) in enumerate(ref):
+        assert j < len(got)
+        gb, gs, gk = got[j]
+        assert gb == rb and gs == rs, j
+        if np.isfinite(rk):
+            assert abs(gk - rk) <= noise + 1e-5 * abs(rk), (j, gk, rk)
+            if abs(rk - 10.0) <= noise:
+                break  # inside the reference's own noise band: the searches may part here
+    else:
+        assert len(got) == len(ref)
