@@ -239,7 +239,7 @@ struct gvp_engine {
   int iteration_body() {
     int r = launch_select_step_v2(step_args(), stream);
     if (r) return r;
-    launches += 2;  // bisection + commit
+    launches += 3;  // residual + bisection probes + commit
     if ((r = factors())) return r;
     return control();
   }
@@ -442,7 +442,7 @@ extern "C" int gvp_engine_step(gvp_engine* e, int32_t iters, int32_t sync) {
       e->launches = before;  // counted per replay below
     }
     GVP_CUDA(cudaGraphLaunch(e->graph, s));
-    e->launches += 3 + (e->K > 2);
+    e->launches += 4 + (e->K > 2);  // residual, probes, commit, [factors], control
     ++e->iters_launched;
   }
   if (sync) GVP_CUDA(cudaStreamSynchronize(s));
@@ -460,7 +460,7 @@ extern "C" int gvp_engine_step_profiled(gvp_engine* e, int32_t iters, double* ms
     if (r) return r;
     GVP_CUDA(cudaEventRecord(ev[1], s));
     if ((r = launch_select_commit(e->step_args(), s))) return r;
-    e->launches += 2;
+    e->launches += 3;  // residual + bisection probes + commit
     GVP_CUDA(cudaEventRecord(ev[2], s));
     if ((r = e->factors())) return r;
     GVP_CUDA(cudaEventRecord(ev[3], s));
