@@ -130,7 +130,7 @@ int gvp_select_step_size(const double* mean, const double* diag, const double* o
                          double* crosses, double* probe_log, int32_t max_probes,
                          int32_t* nprobes, int64_t* where);
 
-/* Candidate lanes (1, 4, 8, 16, 32) gvp_select_step_size probes concurrently;
+/* Candidate lanes (1, 2, 4, 8, 16) gvp_select_step_size probes concurrently;
  * the beta sequence is the reference's for any value (default 32). */
 int gvp_set_step_lanes(int32_t lanes);
 
@@ -147,7 +147,7 @@ typedef struct gvp_plan_config {
   double tol_cost;
   double init_cov_scale;
   int32_t max_iters;
-  int32_t spec_lanes;    /* candidate betas probed concurrently per plan: 0 = auto, else 1/4/8/16/32 */
+  int32_t spec_lanes;    /* candidate betas probed concurrently per plan: 0 = auto, else 1/2/4/8/16 */
 } gvp_plan_config;
 
 typedef struct gvp_engine gvp_engine;
