@@ -131,7 +131,7 @@ int gvp_select_step_size(const double* mean, const double* diag, const double* o
                          int32_t* nprobes, int64_t* where);
 
 /* Candidate lanes (1, 2, 4, 8, 16) gvp_select_step_size probes concurrently;
- * the beta sequence is the reference's for any value (default 32). */
+ * the beta sequence is the reference's for any value (default 16). */
 int gvp_set_step_lanes(int32_t lanes);
 
 /* -------------------------------------------------------- 2. batched engine */
