@@ -249,6 +249,22 @@ int gvp_prior_assemble(int32_t nplans, int32_t S, int32_t n, int32_t m, const do
                        const double* gl_nodes, const double* gl_weights, int32_t nodes, double* phis, double* offs,
                        double* grams, double* diag, double* off, double* info, int32_t* status, int32_t* where);
 
+/* ------------------------------------------------ 7-DOF sphere arm */
+/* Factor moments (the factor_expectations contract, _kernels.pyx:132-177) for
+ * a 7-joint standard-DH arm covered by spheres: psi(q) = sigma sum_s
+ * max(r_s + eps - d(FK_s(q)), 0)^2, q = x[:7], n = 14. Host arrays: means
+ * (F,14), chols (F,14,14) lower; the rule's joint-space projection tables proj
+ * (NP,7), mom (NP,120) = [m0 | m1 (14) | m2 packed (105)], cnt (NP); 3D grid
+ * (nz,ny,nx), origin (x,y,z), cell; dh (7,4) = (a, d, alpha, theta offset),
+ * base (3); spheres: link (S, 0..7), geom (S,4) = (local xyz, radius).
+ * Out: e0 (F), e1 (F,14), e2 (F,14,14), oob (sphere centres outside). */
+int gvp_arm_factor_expectations(int64_t nfac, const double* means, const double* chols, int32_t nproj,
+                                const double* proj, const double* mom, const int32_t* cnt, const double* grid,
+                                const int64_t* shape, const double* origin, double cell, const double* dh,
+                                const double* base, int32_t nspheres, const int32_t* sphere_link,
+                                const double* sphere_geom, double radius_eps, double sigma_obs, double* e0,
+                                double* e1, double* e2, int64_t* oob);
+
 /* ------------------------------------------------ batched device kernels (tests) */
 /* All pointers device memory, plan-minor layout with nplans plans, async on
  * `stream` (a cudaStream_t; NULL = legacy default stream). */
