@@ -104,6 +104,10 @@ int gvp_gbp_mean_solve(const double* diag, const double* off, const double* info
  * gvplan.blocktri.logdet_block_tridiag (blocktri.py:151-174). */
 int gvp_logdet_block_tridiag(const double* diag, const double* off, int64_t nblocks, int32_t n,
                              double* out, int64_t* where);
+/* forward_schur_chols (blocktri.py:151-165): Cholesky factors (K, n, n, lower)
+ * of the forward Schur pivots; GVP_ERR_NOT_SPD with *where = pivot block. */
+int gvp_forward_schur_chols(const double* diag, const double* off, int64_t nblocks, int32_t n, double* chols,
+                            int64_t* where);
 
 /* One closed-form KL-proximal step. Replaces gvplan.optimizer.proximal_update
  * (optimizer.py:129-161). cur (mean, diag, off), prior (kdiag, koff, info),

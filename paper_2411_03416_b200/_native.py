@@ -89,6 +89,7 @@ _SIGS = {
     "gvp_engine_trace_probes": (C.c_int, [C.c_void_p, C.c_int32]),
     "gvp_engine_set_map_bank": (C.c_int, [C.c_void_p, C.c_int32, _dp, _i32p]),
     "gvp_engine_raster_map_bank": (C.c_int, [C.c_void_p, C.c_int32, _i32p, _i32p, _dp, _i32p]),
+    "gvp_forward_schur_chols": (C.c_int, [_dp, _dp, C.c_int64, C.c_int32, _dp, _i64p]),
     "gvp_rasterize": (C.c_int, [C.c_int32, _i64p, _dp, C.c_double, C.c_int32, _i32p, _dp, _dp]),
     "gvp_arm_factor_expectations": (C.c_int, [C.c_int64, _dp, _dp, C.c_int32, _dp, _dp, _i32p, _dp, _i64p, _dp,
                                               C.c_double, _dp, _dp, C.c_int32, _i32p, _dp, C.c_double,

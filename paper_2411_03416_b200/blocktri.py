@@ -221,6 +221,21 @@ def logdet_block_tridiag(mat: BlockTridiagonalMatrix) -> float:
     return float(out[0])
 
 
+def forward_schur_chols(mat: BlockTridiagonalMatrix) -> list:
+    """Cholesky factors of the forward Schur pivots S_0 = D_0, S_i = D_i -
+    U_{i-1}' S_{i-1}^-1 U_{i-1}, on the GPU (blocktri.py:151-165)."""
+    lib = N.load()
+    d, o = _stacks(mat)
+    n, K = mat.block_size, mat.nblocks
+    out = np.zeros((K, n, n))
+    where = np.zeros(1, dtype=np.int64)
+    code = N.check(lib.gvp_forward_schur_chols(N.ptr(d), N.ptr(o), K, n, N.ptr(out), N.ptr(where)),
+                   "forward_schur_chols")
+    if code == N.GVP_ERR_NOT_SPD:
+        raise NotPositiveDefiniteError(f"pivot block {int(where[0])} is not positive definite")
+    return list(out)
+
+
 def is_spd_block_tridiag(mat: BlockTridiagonalMatrix) -> bool:
     try:
         logdet_block_tridiag(mat)

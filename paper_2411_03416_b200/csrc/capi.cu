@@ -345,13 +345,40 @@ extern "C" int gvp_logdet_block_tridiag(const double* diag, const double* off, i
   double* d_out;
   GVP_TRY(C.arena.get(14, 1, &d_out));
   GVP_TRY(launch_logdet_fwd(1, K, n, pview(b.diag, n * n, 1), pview(b.off, n * n, 1), d_out, b.st,
-                            b.st + 1, b.scr, C.stream));
+                            b.st + 1, nullptr, C.stream));
   const int st = fetch_status(C, b.st, where);
   if (st != GVP_OK) {
     set_error("pivot block " + std::to_string(*where) + " is not positive definite");
     return st;
   }
   GVP_TRY(d2h(out, d_out, 1, C.stream));
+  GVP_CUDA(cudaStreamSynchronize(C.stream));
+  return GVP_OK;
+}
+
+// forward_schur_chols (blocktri.py:151-165): Cholesky factors of the forward
+// Schur pivots S_0 = D_0, S_i = D_i - W'W, W = L_{i-1}^-1 U_{i-1}; chols (K, n, n)
+extern "C" int gvp_forward_schur_chols(const double* diag, const double* off, int64_t nblocks, int32_t n,
+                                       double* chols, int64_t* where) {
+  Context& C = ctx();
+  std::lock_guard<std::mutex> lock(C.mu);
+  GVP_TRY(C.init());
+  GVP_TRY(check_n(n));
+  if (nblocks < 1 || !chols) return set_error("need at least one block"), GVP_ERR_ARG;
+  const int64_t K = nblocks;
+  ChainBufs b;
+  GVP_TRY(upload_bt(C, diag, off, K, n, b));
+  double *d_out, *d_ch;
+  GVP_TRY(C.arena.get(14, 1, &d_out));
+  GVP_TRY(C.arena.get(15, (size_t)K * n * n, &d_ch));
+  GVP_TRY(launch_logdet_fwd(1, K, n, pview(b.diag, n * n, 1), pview(b.off, n * n, 1), d_out, b.st,
+                            b.st + 1, d_ch, C.stream));
+  const int st = fetch_status(C, b.st, where);
+  if (st != GVP_OK) {
+    set_error("pivot block " + std::to_string(*where) + " is not positive definite");
+    return st;
+  }
+  GVP_TRY(d2h(chols, d_ch, (size_t)K * n * n, C.stream));
   GVP_CUDA(cudaStreamSynchronize(C.stream));
   return GVP_OK;
 }

@@ -229,7 +229,7 @@ mean_solve_kernel(int nplans, int64_t K, View D, View U, View eta, MutView out,
 template <int N>
 __global__ void __launch_bounds__(64)
 logdet_fwd_kernel(int nplans, int64_t K, View D, View U, double* __restrict__ out,
-                  int* __restrict__ status, int* __restrict__ where) {
+                  int* __restrict__ status, int* __restrict__ where, double* __restrict__ chols) {
   const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= nplans) return;
   double Lprev[N][N], ld = 0.0;
@@ -256,7 +256,10 @@ logdet_fwd_kernel(int nplans, int64_t K, View D, View U, double* __restrict__ ou
 #pragma unroll
     for (int r = 0; r < N; ++r)
 #pragma unroll
-      for (int c = 0; c < N; ++c) Lprev[r][c] = L[r][c];
+      for (int c = 0; c < N; ++c) {
+        Lprev[r][c] = L[r][c];
+        if (chols) chols[((b * K + i) * N + r) * N + c] = c <= r ? L[r][c] : 0.0;  // forward_schur_chols
+      }
   }
   out[b] = ld;
   status[b] = GVP_OK;
@@ -823,12 +826,11 @@ int launch_mean_solve(int nplans, int64_t K, int n, const View& D, const View& U
 }
 
 int launch_logdet_fwd(int nplans, int64_t K, int n, const View& D, const View& U, double* out,
-                      int* status, int* where, double* scratch, cudaStream_t s) {
-  (void)scratch;
+                      int* status, int* where, double* chols, cudaStream_t s) {
   if (nplans == 0 || K == 0) return GVP_OK;
   GVP_DISPATCH_N(n, {
     logdet_fwd_kernel<NN><<<nblk(nplans, kChainTpb), kChainTpb, 0, s>>>(nplans, K, D, U, out,
-                                                                         status, where);
+                                                                         status, where, chols);
   });
   GVP_CUDA(cudaGetLastError());
   return GVP_OK;

@@ -112,8 +112,9 @@ int launch_marginals(int nplans, int64_t K, int n, const View& diag, const View&
 int launch_mean_solve(int nplans, int64_t K, int n, const View& diag, const View& off,
                       const View& eta, const MutView& out, int* status, int* where,
                       double* scratch, cudaStream_t s);
+// chols (nullable): the forward Schur pivots' Cholesky factors, (nplans, K, n, n) lower
 int launch_logdet_fwd(int nplans, int64_t K, int n, const View& diag, const View& off,
-                      double* out, int* status, int* where, double* scratch, cudaStream_t s);
+                      double* out, int* status, int* where, double* chols, cudaStream_t s);
 
 struct StepProblem {
   View mean, diag, off;      // current iterate
