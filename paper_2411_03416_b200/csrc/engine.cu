@@ -95,7 +95,19 @@ __global__ void control_kernel(int B, int64_t F, int n64dim, const double* __res
   }
   const int it = ps.iters[b] + 1;
   double coll = 0.0;  // sum(f.e_psi), ascending factor order (optimizer.py:274)
-  for (int64_t f = 0; f < F; ++f) coll += epsi[f * B + b];
+  {
+    // the loads of a chunk are all in flight before its (sequential, in order) adds
+    constexpr int C = 32;
+    int64_t f = 0;
+    for (; f + C <= F; f += C) {
+      double buf[C];
+#pragma unroll
+      for (int k = 0; k < C; ++k) buf[k] = epsi[(f + k) * B + b];
+#pragma unroll
+      for (int k = 0; k < C; ++k) coll += buf[k];
+    }
+    for (; f < F; ++f) coll += epsi[f * B + b];
+  }
   const double temp = ps.temp[b];
   const double dim = (double)n64dim;
   const double entropy = 0.5 * (dim * (kLog2Pi + 1.0) - ps.logdet[b]);  // optimizer.py:234-235
