@@ -582,7 +582,7 @@ extern "C" int64_t gvp_engine_launches(gvp_engine* e) { return e->launches; }
 // Map bank: nmaps signed-distance maps with the engine's grid
 // geometry; plan b reads map plan_map[b]. From host grids (nmaps x (ny, nx) or
 // (nz, ny, nx), row-major) or rasterised on the device from primitive lists.
-static int install_bank(gvp_engine* e, int nmaps, const double* raw_dev, const int32_t* plan_map) {
+static int install_bank(gvp_engine* e, int nmaps, const double* raw_dev, const int32_t* plan_map, double lip) {
   for (int b = 0; b < e->nreal; ++b)
     if (plan_map[b] < 0 || plan_map[b] >= nmaps) {
       set_error("plan_map entry outside [0, nmaps)");
@@ -602,6 +602,7 @@ static int install_bank(gvp_engine* e, int nmaps, const double* raw_dev, const i
   f.corners = bank;
   f.plan_map = pm;
   f.map_stride = stride;
+  f.lip = lip;
   e->field.dev = f;
   if (e->graph) {  // the captured factor launch holds the old field
     cudaGraphExecDestroy(e->graph);
@@ -618,7 +619,21 @@ extern "C" int gvp_engine_set_map_bank(gvp_engine* e, int32_t nmaps, const doubl
   double* raw = nullptr;
   GVP_CUDA(cudaMalloc(&raw, sizeof(double) * cells * nmaps));
   cudaError_t ce = cudaMemcpyAsync(raw, grids, sizeof(double) * cells * nmaps, cudaMemcpyHostToDevice, e->stream);
-  int r = ce == cudaSuccess ? install_bank(e, nmaps, raw, plan_map) : GVP_ERR_CUDA;
+  // Lipschitz bound over every map of the bank (the factor kernel's clear-cloud shortcut)
+  double gx = 0.0, gy = 0.0, gz = 0.0;
+  bool finite = true;
+  for (int m = 0; m < nmaps; ++m)
+    for (int64_t iz = 0; iz < f.nz; ++iz)
+      for (int64_t iy = 0; iy < f.ny; ++iy)
+        for (int64_t ix = 0; ix < f.nx; ++ix) {
+          const double* g = grids + (size_t)m * cells + (iz * f.ny + iy) * f.nx + ix;
+          finite = finite && std::isfinite(g[0]);
+          if (ix + 1 < f.nx) gx = std::max(gx, std::fabs(g[1] - g[0]));
+          if (iy + 1 < f.ny) gy = std::max(gy, std::fabs(g[f.nx] - g[0]));
+          if (f.ndim == 3 && iz + 1 < f.nz) gz = std::max(gz, std::fabs(g[f.nx * f.ny] - g[0]));
+        }
+  const double lip = finite ? std::sqrt(gx * gx + gy * gy + gz * gz) / f.cell * (1.0 + 1e-12) : INFINITY;
+  int r = ce == cudaSuccess ? install_bank(e, nmaps, raw, plan_map, lip) : GVP_ERR_CUDA;
   if (ce != cudaSuccess) set_error(cudaGetErrorString(ce));
   cudaStreamSynchronize(e->stream);
   cudaFree(raw);
@@ -649,7 +664,7 @@ extern "C" int gvp_engine_raster_map_bank(gvp_engine* e, int32_t nmaps, const in
     GVP_CUDA(cudaMemcpyAsync(par, params, sizeof(double) * 2 * dim * nprim, cudaMemcpyHostToDevice, e->stream));
   }
   int r = rasterize_maps(dim, counts, origin, f.cell, nmaps, off, kd, par, raw, e->stream);
-  if (!r) r = install_bank(e, nmaps, raw, plan_map);
+  if (!r) r = install_bank(e, nmaps, raw, plan_map, INFINITY);  // no host copy: shortcut off
   cudaStreamSynchronize(e->stream);
   cudaFree(raw);
   cudaFree(par);

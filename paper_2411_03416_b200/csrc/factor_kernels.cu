@@ -54,6 +54,20 @@ int Field::build(const double* grid, int ndim, const int64_t* shape, const doubl
   f.oz = ndim == 3 ? origin[2] : 0.0;
   f.cell = cell;
   f.inv_cell = 1.0 / cell;
+  {  // Lipschitz bound of the multilinear interpolant: per axis max |adjacent difference| / cell
+    double gx = 0.0, gy = 0.0, gz = 0.0;
+    bool finite = true;
+    for (int64_t iz = 0; iz < f.nz; ++iz)
+      for (int64_t iy = 0; iy < f.ny; ++iy)
+        for (int64_t ix = 0; ix < f.nx; ++ix) {
+          const double* g = grid + (iz * f.ny + iy) * f.nx + ix;
+          finite = finite && std::isfinite(g[0]);
+          if (ix + 1 < f.nx) gx = std::max(gx, std::fabs(g[1] - g[0]));
+          if (iy + 1 < f.ny) gy = std::max(gy, std::fabs(g[f.nx] - g[0]));
+          if (ndim == 3 && iz + 1 < f.nz) gz = std::max(gz, std::fabs(g[f.nx * f.ny] - g[0]));
+        }
+    f.lip = finite ? std::sqrt(gx * gx + gy * gy + gz * gz) / cell * (1.0 + 1e-12) : INFINITY;
+  }
   std::vector<double> packed;
   if (ndim == 2) {
     // corner-packed cells: (iy, ix) -> {g[iy][ix], g[iy][ix+1], g[iy+1][ix], g[iy+1][ix+1]}
@@ -127,8 +141,15 @@ int Rule::build(const double* points, const double* weights, int64_t npts, int n
   const int M = 1 + n + T;
   std::vector<double> proj((size_t)(nproj * P)), mom((size_t)(nproj * M), 0.0);
   std::vector<int> cnt((size_t)nproj, 0);
-  for (int64_t j = 0; j < nproj; ++j)
-    for (int k = 0; k < P; ++k) proj[j * P + k] = points[order[j] * n + k];
+  double prad = 0.0;
+  for (int64_t j = 0; j < nproj; ++j) {
+    double r2 = 0.0;
+    for (int k = 0; k < P; ++k) {
+      proj[j * P + k] = points[order[j] * n + k];
+      r2 += proj[j * P + k] * proj[j * P + k];
+    }
+    prad = std::max(prad, std::sqrt(r2));
+  }
   for (int64_t l = 0; l < npts; ++l) {  // ascending point order within each group
     const int64_t j = proj_of[l];
     const double w = weights[l];
@@ -164,6 +185,7 @@ int Rule::build(const double* points, const double* weights, int64_t npts, int n
   dev.P = P;
   dev.npts = npts;
   dev.nproj = nproj;
+  dev.proj_radius = prad * (1.0 + 1e-12);
   dev.points = p;
   dev.weights = p + npts * n;
   dev.proj = p + npts * n + npts;
@@ -417,6 +439,38 @@ factor_grads_kernel(int nplans, int64_t nfac, View mean, View covs, RuleDev R, F
     // rule tables live in the kernel's parameter space: every projection
     // coordinate and moment is a constant-bank operand of its DFMA (no loads),
     // the loop is fully unrolled and the accumulation is branch-free
+    // Provably clear: every sigma position lies within Rad = |L[:P,:P]|_F * max_j |xi_j[:P]| of
+    // mu[:P] and the interpolated field is F.lip-Lipschitz, so if d(mu) - lip * Rad exceeds
+    // radius_eps (margin 1e-9 >> rounding) no point can hit; with the cloud inside the grid no
+    // point is out of bounds either. One gather instead of NP — the same zeros as below.
+    if (F.lip < INFINITY) {
+      double fr = 0.0;
+#pragma unroll
+      for (int r = 0; r < P; ++r)
+#pragma unroll
+        for (int k = 0; k <= r; ++k) fr += L[r][k] * L[r][k];
+      const double Rad = sqrt(fr) * R.proj_radius;
+      const double slack = 1e-9 * F.cell;
+      bool inside = (mu[0] - Rad > F.ox + slack) && (mu[0] + Rad < F.ox + (double)(F.nx - 1) * F.cell - slack) &&
+                    (mu[1] - Rad > F.oy + slack) && (mu[1] + Rad < F.oy + (double)(F.ny - 1) * F.cell - slack);
+      if (P == 3)
+        inside = inside && (mu[P - 1] - Rad > F.oz + slack) &&
+                 (mu[P - 1] + Rad < F.oz + (double)(F.nz - 1) * F.cell - slack);
+      if (inside) {
+        bool oc;
+        const double dc = (P == 2) ? interp2<false>(F, mu[0], mu[1], oc)
+                                   : interp3<false>(F, mu[0], mu[1], mu[P - 1], oc);
+        if (dc - F.lip * Rad - radius_eps > 1e-9) {
+#pragma unroll
+          for (int r = 0; r < N; ++r) out.g_mu.p[knot * out.g_mu.sk + b * out.g_mu.sp + r * out.g_mu.se] = 0.0;
+#pragma unroll
+          for (int k = 0; k < T; ++k)
+            out.g_diag.p[knot * out.g_diag.sk + b * out.g_diag.sp + k * out.g_diag.se] = 0.0;
+          out.e_psi(b, f, 0) = 0.0;
+          return;
+        }
+      }
+    }
     double psi[NP];
     bool any_hit = false;
 #pragma unroll

@@ -35,6 +35,11 @@ struct FieldDev {
   // map bank: plan b reads map plan_map[b] at corners + plan_map[b] * map_stride
   const int* plan_map;    // device, nullptr = one map for every plan
   int64_t map_stride;     // doubles per packed map
+  // Lipschitz bound of the interpolated field (max |grid difference| / cell per
+  // axis, combined in 2-norm; INFINITY = unknown): the fused factor kernel
+  // skips the per-point gathers of a factor whose whole sigma-point cloud is
+  // provably clear of every obstacle
+  double lip;
 };
 // corner-pack raw grids on the device (nmaps maps of the geometry in f) into dst
 int pack_field_maps(const FieldDev& f, int nmaps, const double* raw_dev, double* dst_dev, cudaStream_t s);
@@ -71,6 +76,7 @@ struct RuleDev {
   const double* mom;      // (nproj, 1 + n + n(n+1)/2)
   const int* cnt;         // (nproj)
   const void* host;       // the owning host Rule (projection tables for by-value launch)
+  double proj_radius;     // max_j |proj_j| (2-norm): the sigma cloud lies within |L[:P,:P]|_F * this
 };
 
 struct Rule {
