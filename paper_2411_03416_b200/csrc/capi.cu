@@ -2,6 +2,8 @@
 // See include/gvp_b200.h for the contract of every function.
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include <algorithm>
 #include <climits>
 #include <cmath>
@@ -278,6 +280,10 @@ int fetch_status(Context& C, const int* d_st, int64_t* where) {
 }
 }  // namespace
 
+// cyclic reduction for short chains: its rounding grows faster with K than the
+// sequential sweep's on ill-conditioned (anchored) chains (cr_kernels.cu)
+constexpr int64_t kCrMaxKnots = 128;
+
 extern "C" int gvp_gbp_marginals(const double* diag, const double* off, int64_t nblocks,
                                  int32_t n, double* covs, double* crosses, int64_t* where) {
   Context& C = ctx();
@@ -291,10 +297,27 @@ extern "C" int gvp_gbp_marginals(const double* diag, const double* off, int64_t 
   double *d_cov, *d_cr;
   GVP_TRY(C.arena.get(14, K * n * n, &d_cov));
   GVP_TRY(C.arena.get(15, std::max<int64_t>(K - 1, 1) * n * n, &d_cr));
-  GVP_TRY(launch_marginals(1, K, n, pview(b.diag, n * n, 1), pview(b.off, n * n, 1),
-                           pmview(d_cov, n * n, 1), pmview(d_cr, n * n, 1), nullptr, b.st,
-                           b.st + 1, b.scr, nullptr, C.stream));
-  const int st = fetch_status(C, b.st, where);
+  // log-depth cyclic reduction (one plan: the sequential sweep would be pure latency);
+  // on a non-SPD pivot the sequential sweep names the reference's knot
+  static const int mode = [] {  // GVP_MARGINALS=seq|cr overrides the choice (A/B measurements)
+    const char* ev = std::getenv("GVP_MARGINALS");
+    return !ev ? 0 : (ev[0] == 's' ? 1 : 2);
+  }();
+  const bool use_cr = mode == 2 || (mode == 0 && K <= kCrMaxKnots);
+  int st = GVP_ERR_NOT_SPD;
+  if (use_cr) {
+    double* d_ws;
+    GVP_TRY(C.arena.get(16, (size_t)cr_workspace_doubles(1, K, n), &d_ws));
+    GVP_TRY(launch_cr_marginals(1, K, n, pview(b.diag, n * n, 1), pview(b.off, n * n, 1), pmview(d_cov, n * n, 1),
+                                pmview(d_cr, n * n, 1), d_ws, b.st, b.st + 1, C.stream));
+    st = fetch_status(C, b.st, where);
+  }
+  if (st != GVP_OK) {
+    GVP_TRY(launch_marginals(1, K, n, pview(b.diag, n * n, 1), pview(b.off, n * n, 1),
+                             pmview(d_cov, n * n, 1), pmview(d_cr, n * n, 1), nullptr, b.st,
+                             b.st + 1, b.scr, nullptr, C.stream));
+    st = fetch_status(C, b.st, where);
+  }
   if (st != GVP_OK) {
     set_error("belief precision at knot " + std::to_string(*where) + " is not positive definite");
     return st;

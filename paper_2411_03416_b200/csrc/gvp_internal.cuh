@@ -112,6 +112,10 @@ int launch_factor_grads(int nplans, int64_t nknots, int n, const View& mean, con
                         cudaStream_t s);
 
 // chain kernels (chain_kernels.cu)
+// GBP marginals by cyclic reduction (cr_kernels.cu): one CTA per plan, log-depth
+int launch_cr_marginals(int nplans, int64_t K, int n, const View& D, const View& U, const MutView& cov,
+                        const MutView& cross, double* ws, int* status, int* where, cudaStream_t s);
+int64_t cr_workspace_doubles(int nplans, int64_t K, int n);
 int launch_marginals(int nplans, int64_t K, int n, const View& diag, const View& off,
                      const MutView& covs, const MutView& crosses, double* logdet, int* status,
                      int* where, double* scratch, const int* active, cudaStream_t s);
