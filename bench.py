@@ -434,7 +434,8 @@ def main():
         ach = bis_flops / (bis_ms / 1e3) / 1e12
         # the engine runs the split probe kernel while the grid is below 2 CTAs per SM
         lanes = eng.lanes()
-        probe_kernel = "probe_split_kernel" if (B + 1) // 2 * 2 * lanes // 32 < 2 * 148 else "probe_fused_kernel"
+        P_cols = 32 // lanes  # launch_probe: split while ceil(B / P) < 2 x 148 CTAs
+        probe_kernel = "probe_split_kernel" if -(-B // P_cols) < 2 * 148 else "probe_fused_kernel"
         traffic = None
         tpath = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "ncu_traffic.json")
         if os.path.exists(tpath):
@@ -473,6 +474,8 @@ def main():
                          "traffic_unit": "bytes/launch (ncu dram read+write)",
                          "flops_per_probe_knot": fl["total"], "probes_per_plan_iter": probes / max(1, B * steps_prof),
                          "lanes_per_plan": lanes,
+                         "plans_per_cta": (min(P_cols, max(2, -(-(-(-B // 296)) // 2) * 2))
+                                           if probe_kernel == "probe_split_kernel" else P_cols),
                          "peak_source": "148 SMs x 64 DFMA/clk (ncu sm__sass_thread_inst_executed_op_dfma"
                                         "_pred_on.sum.peak_sustained) x 2 x sm_max_mhz (MEASURED_PEAKS.json)",
                          "factor_grads": {"bound": "hbm", "achieved": fac_ach, "peak": hbm, "unit": "GB/s",

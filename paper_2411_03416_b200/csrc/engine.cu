@@ -168,6 +168,7 @@ struct gvp_engine {
   int n = 0, T = 0;
   bool shared_prior = false;
   int lanes = 1;
+  bool fill = false;  // auto lanes: the probe kernel fills every resident CTA slot
   cudaStream_t stream = nullptr;
   Field field;
   Rule rule;
@@ -223,6 +224,7 @@ struct gvp_engine {
     q.n = n;
     q.Bp = B;
     q.lanes = lanes;
+    q.fill = fill;
     q.ld = diag; q.lo = off; q.kd = kdiag; q.ko = koff; q.gd = gdiag;
     q.g = gmu; q.eta = info; q.v = v; q.mu = mean; q.pmean = pmean;
     q.kshared = shared_prior;
@@ -259,14 +261,19 @@ struct gvp_engine {
 
 static int pick_lanes(const gvp_plan_config* cfg, int B) {
   if (cfg->spec_lanes > 0) return cfg->spec_lanes;
-  // Speculative lanes only pay while the GPU would otherwise idle: take the
-  // fewest lanes that give ~6 probe warps per SM (the split probe kernel runs
-  // 4 warps per 32 lane slots). B200, C5 (4096 plans x 1001 knots): 2 lanes
-  // (split) 11.6 ms < 4 lanes (fused) 12.0 < 4 lanes (split) 14.0 per
-  // bisection; a single plan takes 16 lanes.
-  int L = 1;
-  while (L < 16 && (int64_t)B * L * 4 / 32 < 148 * 6) L *= 2;
-  return L;
+  // A split-probe CTA's bisection time is its per-knot step latency times its
+  // rounds, nearly independent of how many CTAs share its SM (B200, C5: 3552
+  // and 4096 plans over 222 / 256 CTAs both 11.5 ms). So spread the plans over
+  // all 2 x 148 resident CTAs (launch_probe's fill: ppc = ceil(B / 296), even)
+  // and take the layout with the fewest plan columns P = 32 / L >= ppc: each
+  // plan gets 32 / ppc speculative lanes, which cut its rounds. C5: 14 plans
+  // per CTA, 11.1 ms vs 12.0 ms at 16 per CTA; 3000 plans: 11.9 -> see DESIGN.
+  const int64_t slots = 2 * 148;
+  int64_t need = (B + slots - 1) / slots;
+  need = std::max<int64_t>(2, (need + 1) / 2 * 2);
+  int P = 2;
+  while (P < need && P < 32) P *= 2;
+  return 32 / P;
 }
 
 extern "C" int gvp_engine_create(gvp_engine** out, int32_t nplans, int64_t nknots, int32_t n,
@@ -307,6 +314,7 @@ extern "C" int gvp_engine_create(gvp_engine** out, int32_t nplans, int64_t nknot
   e->n = n;
   e->T = n * (n + 1) / 2;
   e->lanes = lanes;
+  e->fill = cfg->spec_lanes <= 0;
   e->shared_prior = shared_prior != 0;
   e->cfg = *cfg;
   e->radius_eps = radius_eps;

@@ -167,6 +167,7 @@ struct V2Launch {
   int n;
   int64_t Bp;
   int lanes;
+  bool fill;  // probes: spread the plans over every resident CTA slot (fewer plans per CTA, more lanes each)
   const double *ld, *lo, *kd, *ko, *gd, *g, *eta, *v, *mu, *pmean;
   bool kshared;
   double *o_mu, *o_ld, *o_lo, *o_cov, *o_cr, *o_v;

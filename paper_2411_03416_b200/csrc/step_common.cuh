@@ -140,7 +140,8 @@ GVP_DEV void search_init(const A& a, PlanSt* pst, int P, int64_t b0, bool commit
 struct Pick {
   int p;        // plan column this slot serves (0 for idle slots)
   int my_rank;  // rank among active plans of plan `tid` (tid < P), else -1
-  int kl;       // slots per active plan this round
+  int kl;       // slots of the plan this slot serves (0: every plan is done)
+  int dbase, dkl;  // first slot / slot count of plan `tid` (my_rank >= 0)
   int phase;    // phase of the served plan (4: idle slot)
   bool on, write;
   double beta;
@@ -154,12 +155,16 @@ GVP_DEV Pick search_pick(const A& a, const PlanSt* pst, int P, int LP, int lcol,
   k.beta = 0.0;
   int nact = 0;
   for (int j = 0; j < P; ++j) nact += pst[j].phase < 4 ? 1 : 0;
-  k.kl = nact ? LP / nact : 0;
+  k.kl = 0;
   k.my_rank = -1;
+  k.dbase = k.dkl = 0;
   k.p = 0;
   k.phase = 4;
   if (nact == 0) return k;
-  const int my_idx = lcol / k.kl, q = lcol % k.kl;
+  // plan rank r owns slots [r LP / nact, (r + 1) LP / nact): all LP slots in use
+  auto first = [&](int r) { return r * LP / nact; };
+  const int my_idx = ((lcol + 1) * nact - 1) / LP, q = lcol - first(my_idx);
+  k.kl = first(my_idx + 1) - first(my_idx);
   int pj = -1;
   for (int j = 0, c = 0; j < P; ++j)
     if (pst[j].phase < 4) {
@@ -167,6 +172,10 @@ GVP_DEV Pick search_pick(const A& a, const PlanSt* pst, int P, int LP, int lcol,
       if (j == tid) k.my_rank = c;
       ++c;
     }
+  if (k.my_rank >= 0) {
+    k.dbase = first(k.my_rank);
+    k.dkl = first(k.my_rank + 1) - k.dbase;
+  }
   if (pj < 0) return k;
   k.p = pj;
   const PlanSt& S = pst[pj];

@@ -46,12 +46,21 @@ namespace v4 {
 using v3::PlanSt;
 using v3::Pick;
 using v3::T_;
-#ifndef GVP_PROBE_MINB
-#define GVP_PROBE_MINB 2
+// resident split-probe CTAs per SM the register budget targets. 3 at n = 4
+// (168 registers, spilling) made every step ~12% slower and lost overall
+// (C5: 13.7 ms vs 11.6 ms per bisection), so 2.
+template <int N>
+constexpr int probe_minb() {
+#ifdef GVP_PROBE_MINB
+  return GVP_PROBE_MINB;
+#else
+  return 2;
 #endif
+}
 
 // Compile-time shared-memory layout (32 lane slots = P plans x L lanes, four
 // warps over the same 32 slots, see the kernel).
+constexpr int kMaxStagesTail = 8;  // mbarriers
 template <int N, int L, bool KS, bool SPLIT>
 struct Lay {
   static constexpr int T = T_<N>, N2 = N * N;
@@ -66,8 +75,13 @@ struct Lay {
                        STAGE = OFF_PRIOR + v3::cx_round(KR * Kb, 16);
   // producer -> consumer ring (2 steps x 2 chains): Li T | W N2 | v N, per slot
   static constexpr int ENT = T + N2 + N, E_LI = 0, E_W = T, E_V = T + N2;
+  // split: as many stages (4..8) as fit probe_minb CTAs per SM (228 KB, 1 KB
+  // reserved per CTA) next to the producer ring and the fixed tail
+  static constexpr int FIXED = (SPLIT ? 2 * 2 * ENT * 32 : 0) + (5 + 10 + 5) * 32 + kMaxStagesTail;
+  static constexpr int FIT = ((233472 / probe_minb<N>() - 1024) / 8 - FIXED) / STAGE;
   // prefetch distance: at step s the consumers still read knot s-1's slot
-  static constexpr int NS = v3::ring_stages(STAGE), AH = SPLIT ? NS - 2 : NS - 1;
+  static constexpr int NS = SPLIT ? (FIT < 4 ? 4 : FIT > 8 ? 8 : FIT) : v3::ring_stages(STAGE),
+                       AH = SPLIT ? NS - 2 : NS - 1;
   static constexpr int RING = NS * STAGE;
   static constexpr int XCH = RING + (SPLIT ? 2 * 2 * ENT * 32 : 0);  // 4 roles x 32 doubles + 2 x 32 ints
   static constexpr int PST = XCH + 5 * 32;
@@ -88,6 +102,7 @@ struct Args {
   double* probe_log;
   int max_probes;
   const int* active;
+  int ppc;  // plans per CTA (<= the layout's P = 32 / L)
 };
 
 template <int N>
@@ -105,7 +120,7 @@ GVP_DEV double symv(const double (&A)[T_<N>], int r, int c) {
 // Splitting the chains (instead of more speculative lanes) doubles the warps
 // that hide the fp64 dependency latency without adding probes.
 template <int N, int L, bool KS>
-__global__ void __launch_bounds__(128, GVP_PROBE_MINB) probe_split_kernel(const __grid_constant__ Args a) {
+__global__ void __launch_bounds__(128, probe_minb<N>()) probe_split_kernel(const __grid_constant__ Args a) {
   using LO = Lay<N, L, KS, true>;
   constexpr int T = LO::T, N2 = LO::N2;
   extern __shared__ __align__(1024) double smem[];
@@ -116,7 +131,7 @@ __global__ void __launch_bounds__(128, GVP_PROBE_MINB) probe_split_kernel(const 
   const bool tangent = (role & 1) != 0;
   const int lcol = tid & 31;            // lane slot
   constexpr int P = LO::P, Pb = LO::Pb, Kb = LO::Kb, LP = P * L;
-  const int64_t b0 = (int64_t)blockIdx.x * P;
+  const int64_t b0 = (int64_t)blockIdx.x * a.ppc;
   const int64_t K = a.K;
   double* ring = smem + LO::RING;
   double* xch = smem + LO::XCH;
@@ -132,7 +147,7 @@ __global__ void __launch_bounds__(128, GVP_PROBE_MINB) probe_split_kernel(const 
     for (int s = 0; s < LO::NS; ++s) v3::mbar_init(&bars[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
-  v3::search_init(a, pst, P, b0, false, tid);
+  v3::search_init(a, pst, a.ppc, b0, false, tid);
   __syncthreads();
 
   auto slot = [&](int64_t s) { return smem + (s % LO::NS) * LO::STAGE; };
@@ -159,9 +174,9 @@ __global__ void __launch_bounds__(128, GVP_PROBE_MINB) probe_split_kernel(const 
 
   int64_t sbase = 0;
   for (;;) {
-    const Pick pk = v3::search_pick(a, pst, P, LP, lcol, tid, false);
+    const Pick pk = v3::search_pick(a, pst, a.ppc, LP, lcol, tid, false);
     if (pk.kl == 0) break;  // uniform: every thread read the same shared state
-    const int p = pk.p, kl = pk.kl, my_rank = pk.my_rank;
+    const int p = pk.p, my_rank = pk.my_rank;
     const int kcol = KS ? 0 : p;
     const double temp = pst[p].temp, ldc = pst[p].ldc;
     const bool lane_on = pk.on;
@@ -388,7 +403,7 @@ __global__ void __launch_bounds__(128, GVP_PROBE_MINB) probe_split_kernel(const 
     }
     __syncthreads();
     if (my_rank >= 0)
-      v3::search_decide(a, pst, tid, my_rank * kl, kl, b0, false, r_beta, r_kl, r_res, r_fail, r_on);
+      v3::search_decide(a, pst, tid, pk.dbase, pk.dkl, b0, false, r_beta, r_kl, r_res, r_fail, r_on);
     __syncthreads();
   }
 }
@@ -407,7 +422,7 @@ __global__ void __launch_bounds__(64) probe_fused_kernel(const __grid_constant__
   const int role = tid >> 5;  // 0: Lambda' chain (log det, trace), 1: S chain (Mahalanobis)
   const int lcol = tid & 31;
   constexpr int P = LO::P, Pb = LO::Pb, Kb = LO::Kb, LP = P * L;
-  const int64_t b0 = (int64_t)blockIdx.x * P;
+  const int64_t b0 = (int64_t)blockIdx.x * a.ppc;
   const int64_t K = a.K;
   double* xch = smem + LO::XCH;
   PlanSt* pst = reinterpret_cast<PlanSt*>(smem + LO::PST);
@@ -421,7 +436,7 @@ __global__ void __launch_bounds__(64) probe_fused_kernel(const __grid_constant__
     for (int s = 0; s < LO::NS; ++s) v3::mbar_init(&bars[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
-  v3::search_init(a, pst, P, b0, false, tid);
+  v3::search_init(a, pst, a.ppc, b0, false, tid);
   __syncthreads();
 
   auto slot = [&](int64_t s) { return smem + (s % LO::NS) * LO::STAGE; };
@@ -442,9 +457,9 @@ __global__ void __launch_bounds__(64) probe_fused_kernel(const __grid_constant__
 
   int64_t sbase = 0;
   for (;;) {
-    const Pick pk = v3::search_pick(a, pst, P, LP, lcol, tid, false);
+    const Pick pk = v3::search_pick(a, pst, a.ppc, LP, lcol, tid, false);
     if (pk.kl == 0) break;
-    const int p = pk.p, kl = pk.kl, my_rank = pk.my_rank;
+    const int p = pk.p, my_rank = pk.my_rank;
     const int kcol = KS ? 0 : p;
     const double temp = pst[p].temp, ldc = pst[p].ldc;
     const bool lane_on = pk.on;
@@ -626,7 +641,7 @@ __global__ void __launch_bounds__(64) probe_fused_kernel(const __grid_constant__
     }
     __syncthreads();
     if (my_rank >= 0)
-      v3::search_decide(a, pst, tid, my_rank * kl, kl, b0, false, r_beta, r_kl, r_res, r_fail, r_on);
+      v3::search_decide(a, pst, tid, pk.dbase, pk.dkl, b0, false, r_beta, r_kl, r_res, r_fail, r_on);
     __syncthreads();
   }
 }
@@ -727,6 +742,7 @@ int launch_probe(const V2Launch& q, const int L, cudaStream_t s) {
   a.probe_log = q.probe_log;
   a.max_probes = q.max_probes;
   a.active = q.active;
+  a.ppc = P;
   const unsigned grid = (unsigned)((q.nplans + P - 1) / P);
   // split chains (4 warps) while the grid is far from filling the GPU, fused
   // chains (2 warps, fewer barriers) once every SM has several CTAs;
@@ -736,13 +752,32 @@ int launch_probe(const V2Launch& q, const int L, cudaStream_t s) {
     return !e ? 0 : (std::strcmp(e, "split") == 0 ? 1 : std::strcmp(e, "fused") == 0 ? 2 : 0);
   }();
   const bool split = forced ? forced == 1 : grid < 2u * 148u;
+  // q.fill (auto lanes): the split CTA's time is its step latency times its
+  // rounds, nearly independent of how many CTAs share the SM, so spread the
+  // plans over every resident CTA slot; each plan then gets 32 / ppc lanes
+  auto fill_ppc = [&](const void* fn, size_t bytes) {
+    if (!q.fill) return;
+    static int nsm = 0;
+    if (!nsm) {
+      int dev = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    }
+    int occ = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, 128, bytes) != cudaSuccess || occ < 1) occ = 1;
+    const int64_t slots = (int64_t)occ * std::max(nsm, 1);
+    // even: a TMA box must start on a 16-byte boundary of the plan-minor rows
+    const int64_t want = (q.nplans + slots - 1) / slots;
+    a.ppc = (int)std::min<int64_t>(P, std::max<int64_t>(2, (want + 1) / 2 * 2));
+  };
 #define GVP_V4_KS(NN, LL, KK)                                                                          \
   {                                                                                                    \
     if (split) {                                                                                       \
       using LOH = v4::Lay<NN, LL, KK, true>;                                                           \
       GVP_CUDA(cudaFuncSetAttribute(v4::probe_split_kernel<NN, LL, KK>,                                \
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)LOH::BYTES));    \
-      v4::probe_split_kernel<NN, LL, KK><<<grid, 128, LOH::BYTES, s>>>(a);                             \
+      fill_ppc((const void*)v4::probe_split_kernel<NN, LL, KK>, LOH::BYTES);                           \
+      v4::probe_split_kernel<NN, LL, KK><<<(unsigned)((q.nplans + a.ppc - 1) / a.ppc), 128, LOH::BYTES, s>>>(a); \
     } else {                                                                                           \
       using LOH = v4::Lay<NN, LL, KK, false>;                                                          \
       GVP_CUDA(cudaFuncSetAttribute(v4::probe_fused_kernel<NN, LL, KK>,                                \
