@@ -136,6 +136,15 @@ static int check_n(int n) {
   }
   return GVP_OK;
 }
+// the block-chain drop-ins also take wide blocks (wide_kernels.cu)
+constexpr int kWideMin = 9, kWideMax = 32;
+static int check_chain_n(int n) {
+  if (n < 1 || n > kWideMax) {
+    set_error("block size n must be in 1..32");
+    return GVP_ERR_UNSUPPORTED;
+  }
+  return GVP_OK;
+}
 
 }  // namespace gvp
 
@@ -289,9 +298,32 @@ extern "C" int gvp_gbp_marginals(const double* diag, const double* off, int64_t 
   Context& C = ctx();
   std::lock_guard<std::mutex> lock(C.mu);
   GVP_TRY(C.init());
-  GVP_TRY(check_n(n));
+  GVP_TRY(check_chain_n(n));
   if (nblocks < 1) return set_error("need at least one block"), GVP_ERR_ARG;
   const int64_t K = nblocks;
+  if (n >= kWideMin) {
+    double *d_d, *d_o, *d_cov, *d_cr, *d_scr;
+    int* d_st;
+    GVP_TRY(C.arena.get(10, K * n * n, &d_d));
+    GVP_TRY(C.arena.get(11, std::max<int64_t>(K - 1, 1) * n * n, &d_o));
+    GVP_TRY(C.arena.get(12, (size_t)wide_scratch_doubles(1, K, n), &d_scr));
+    GVP_TRY(C.arena.get(13, 4, &d_st));
+    GVP_TRY(C.arena.get(14, K * n * n, &d_cov));
+    GVP_TRY(C.arena.get(15, std::max<int64_t>(K - 1, 1) * n * n, &d_cr));
+    GVP_TRY(h2d(d_d, diag, K * n * n, C.stream));
+    GVP_TRY(h2d(d_o, off, (K - 1) * n * n, C.stream));
+    GVP_TRY(launch_wide_marginals(1, K, n, pview(d_d, n * n, 1), pview(d_o, n * n, 1), pmview(d_cov, n * n, 1),
+                                  pmview(d_cr, n * n, 1), nullptr, d_scr, d_st, d_st + 1, C.stream));
+    const int st = fetch_status(C, d_st, where);
+    if (st != GVP_OK) {
+      set_error("belief precision at knot " + std::to_string(*where) + " is not positive definite");
+      return st;
+    }
+    GVP_TRY(d2h(covs, d_cov, K * n * n, C.stream));
+    GVP_TRY(d2h(crosses, d_cr, (K - 1) * n * n, C.stream));
+    GVP_CUDA(cudaStreamSynchronize(C.stream));
+    return GVP_OK;
+  }
   ChainBufs b;
   GVP_TRY(upload_bt(C, diag, off, K, n, b));
   double *d_cov, *d_cr;
@@ -333,15 +365,28 @@ extern "C" int gvp_gbp_mean_solve(const double* diag, const double* off, const d
   Context& C = ctx();
   std::lock_guard<std::mutex> lock(C.mu);
   GVP_TRY(C.init());
-  GVP_TRY(check_n(n));
+  GVP_TRY(check_chain_n(n));
   if (nblocks < 1) return set_error("need at least one block"), GVP_ERR_ARG;
   const int64_t K = nblocks;
   ChainBufs b;
-  GVP_TRY(upload_bt(C, diag, off, K, n, b));
+  if (n >= kWideMin) {
+    GVP_TRY(C.arena.get(10, K * n * n, &b.diag));
+    GVP_TRY(C.arena.get(11, std::max<int64_t>(K - 1, 1) * n * n, &b.off));
+    GVP_TRY(C.arena.get(12, (size_t)wide_scratch_doubles(1, K, n), &b.scr));
+    GVP_TRY(C.arena.get(13, 4, &b.st));
+    GVP_TRY(h2d(b.diag, diag, K * n * n, C.stream));
+    GVP_TRY(h2d(b.off, off, (K - 1) * n * n, C.stream));
+  } else {
+    GVP_TRY(upload_bt(C, diag, off, K, n, b));
+  }
   double *d_eta, *d_out;
   GVP_TRY(C.arena.get(14, K * n, &d_eta));
   GVP_TRY(C.arena.get(15, K * n, &d_out));
   GVP_TRY(h2d(d_eta, info, K * n, C.stream));
+  if (n >= kWideMin)
+    GVP_TRY(launch_wide_mean_solve(1, K, n, pview(b.diag, n * n, 1), pview(b.off, n * n, 1), pview(d_eta, n, 1),
+                                   pmview(d_out, n, 1), b.scr, b.st, b.st + 1, C.stream));
+  else
   GVP_TRY(launch_mean_solve(1, K, n, pview(b.diag, n * n, 1), pview(b.off, n * n, 1),
                             pview(d_eta, n, 1), pmview(d_out, n, 1), b.st, b.st + 1, b.scr,
                             C.stream));
@@ -360,13 +405,17 @@ extern "C" int gvp_logdet_block_tridiag(const double* diag, const double* off, i
   Context& C = ctx();
   std::lock_guard<std::mutex> lock(C.mu);
   GVP_TRY(C.init());
-  GVP_TRY(check_n(n));
+  GVP_TRY(check_chain_n(n));
   if (nblocks < 1) return set_error("need at least one block"), GVP_ERR_ARG;
   const int64_t K = nblocks;
   ChainBufs b;
-  GVP_TRY(upload_bt(C, diag, off, K, n, b));
+  GVP_TRY(upload_bt(C, diag, off, K, n, b, 0));
   double* d_out;
   GVP_TRY(C.arena.get(14, 1, &d_out));
+  if (n >= kWideMin)
+    GVP_TRY(launch_wide_logdet(1, K, n, pview(b.diag, n * n, 1), pview(b.off, n * n, 1), d_out, nullptr, b.st,
+                               b.st + 1, C.stream));
+  else
   GVP_TRY(launch_logdet_fwd(1, K, n, pview(b.diag, n * n, 1), pview(b.off, n * n, 1), d_out, b.st,
                             b.st + 1, nullptr, C.stream));
   const int st = fetch_status(C, b.st, where);
@@ -386,14 +435,18 @@ extern "C" int gvp_forward_schur_chols(const double* diag, const double* off, in
   Context& C = ctx();
   std::lock_guard<std::mutex> lock(C.mu);
   GVP_TRY(C.init());
-  GVP_TRY(check_n(n));
+  GVP_TRY(check_chain_n(n));
   if (nblocks < 1 || !chols) return set_error("need at least one block"), GVP_ERR_ARG;
   const int64_t K = nblocks;
   ChainBufs b;
-  GVP_TRY(upload_bt(C, diag, off, K, n, b));
+  GVP_TRY(upload_bt(C, diag, off, K, n, b, 0));
   double *d_out, *d_ch;
   GVP_TRY(C.arena.get(14, 1, &d_out));
   GVP_TRY(C.arena.get(15, (size_t)K * n * n, &d_ch));
+  if (n >= kWideMin)
+    GVP_TRY(launch_wide_logdet(1, K, n, pview(b.diag, n * n, 1), pview(b.off, n * n, 1), d_out, d_ch, b.st,
+                               b.st + 1, C.stream));
+  else
   GVP_TRY(launch_logdet_fwd(1, K, n, pview(b.diag, n * n, 1), pview(b.off, n * n, 1), d_out, b.st,
                             b.st + 1, d_ch, C.stream));
   const int st = fetch_status(C, b.st, where);
@@ -456,6 +509,81 @@ int upload_step(Context& C, const double* mean, const double* diag, const double
 }
 }  // namespace
 
+namespace {
+// wide blocks (9 <= n <= 32): one CTA per plan, probe slots on warp pairs
+// (wide_kernels.cu). fixed: proximal_update at beta; else select_step_size.
+int wide_step_call(Context& C, const double* mean, const double* diag, const double* off, const double* kdiag,
+                   const double* koff, const double* info, const double* g_mu, const double* gdiag,
+                   const double* goff, int64_t K, int n, bool fixed, double beta_fixed, double temp,
+                   double kl_bound, double beta_min, double beta_max, double* beta, double* kl, double* out_mean,
+                   double* out_diag, double* out_off, double* covs, double* crosses, double* probe_log,
+                   int max_probes, int* nprobes, int64_t* where) {
+  const int64_t B2 = (int64_t)n * n;
+  cudaStream_t s = C.stream;
+  StepBufs b;
+  StepProblem pb;
+  GVP_TRY(upload_step(C, mean, diag, off, kdiag, koff, info, g_mu, gdiag, goff, K, n,
+                      probe_log ? max_probes : 0, b, pb));
+  double* wscr;
+  GVP_TRY(C.arena.get(60, (size_t)wide_scratch_doubles(1, K, n), &wscr));
+  // scal: 0 beta (in: previous / fixed, out: accepted), 1 kl, 2 ld_next, 4 temp, 5 ld_cur
+  const double init[6] = {fixed ? beta_fixed : NAN, 0.0, 0.0, 0.0, temp, 0.0};
+  GVP_TRY(h2d(b.scal, init, 6, s));
+  if (!fixed) {  // log det of the current precision (kl_joint's logdet_cur, forward Schur)
+    GVP_TRY(launch_wide_logdet(1, K, n, pb.diag, pb.off, b.scal + 5, nullptr, b.st, b.st + 1, s));
+    int64_t w0 = -1;
+    if (fetch_status(C, b.st, &w0) != GVP_OK) {
+      if (where) *where = w0;
+      set_error("pivot block " + std::to_string(w0) + " is not positive definite");
+      return GVP_ERR_NOT_SPD;
+    }
+  }
+  WideStep q{};
+  q.nplans = 1; q.K = K; q.n = n;
+  q.mean = pb.mean; q.diag = pb.diag; q.off = pb.off; q.kdiag = pb.kdiag; q.koff = pb.koff; q.info = pb.info;
+  q.gmu = pb.gmu; q.gdiag = pb.gdiag; q.goff = pb.goff; q.has_goff = pb.has_goff;
+  q.o_mean = pmview(b.omean, n, 1); q.o_diag = pmview(b.odiag, B2, 1); q.o_off = pmview(b.ooff, B2, 1);
+  q.o_cov = pmview(b.covs, B2, 1); q.o_cross = pmview(b.crosses, B2, 1);
+  q.active = nullptr; q.status = b.st; q.where = b.st + 1; q.nprobes = b.np;
+  q.beta = b.scal; q.kl = b.scal + 1; q.ld_next = b.scal + 2; q.temp = b.scal + 4; q.ld_cur = b.scal + 5;
+  q.kl_bound = kl_bound; q.beta_min = beta_min; q.beta_max = beta_max;
+  q.probe_log = probe_log ? b.plog : nullptr; q.max_probes = max_probes;
+  q.scratch = wscr; q.fixed = fixed;
+  GVP_TRY(launch_wide_step(q, s));
+  int stw[3];
+  GVP_TRY(d2h(stw, b.st, 3, s));
+  GVP_CUDA(cudaStreamSynchronize(s));
+  if (nprobes) *nprobes = fixed ? 0 : stw[2];
+  if (probe_log && !fixed && stw[2] > 0) {
+    GVP_TRY(d2h(probe_log, b.plog, (size_t)std::min(stw[2], max_probes) * 3, s));
+    GVP_CUDA(cudaStreamSynchronize(s));
+  }
+  if (stw[0] != GVP_OK) {
+    if (where) *where = stw[1];
+    if (stw[0] == GVP_ERR_NO_FEASIBLE_STEP) {
+      char msg[160];
+      std::snprintf(msg, sizeof msg, "no feasible step size at beta_min=%g (KL bound %g)", beta_min, kl_bound);
+      set_error(msg);
+    } else {
+      set_error("pivot block " + std::to_string(stw[1] & ~GVP_WHERE_MEAN_SOLVE_BIAS) + " is not positive definite");
+    }
+    return stw[0];
+  }
+  double sc[2];
+  GVP_TRY(d2h(sc, b.scal, 2, s));
+  GVP_TRY(d2h(out_mean, b.omean, K * n, s));
+  GVP_TRY(d2h(out_diag, b.odiag, K * B2, s));
+  GVP_TRY(d2h(out_off, b.ooff, (K - 1) * B2, s));
+  if (covs) GVP_TRY(d2h(covs, b.covs, K * B2, s));
+  if (crosses) GVP_TRY(d2h(crosses, b.crosses, (K - 1) * B2, s));
+  GVP_CUDA(cudaStreamSynchronize(s));
+  if (beta) *beta = sc[0];
+  if (kl) *kl = sc[1];
+  if (where) *where = -1;
+  return GVP_OK;
+}
+}  // namespace
+
 extern "C" int gvp_proximal_update(const double* mean, const double* diag, const double* off,
                                    const double* kdiag, const double* koff, const double* info,
                                    const double* g_mu, const double* gdiag, const double* goff,
@@ -466,8 +594,12 @@ extern "C" int gvp_proximal_update(const double* mean, const double* diag, const
   Context& C = ctx();
   std::lock_guard<std::mutex> lock(C.mu);
   GVP_TRY(C.init());
-  GVP_TRY(check_n(n));
+  GVP_TRY(check_chain_n(n));
   const int64_t K = nblocks, B2 = (int64_t)n * n;
+  if (n >= kWideMin)
+    return wide_step_call(C, mean, diag, off, kdiag, koff, info, g_mu, gdiag, goff, K, n, true, beta, temp, 0.0,
+                          0.0, 0.0, nullptr, nullptr, out_mean, out_diag, out_off, nullptr, nullptr, nullptr, 0,
+                          nullptr, where);
   StepBufs b;
   StepProblem pb;
   GVP_TRY(upload_step(C, mean, diag, off, kdiag, koff, info, g_mu, gdiag, goff, K, n, 0, b, pb));
@@ -591,7 +723,11 @@ extern "C" int gvp_select_step_size(const double* mean, const double* diag, cons
   Context& C = ctx();
   std::lock_guard<std::mutex> lock(C.mu);
   GVP_TRY(C.init());
-  GVP_TRY(check_n(n));
+  GVP_TRY(check_chain_n(n));
+  if (n >= kWideMin)
+    return wide_step_call(C, mean, diag, off, kdiag, koff, info, g_mu, gdiag, goff, nblocks, n, false, 0.0, temp,
+                          kl_bound, beta_min, beta_max, beta, kl, out_mean, out_diag, out_off, covs, crosses,
+                          probe_log, max_probes, nprobes, where);
   const int64_t K = nblocks, N2 = (int64_t)n * n, K1 = std::max<int64_t>(K - 1, 0);
   const bool v2_ok = (n == 2 || n == 4 || n == 6) && blocks_symmetric(diag, K, n) &&
                      blocks_symmetric(kdiag, K, n) && blocks_symmetric(gdiag, K, n) &&

@@ -182,6 +182,33 @@ struct V2Launch {
   double* scratch;
   const int* active;
 };
+// ---- wide blocks, 9 <= n <= 32 (wide_kernels.cu): one warp per chain, lanes over rows
+struct WideStep {
+  int nplans;
+  int64_t K;
+  int n;
+  View mean, diag, off, kdiag, koff, info, gmu, gdiag, goff;  // full n x n blocks
+  bool has_goff;
+  MutView o_mean, o_diag, o_off, o_cov, o_cross;
+  const int* active;
+  int *status, *where, *nprobes;
+  double *beta, *kl, *ld_next;  // beta: in = previous beta (NaN: none) / fixed beta, out = accepted
+  const double *temp, *ld_cur;
+  double kl_bound, beta_min, beta_max;
+  double* probe_log;
+  int max_probes;
+  double* scratch;  // wide_scratch_doubles
+  bool fixed;       // proximal_update only
+};
+int64_t wide_scratch_doubles(int nplans, int64_t K, int n);
+int launch_wide_marginals(int nplans, int64_t K, int n, const View& D, const View& U, const MutView& cov,
+                          const MutView& cross, double* logdet, double* scratch, int* status, int* where,
+                          cudaStream_t s);
+int launch_wide_mean_solve(int nplans, int64_t K, int n, const View& D, const View& U, const View& E,
+                           const MutView& x, double* scratch, int* status, int* where, cudaStream_t s);
+int launch_wide_logdet(int nplans, int64_t K, int n, const View& D, const View& U, double* logdet, double* chols,
+                       int* status, int* where, cudaStream_t s);
+int launch_wide_step(const WideStep& q, cudaStream_t s);
 int launch_select_step_v2(const V2Launch& q, cudaStream_t s);
 int launch_select_bisect(const V2Launch& q, cudaStream_t s);  // bisection only
 int launch_select_commit(const V2Launch& q, cudaStream_t s);  // commit of q.beta

@@ -1,0 +1,848 @@
+// Block-chain kernels for wide blocks, 9 <= n <= 32 (the 7-DOF arm of
+// configuration C3 has n = 14). The n <= 8 kernels keep a whole block per
+// thread in registers; at n = 14 a block is 196 doubles, so here one warp
+// owns one chain and its 32 lanes own the ROWS of the current blocks
+// (registers), with the blocks the other lanes need staged in the warp's
+// own shared-memory tiles (odd row stride: row-parallel reads are
+// bank-conflict free, column reads are broadcasts). No CTA barriers inside
+// a chain: each warp synchronises with __syncwarp only.
+//
+// The algorithms are the reference's, step for step:
+//   gbp_marginals   (gbp.py:43-80)   backward Schur with Cholesky of the
+//                                    symmetrised trailing block, forward
+//                                    covariance recursion;
+//   gbp_mean_solve  (gbp.py:83-106)  block forward elimination, back
+//                                    substitution;
+//   forward_schur_chols / logdet_block_tridiag (blocktri.py:151-174);
+//   select_step_size (optimizer.py:188-231) with proximal_update
+//                                    (optimizer.py:129-161) and kl_joint
+//                                    (optimizer.py:164-177): every probe is
+//                                    the mean solve on one warp and the
+//                                    marginals + trace on another; W probe
+//                                    slots per CTA evaluate the bisection's
+//                                    candidate betas speculatively (the
+//                                    shared search logic of step_common.cuh
+//                                    replays the reference's sequence).
+// Cholesky pivots follow chol_spd (blocktri.py:24-32): not > 0 (or NaN) or a
+// square root <= 1e-300 is "not positive definite".
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+
+#include "gvp_internal.cuh"
+#include "step_common.cuh"
+
+namespace gvp {
+namespace wide {
+
+constexpr unsigned FULL = 0xffffffffu;
+GVP_DEV int lane() { return threadIdx.x & 31; }
+
+template <int NM>
+struct Tile {
+  static constexpr int LD = NM + 1;   // odd stride
+  static constexpr int MAT = NM * LD;  // doubles per tile
+};
+
+// per-warp shared workspace: 5 tiles + 4 vectors
+template <int NM>
+struct WarpWs {
+  static constexpr int LD = Tile<NM>::LD, MAT = Tile<NM>::MAT;
+  static constexpr int DOUBLES = 5 * MAT + 4 * 32;
+  double *T, *L, *Li, *U, *X, *v0, *v1, *v2, *v3;
+  GVP_DEV explicit WarpWs(double* base) {
+    T = base;
+    L = base + MAT;
+    Li = base + 2 * MAT;
+    U = base + 3 * MAT;
+    X = base + 4 * MAT;
+    v0 = base + 5 * MAT;
+    v1 = v0 + 32;
+    v2 = v1 + 32;
+    v3 = v2 + 32;
+  }
+};
+
+// dst[r][c] = f(r, c) for the n x n block, lanes over the flattened entries
+template <int NM, class F>
+GVP_DEV void stage(double* dst, int n, F f) {
+  constexpr int LD = Tile<NM>::LD;
+  for (int idx = lane(); idx < n * n; idx += 32) {
+    const int r = idx / n, c = idx - r * n;
+    dst[r * LD + c] = f(r, c);
+  }
+  __syncwarp();
+}
+
+// Cholesky of the n x n block in tile A (lower triangle of A, or of
+// 0.5 (A + A') when SYM — the reference's chol_spd(symmetrize(.))) into tile
+// L (row r by lane r). Pivots multiply into (pm, pe) (mantissa, exponent).
+template <int NM, bool SYM>
+GVP_DEV bool chol(const double* A, double* L, int n, double& pm, int& pe) {
+  constexpr int LD = Tile<NM>::LD;
+  const int r = lane();
+  double a[NM], l[NM];
+#pragma unroll
+  for (int j = 0; j < NM; ++j) {
+    a[j] = 0.0;
+    l[j] = 0.0;
+    if (j < n && r < n && j <= r) a[j] = SYM ? 0.5 * (A[r * LD + j] + A[j * LD + r]) : A[r * LD + j];
+  }
+  bool ok = true;
+#pragma unroll
+  for (int j = 0; j < NM; ++j) {
+    if (j < n) {
+      double s = a[j];
+#pragma unroll
+      for (int k = 0; k < j; ++k) s -= l[k] * L[j * LD + k];
+      const double d = __shfl_sync(FULL, s, j);
+      const double piv = sqrt(d);
+      ok = ok && (d > 0.0) && (piv > kPivotFloor);
+      l[j] = (r == j) ? piv : (r > j ? s / piv : 0.0);
+      if (r < n && r >= j) L[r * LD + j] = l[j];
+      int e;
+      pm = frexp(pm * piv, &e);
+      pe += e;
+      __syncwarp();
+    }
+  }
+  return ok;
+}
+
+// Li = L^-1 (lower), lane c computes column c by forward substitution
+template <int NM>
+GVP_DEV void trinv(const double* L, double* Li, int n) {
+  constexpr int LD = Tile<NM>::LD;
+  const int c = lane();
+  double x[NM];
+#pragma unroll
+  for (int r = 0; r < NM; ++r) {
+    x[r] = 0.0;
+    if (r < n) {
+      double t = (r == c) ? 1.0 : 0.0;
+#pragma unroll
+      for (int k = 0; k < r; ++k) t -= L[r * LD + k] * x[k];
+      x[r] = (r >= c) ? t / L[r * LD + r] : 0.0;
+      if (c < n) Li[r * LD + c] = x[r];
+    }
+  }
+  __syncwarp();
+}
+
+// P = Li' Li (symmetric, exactly: entry (r, c) and (c, r) sum the same
+// products in the same order); row r by lane r into tile P
+template <int NM>
+GVP_DEV void ltl(const double* Li, double* P, int n) {
+  constexpr int LD = Tile<NM>::LD;
+  const int r = lane();
+  double p[NM];
+#pragma unroll
+  for (int c = 0; c < NM; ++c) {
+    double t = 0.0;
+    if (c < n && r < n) {
+#pragma unroll
+      for (int k = 0; k < NM; ++k)
+        if (k < n && k >= r && k >= c) t += Li[k * LD + r] * Li[k * LD + c];
+    }
+    p[c] = t;
+  }
+  __syncwarp();
+#pragma unroll
+  for (int c = 0; c < NM; ++c)
+    if (c < n && r < n) P[r * LD + c] = p[c];
+  __syncwarp();
+}
+
+// tile -> global rows (n x n, row-major, stride n)
+template <int NM>
+GVP_DEV void store_g(double* g, const double* S, int n) {
+  constexpr int LD = Tile<NM>::LD;
+  for (int idx = lane(); idx < n * n; idx += 32) {
+    const int r = idx / n, c = idx - r * n;
+    g[idx] = S[r * LD + c];
+  }
+}
+template <int NM>
+GVP_DEV void load_g(double* S, const double* g, int n) {
+  constexpr int LD = Tile<NM>::LD;
+  for (int idx = lane(); idx < n * n; idx += 32) {
+    const int r = idx / n, c = idx - r * n;
+    S[r * LD + c] = g[idx];
+  }
+  __syncwarp();
+}
+
+GVP_DEV double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
+  return v;
+}
+
+// ------------------------------------------------------------------ chain A
+// gbp_marginals of the chain whose blocks the source gives (diag(i, r, c),
+// off(i, r, c) = block (i, i+1)): backward Schur pivots Phi_i -> Phi_i^-1 in
+// the global scratch pg (K x n x n), then the forward covariance recursion.
+// Optional: covs/crosses out, tr(Lambda Sigma) against a second chain (tr),
+// log det from the backward pivots. Returns the failing knot or -1.
+template <int NM, class Src, class Out, class Tr>
+GVP_DEV int chain_marginals(const Src& src, int64_t K, int n, double* pg, WarpWs<NM>& w, const Out& out,
+                            const Tr& trc, double& trace, double& logdet) {
+  constexpr int LD = Tile<NM>::LD;
+  const int r = lane();
+  double pm = 1.0;
+  int pe = 0;
+  // ---- backward sweep: X holds Phi_{i+1}^-1
+  for (int64_t i = K - 1; i >= 0; --i) {
+    stage<NM>(w.T, n, [&](int a, int b) { return src.diag(i, a, b); });
+    if (i < K - 1) {
+      stage<NM>(w.U, n, [&](int a, int b) { return src.off(i, a, b); });
+      // trailing = D - U Phi^-1 U'
+      double y[NM];
+#pragma unroll
+      for (int c = 0; c < NM; ++c) {
+        double t = 0.0;
+        if (c < n && r < n) {
+#pragma unroll
+          for (int k = 0; k < NM; ++k)
+            if (k < n) t += w.U[r * LD + k] * w.X[k * LD + c];
+        }
+        y[c] = t;
+      }
+#pragma unroll
+      for (int c = 0; c < NM; ++c) {
+        if (c < n && r < n) {
+          double t = 0.0;
+#pragma unroll
+          for (int k = 0; k < NM; ++k)
+            if (k < n) t += y[k] * w.U[c * LD + k];
+          w.T[r * LD + c] -= t;
+        }
+      }
+      __syncwarp();
+    }
+    if (!chol<NM, true>(w.T, w.L, n, pm, pe)) return (int)i;
+    trinv<NM>(w.L, w.Li, n);
+    ltl<NM>(w.Li, w.X, n);
+    store_g<NM>(pg + i * (int64_t)n * n, w.X, n);
+  }
+  logdet = 2.0 * (log(pm) + (double)pe * 0.6931471805599453);
+  // ---- forward sweep: T holds Sigma_ii
+  __syncwarp();
+  load_g<NM>(w.T, pg, n);  // Sigma_00 = Phi_0^-1 (exactly symmetric)
+  double tr = 0.0;
+  for (int64_t i = 0; i < K; ++i) {
+    if (r < n) {
+#pragma unroll
+      for (int c = 0; c < NM; ++c)
+        if (c < n) {
+          const double s = w.T[r * LD + c];
+          out.cov(i, r, c, s);
+          tr += trc.diag(i, r, c) * w.T[c * LD + r];
+        }
+    }
+    if (i + 1 >= K) break;
+    load_g<NM>(w.X, pg + (i + 1) * (int64_t)n * n, n);  // Pn = Phi_{i+1}^-1
+    stage<NM>(w.U, n, [&](int a, int b) { return src.off(i, a, b); });
+    // G = U Pn -> L tile
+    {
+      double g[NM];
+#pragma unroll
+      for (int c = 0; c < NM; ++c) {
+        double t = 0.0;
+        if (c < n && r < n) {
+#pragma unroll
+          for (int k = 0; k < NM; ++k)
+            if (k < n) t += w.U[r * LD + k] * w.X[k * LD + c];
+        }
+        g[c] = t;
+      }
+#pragma unroll
+      for (int c = 0; c < NM; ++c)
+        if (c < n && r < n) w.L[r * LD + c] = g[c];
+      __syncwarp();
+    }
+    // C = Sigma_ii G = -Sigma_{i,i+1} -> Li tile
+    {
+      double cg[NM];
+#pragma unroll
+      for (int c = 0; c < NM; ++c) {
+        double t = 0.0;
+        if (c < n && r < n) {
+#pragma unroll
+          for (int k = 0; k < NM; ++k)
+            if (k < n) t += w.T[r * LD + k] * w.L[k * LD + c];
+        }
+        cg[c] = t;
+      }
+      __syncwarp();
+#pragma unroll
+      for (int c = 0; c < NM; ++c)
+        if (c < n && r < n) {
+          w.Li[r * LD + c] = cg[c];
+          out.cross(i, r, c, -cg[c]);
+          tr += 2.0 * trc.off(i, r, c) * (-cg[c]);
+        }
+      __syncwarp();
+    }
+    // Sigma_{i+1} = Pn + G' C, symmetrised
+    {
+      double s[NM];
+#pragma unroll
+      for (int c = 0; c < NM; ++c) {
+        double t = 0.0;
+        if (c < n && r < n) {
+          t = w.X[r * LD + c];
+          double u = 0.0;
+#pragma unroll
+          for (int k = 0; k < NM; ++k)
+            if (k < n) u += w.L[k * LD + r] * w.Li[k * LD + c];
+          t += u;
+        }
+        s[c] = t;
+      }
+#pragma unroll
+      for (int c = 0; c < NM; ++c)
+        if (c < n && r < n) w.U[r * LD + c] = s[c];
+      __syncwarp();
+#pragma unroll
+      for (int c = 0; c < NM; ++c)
+        if (c < n && r < n) w.T[r * LD + c] = 0.5 * (w.U[r * LD + c] + w.U[c * LD + r]);
+      __syncwarp();
+    }
+  }
+  trace = warp_sum(tr);
+  return -1;
+}
+
+// ------------------------------------------------------------------ chain B
+// gbp_mean_solve: forward elimination (pivots Cholesky-checked, the
+// reference's "pivot block i"), back substitution. Li_i and z_i = Li_i r_i
+// go to the global scratch (lg: K x n x n, zg: K x n). Optional: the result
+// (out.mean) and the Mahalanobis term d' Lambda d of d = mu - x against a
+// second chain (mh.diag / mh.off / mh.mean). Returns the failing knot or -1.
+template <int NM, class Src, class Out, class Mh>
+GVP_DEV int chain_mean(const Src& src, int64_t K, int n, double* lg, double* zg, WarpWs<NM>& w, const Out& out,
+                       const Mh& mh, double& mahal) {
+  constexpr int LD = Tile<NM>::LD;
+  const int r = lane();
+  double pm = 1.0;
+  int pe = 0;
+  for (int64_t i = 0; i < K; ++i) {
+    stage<NM>(w.T, n, [&](int a, int b) { return src.diag(i, a, b); });
+    double rv = r < n ? src.rhs(i, r) : 0.0;
+    if (i > 0) {
+      stage<NM>(w.U, n, [&](int a, int b) { return src.off(i - 1, a, b); });
+      // Z = Li_{i-1} U_{i-1} -> X tile;  trailing -= Z'Z;  r -= Z' z_{i-1}
+      double z[NM];
+#pragma unroll
+      for (int c = 0; c < NM; ++c) {
+        double t = 0.0;
+        if (c < n && r < n) {
+#pragma unroll
+          for (int k = 0; k < NM; ++k)
+            if (k < n && k <= r) t += w.Li[r * LD + k] * w.U[k * LD + c];
+        }
+        z[c] = t;
+      }
+#pragma unroll
+      for (int c = 0; c < NM; ++c)
+        if (c < n && r < n) w.X[r * LD + c] = z[c];
+      __syncwarp();
+      if (r < n) {
+        double t2 = 0.0;
+#pragma unroll
+        for (int c = 0; c < NM; ++c)
+          if (c < n) {
+            double t = 0.0;
+#pragma unroll
+            for (int k = 0; k < NM; ++k)
+              if (k < n) t += w.X[k * LD + r] * w.X[k * LD + c];
+            w.T[r * LD + c] -= t;
+          }
+#pragma unroll
+        for (int k = 0; k < NM; ++k)
+          if (k < n) t2 += w.X[k * LD + r] * w.v0[k];
+        rv -= t2;
+      }
+      __syncwarp();
+    }
+    if (!chol<NM, true>(w.T, w.L, n, pm, pe)) return (int)i;
+    trinv<NM>(w.L, w.Li, n);
+    if (r < 32) w.v1[r] = rv;
+    __syncwarp();
+    double zr = 0.0;
+    if (r < n) {
+#pragma unroll
+      for (int k = 0; k < NM; ++k)
+        if (k < n && k <= r) zr += w.Li[r * LD + k] * w.v1[k];
+    }
+    __syncwarp();
+    w.v0[r] = zr;
+    if (r < n) zg[i * n + r] = zr;
+    store_g<NM>(lg + i * (int64_t)n * n, w.Li, n);
+    __syncwarp();
+  }
+  // ---- back substitution: v2 holds x_{i+1}, v3 holds d_{i+1}
+  double mhl = 0.0;
+  for (int64_t i = K - 1; i >= 0; --i) {
+    load_g<NM>(w.Li, lg + i * (int64_t)n * n, n);
+    double wr = r < n ? zg[i * n + r] : 0.0;
+    if (i < K - 1) {
+      stage<NM>(w.U, n, [&](int a, int b) { return src.off(i, a, b); });
+      double q = 0.0;
+      if (r < n) {
+#pragma unroll
+        for (int k = 0; k < NM; ++k)
+          if (k < n) q += w.U[r * LD + k] * w.v2[k];
+      }
+      w.v1[r] = q;
+      __syncwarp();
+      double t = 0.0;
+      if (r < n) {
+#pragma unroll
+        for (int k = 0; k < NM; ++k)
+          if (k < n && k <= r) t += w.Li[r * LD + k] * w.v1[k];
+      }
+      wr -= t;
+      __syncwarp();
+    }
+    w.v1[r] = wr;
+    __syncwarp();
+    double x = 0.0;
+    if (r < n) {
+#pragma unroll
+      for (int k = 0; k < NM; ++k)
+        if (k < n && k >= r) x += w.Li[k * LD + r] * w.v1[k];
+      out.mean(i, r, x);
+    }
+    const double d = r < n ? mh.mean(i, r) - x : 0.0;
+    w.v0[r] = d;
+    __syncwarp();
+    if (r < n) {
+      double t = 0.0, t2 = 0.0;
+#pragma unroll
+      for (int c = 0; c < NM; ++c)
+        if (c < n) {
+          t += mh.diag(i, r, c) * w.v0[c];
+          if (i < K - 1) t2 += mh.off(i, r, c) * w.v3[c];
+        }
+      mhl += d * t + 2.0 * d * t2;
+    }
+    __syncwarp();
+    w.v2[r] = x;
+    w.v3[r] = d;
+    __syncwarp();
+  }
+  mahal = warp_sum(mhl);
+  return -1;
+}
+
+// ------------------------------------------------------------------ sources
+struct BtSrc {  // a stored block-tridiagonal matrix (+ rhs)
+  View D, U, E;
+  int64_t b;
+  int n;
+  GVP_DEV double diag(int64_t i, int r, int c) const { return D(b, i, r * n + c); }
+  GVP_DEV double off(int64_t i, int r, int c) const { return U(b, i, r * n + c); }
+  GVP_DEV double rhs(int64_t i, int r) const { return E(b, i, r); }
+};
+struct NoOut {
+  GVP_DEV void cov(int64_t, int, int, double) const {}
+  GVP_DEV void cross(int64_t, int, int, double) const {}
+  GVP_DEV void mean(int64_t, int, double) const {}
+};
+struct BtOut {
+  MutView C, X, M;
+  int64_t b;
+  int n;
+  GVP_DEV void cov(int64_t i, int r, int c, double v) const {
+    if (C.p) C(b, i, r * n + c) = v;
+  }
+  GVP_DEV void cross(int64_t i, int r, int c, double v) const {
+    if (X.p) X(b, i, r * n + c) = v;
+  }
+  GVP_DEV void mean(int64_t i, int r, double v) const {
+    if (M.p) M(b, i, r) = v;
+  }
+};
+struct NoTr {
+  GVP_DEV double diag(int64_t, int, int) const { return 0.0; }
+  GVP_DEV double off(int64_t, int, int) const { return 0.0; }
+  GVP_DEV double mean(int64_t, int) const { return 0.0; }
+};
+
+// ------------------------------------------------------------------ drop-in kernels (one warp per plan)
+template <int NM>
+__global__ void __launch_bounds__(32) marginals_kernel(int64_t K, int n, View D, View U, MutView cov, MutView cross,
+                                                       double* logdet, double* scratch, int* status, int* where) {
+  extern __shared__ __align__(16) double sm[];
+  WarpWs<NM> w(sm);
+  const int64_t b = blockIdx.x;
+  BtSrc src{D, U, View{nullptr, 0, 0, 0}, b, n};
+  BtOut out{cov, cross, MutView{nullptr, 0, 0, 0}, b, n};
+  double tr, ld;
+  const int f = chain_marginals<NM>(src, K, n, scratch + b * K * n * n, w, out, NoTr{}, tr, ld);
+  if (lane() == 0) {
+    status[b] = f < 0 ? GVP_OK : GVP_ERR_NOT_SPD;
+    where[b] = f;
+    if (logdet && f < 0) logdet[b] = ld;
+  }
+}
+
+template <int NM>
+__global__ void __launch_bounds__(32) mean_solve_kernel(int64_t K, int n, View D, View U, View E, MutView x,
+                                                        double* scratch, int* status, int* where) {
+  extern __shared__ __align__(16) double sm[];
+  WarpWs<NM> w(sm);
+  const int64_t b = blockIdx.x;
+  BtSrc src{D, U, E, b, n};
+  BtOut out{MutView{nullptr, 0, 0, 0}, MutView{nullptr, 0, 0, 0}, x, b, n};
+  double mh;
+  double* lg = scratch + b * K * (n * n + n);
+  const int f = chain_mean<NM>(src, K, n, lg, lg + K * n * n, w, out, NoTr{}, mh);
+  if (lane() == 0) {
+    status[b] = f < 0 ? GVP_OK : GVP_ERR_NOT_SPD;
+    where[b] = f;
+  }
+}
+
+// forward_schur_chols (blocktri.py:151-165): S_0 = D_0, S_i = D_i - W'W with
+// W = L_{i-1}^-1 U_{i-1}; chol_spd without symmetrising (LAPACK reads the
+// lower triangle); log det = 2 sum log diag L
+template <int NM>
+__global__ void __launch_bounds__(32) logdet_kernel(int64_t K, int n, View D, View U, double* logdet, double* chols,
+                                                    int* status, int* where) {
+  constexpr int LD = Tile<NM>::LD;
+  extern __shared__ __align__(16) double sm[];
+  WarpWs<NM> w(sm);
+  const int64_t b = blockIdx.x;
+  const int r = lane();
+  double pm = 1.0;
+  int pe = 0;
+  int f = -1;
+  for (int64_t i = 0; i < K; ++i) {
+    stage<NM>(w.T, n, [&](int a, int c) { return D(b, i, a * n + c); });
+    if (i > 0) {
+      stage<NM>(w.U, n, [&](int a, int c) { return U(b, i - 1, a * n + c); });
+      double z[NM];
+#pragma unroll
+      for (int c = 0; c < NM; ++c) {
+        double t = 0.0;
+        if (c < n && r < n) {
+#pragma unroll
+          for (int k = 0; k < NM; ++k)
+            if (k < n && k <= r) t += w.Li[r * LD + k] * w.U[k * LD + c];
+        }
+        z[c] = t;
+      }
+#pragma unroll
+      for (int c = 0; c < NM; ++c)
+        if (c < n && r < n) w.X[r * LD + c] = z[c];
+      __syncwarp();
+      if (r < n) {
+#pragma unroll
+        for (int c = 0; c < NM; ++c)
+          if (c < n) {
+            double t = 0.0;
+#pragma unroll
+            for (int k = 0; k < NM; ++k)
+              if (k < n) t += w.X[k * LD + r] * w.X[k * LD + c];
+            w.T[r * LD + c] -= t;
+          }
+      }
+      __syncwarp();
+    }
+    if (!chol<NM, false>(w.T, w.L, n, pm, pe)) {
+      f = (int)i;
+      break;
+    }
+    if (chols) {
+      double* g = chols + (b * K + i) * n * n;
+      for (int idx = lane(); idx < n * n; idx += 32) {
+        const int a = idx / n, c = idx - a * n;
+        g[idx] = c <= a ? w.L[a * LD + c] : 0.0;
+      }
+    }
+    trinv<NM>(w.L, w.Li, n);
+  }
+  if (lane() == 0) {
+    status[b] = f < 0 ? GVP_OK : GVP_ERR_NOT_SPD;
+    where[b] = f;
+    if (f < 0) logdet[b] = 2.0 * (log(pm) + (double)pe * 0.6931471805599453);
+  }
+}
+
+// ------------------------------------------------------------------ step (bisection) kernel
+struct StepArgs {
+  // problem (one plan per CTA; plan-minor views)
+  View mean, diag, off, kdiag, koff, info, gmu, gdiag, goff;
+  bool has_goff;
+  int n;
+  int64_t K;
+  // outputs (write mode)
+  MutView o_mean, o_diag, o_off, o_cov, o_cross;
+  // search state / records (the field names step_common's search expects)
+  int B;
+  const int* active;
+  int* status;
+  int* where;
+  int* nprobes;
+  double* beta;
+  double* kl;
+  double* ld_next;
+  const double* temp;
+  const double* ld_cur;
+  double kl_bound, beta_min, beta_max;
+  double* probe_log;
+  int max_probes;
+  double* scratch;  // per plan: W slots x (A: K n^2 | B: K n^2 + K n)
+  int fixed;        // 1: proximal_update only (beta = beta[b], mean solve + Lambda')
+};
+
+// Lambda' and the mean system S of one probe (optimizer.py:151-159)
+struct ProbeSrcA {  // Lambda' = ((2 G / T + K / T) + Lambda / beta) * c, diag blocks symmetrised
+  const StepArgs* a;
+  int64_t b;
+  double two_t, inv_t, inv_b, c;
+  GVP_DEV double raw(int64_t i, int r, int q) const {
+    const int n = a->n;
+    return ((a->gdiag(b, i, r * n + q) * two_t + a->kdiag(b, i, r * n + q) * inv_t) + a->diag(b, i, r * n + q) * inv_b) * c;
+  }
+  GVP_DEV double diag(int64_t i, int r, int q) const { return 0.5 * (raw(i, r, q) + raw(i, q, r)); }
+  GVP_DEV double off(int64_t i, int r, int q) const {
+    const int n = a->n;
+    const double g = a->has_goff ? a->goff(b, i, r * n + q) : 0.0;
+    return ((g * two_t + a->koff(b, i, r * n + q) * inv_t) + a->off(b, i, r * n + q) * inv_b) * c;
+  }
+};
+struct ProbeSrcB {  // S = K / T + Lambda / beta; rhs = (-g / T + eta / T) + (Lambda / beta) mu
+  const StepArgs* a;
+  int64_t b;
+  double temp, inv_t, inv_b;
+  GVP_DEV double diag(int64_t i, int r, int q) const {
+    const int n = a->n;
+    return a->kdiag(b, i, r * n + q) * inv_t + a->diag(b, i, r * n + q) * inv_b;
+  }
+  GVP_DEV double off(int64_t i, int r, int q) const {
+    const int n = a->n;
+    return a->koff(b, i, r * n + q) * inv_t + a->off(b, i, r * n + q) * inv_b;
+  }
+  GVP_DEV double rhs(int64_t i, int r) const {
+    const int n = a->n;
+    double mv = 0.0;  // blocktri matvec of Lambda * (1/beta): D_i mu_i + U_i mu_{i+1} + U_{i-1}' mu_{i-1}
+    for (int q = 0; q < n; ++q) mv += (a->diag(b, i, r * n + q) * inv_b) * a->mean(b, i, q);
+    if (i + 1 < a->K)
+      for (int q = 0; q < n; ++q) mv += (a->off(b, i, r * n + q) * inv_b) * a->mean(b, i + 1, q);
+    if (i > 0)
+      for (int q = 0; q < n; ++q) mv += (a->off(b, i - 1, q * n + r) * inv_b) * a->mean(b, i - 1, q);
+    return ((-a->gmu(b, i, r)) / temp + a->info(b, i, r) / temp) + mv;
+  }
+};
+struct CurTr {  // the current precision Lambda and mean (trace / Mahalanobis terms)
+  const StepArgs* a;
+  int64_t b;
+  GVP_DEV double diag(int64_t i, int r, int c) const { return a->diag(b, i, r * a->n + c); }
+  GVP_DEV double off(int64_t i, int r, int c) const { return a->off(b, i, r * a->n + c); }
+  GVP_DEV double mean(int64_t i, int r) const { return a->mean(b, i, r); }
+};
+
+template <int NM, int W>
+__global__ void __launch_bounds__(64 * W) step_kernel(const __grid_constant__ StepArgs a) {
+  extern __shared__ __align__(16) double sm[];
+  const int tid = threadIdx.x, warp = tid >> 5, slot = warp >> 1, role = warp & 1;
+  const int64_t b = blockIdx.x;
+  const int n = a.n;
+  const int64_t K = a.K;
+  WarpWs<NM> w(sm + warp * WarpWs<NM>::DOUBLES);
+  double* tail = sm + 2 * W * WarpWs<NM>::DOUBLES;
+  v3::PlanSt* pst = reinterpret_cast<v3::PlanSt*>(tail);  // 10 doubles
+  double* r_beta = tail + 16;
+  double* r_kl = r_beta + W;
+  int* r_res = reinterpret_cast<int*>(r_kl + W);
+  int* r_fail = r_res + W;
+  int* r_on = r_fail + W;
+  double* xv = reinterpret_cast<double*>(r_on + W + (W & 1));  // per slot: trace, logdet, mahal
+  int* xf = reinterpret_cast<int*>(xv + 3 * W);                 // per slot: fail A, fail B
+  const int64_t per_slot = K * n * n * 2 + K * n;
+  double* scr = a.scratch + (b * W + slot) * per_slot;
+
+  auto run = [&](double beta, bool write) {
+    const double temp = a.temp[b];
+    const double inv_t = 1.0 / temp, two_t = 2.0 / temp, inv_b = 1.0 / beta, c = beta / (beta + 1.0);
+    double tr = 0.0, ld = 0.0, mh = 0.0;
+    int f = -1;
+    if (role == 0) {
+      if (!a.fixed) {
+        ProbeSrcA src{&a, b, two_t, inv_t, inv_b, c};
+        BtOut out{write ? a.o_cov : MutView{nullptr, 0, 0, 0}, write ? a.o_cross : MutView{nullptr, 0, 0, 0},
+                  MutView{nullptr, 0, 0, 0}, b, n};
+        f = chain_marginals<NM>(src, K, n, scr, w, out, CurTr{&a, b}, tr, ld);
+      }
+      if (write) {  // Lambda' blocks (symmetrised diagonal, optimizer.py:151-153)
+        ProbeSrcA src{&a, b, two_t, inv_t, inv_b, c};
+        for (int64_t idx = lane(); idx < K * n * n; idx += 32) {
+          const int64_t i = idx / (n * n);
+          const int e = (int)(idx - i * n * n), r = e / n, q = e - r * n;
+          a.o_diag(b, i, e) = src.diag(i, r, q);
+          if (i + 1 < K) a.o_off(b, i, e) = src.off(i, r, q);
+        }
+      }
+    } else {
+      ProbeSrcB src{&a, b, temp, inv_t, inv_b};
+      BtOut out{MutView{nullptr, 0, 0, 0}, MutView{nullptr, 0, 0, 0}, write ? a.o_mean : MutView{nullptr, 0, 0, 0},
+                b, n};
+      f = chain_mean<NM>(src, K, n, scr + K * n * n, scr + 2 * K * n * n, w, out, CurTr{&a, b}, mh);
+    }
+    if (lane() == 0) {
+      if (role == 0) {
+        xv[slot * 3 + 0] = tr;
+        xv[slot * 3 + 1] = ld;
+        xf[slot * 2 + 0] = f;
+      } else {
+        xv[slot * 3 + 2] = mh;
+        xf[slot * 2 + 1] = f;
+      }
+    }
+  };
+
+  if (a.fixed) {  // proximal_update: slot 0 only
+    if (slot == 0) run(a.beta[b], true);
+    __syncthreads();
+    if (tid == 0) {
+      const int fB = xf[1];
+      a.status[b] = fB < 0 ? GVP_OK : GVP_ERR_NOT_SPD;
+      a.where[b] = fB;
+    }
+    return;
+  }
+
+  v3::search_init(a, pst, 1, b, false, tid);
+  __syncthreads();
+  for (;;) {
+    const v3::Pick pk = v3::search_pick(a, pst, 1, W, slot, tid, false);
+    if (pk.kl == 0) break;
+    __syncthreads();
+    if (pk.on) run(pk.beta, false);
+    __syncthreads();
+    if (tid < W) {
+      const int s = tid;
+      const v3::Pick ps = v3::search_pick(a, pst, 1, W, s, -1, false);
+      const int fA = xf[s * 2], fB = xf[s * 2 + 1];
+      const int rr = fB >= 0 ? 2 : (fA >= 0 ? 1 : 0);
+      double klv = 0.0;
+      if (ps.on && rr == 0) {
+        const double x = 0.5 * ((((xv[s * 3] + xv[s * 3 + 2]) - (double)(K * n)) + xv[s * 3 + 1]) - a.ld_cur[b]);
+        klv = (0.0 > x) ? 0.0 : x;  // python max(x, 0.0): NaN stays NaN
+      }
+      r_beta[s] = ps.beta;
+      r_kl[s] = klv;
+      r_res[s] = rr;
+      r_fail[s] = fB >= 0 ? fB : fA;
+      r_on[s] = ps.on ? 1 : 0;
+    }
+    __syncthreads();
+    if (tid == 0) v3::search_decide(a, pst, 0, pk.dbase, pk.dkl, b, false, r_beta, r_kl, r_res, r_fail, r_on);
+    __syncthreads();
+  }
+  // commit: the accepted beta re-probed in write mode (deterministic: the same
+  // numbers as its probe), KL and log det of the accepted state
+  const bool ok = (b < a.B) && (!a.active || a.active[b]) && a.status[b] == GVP_OK;
+  if (ok && slot == 0) run(a.beta[b], true);
+  __syncthreads();
+  if (ok && tid == 0) {
+    const int fA = xf[0], fB = xf[1];
+    if (fA >= 0 || fB >= 0) {
+      a.status[b] = GVP_ERR_NOT_SPD;
+      a.where[b] = fB >= 0 ? (fB | GVP_WHERE_MEAN_SOLVE_BIAS) : fA;
+    } else {
+      const double x = 0.5 * ((((xv[0] + xv[2]) - (double)(K * n)) + xv[1]) - a.ld_cur[b]);
+      a.kl[b] = (0.0 > x) ? 0.0 : x;
+      if (a.ld_next) a.ld_next[b] = xv[1];
+    }
+  }
+}
+
+template <int NM>
+constexpr int slots() {
+  return NM <= 16 ? 8 : 2;
+}
+
+}  // namespace wide
+
+// ---------------------------------------------------------------------- host
+int64_t wide_scratch_doubles(int nplans, int64_t K, int n) {
+  const int W = n <= 16 ? wide::slots<16>() : wide::slots<32>();
+  return (int64_t)nplans * W * (K * n * n * 2 + K * n);
+}
+
+template <class F>
+static int wide_dispatch(int n, F f) {
+  if (n >= 9 && n <= 16) return f(std::integral_constant<int, 16>{});
+  if (n >= 17 && n <= 32) return f(std::integral_constant<int, 32>{});
+  set_error("wide block kernels support 9 <= n <= 32");
+  return GVP_ERR_UNSUPPORTED;
+}
+
+int launch_wide_marginals(int nplans, int64_t K, int n, const View& D, const View& U, const MutView& cov,
+                          const MutView& cross, double* logdet, double* scratch, int* status, int* where,
+                          cudaStream_t s) {
+  return wide_dispatch(n, [&](auto tag) -> int {
+    constexpr int NM = decltype(tag)::value;
+    const size_t bytes = wide::WarpWs<NM>::DOUBLES * 8;
+    GVP_CUDA(cudaFuncSetAttribute(wide::marginals_kernel<NM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+    wide::marginals_kernel<NM><<<nplans, 32, bytes, s>>>(K, n, D, U, cov, cross, logdet, scratch, status, where);
+    GVP_CUDA(cudaGetLastError());
+    return GVP_OK;
+  });
+}
+
+int launch_wide_mean_solve(int nplans, int64_t K, int n, const View& D, const View& U, const View& E,
+                           const MutView& x, double* scratch, int* status, int* where, cudaStream_t s) {
+  return wide_dispatch(n, [&](auto tag) -> int {
+    constexpr int NM = decltype(tag)::value;
+    const size_t bytes = wide::WarpWs<NM>::DOUBLES * 8;
+    GVP_CUDA(cudaFuncSetAttribute(wide::mean_solve_kernel<NM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+    wide::mean_solve_kernel<NM><<<nplans, 32, bytes, s>>>(K, n, D, U, E, x, scratch, status, where);
+    GVP_CUDA(cudaGetLastError());
+    return GVP_OK;
+  });
+}
+
+int launch_wide_logdet(int nplans, int64_t K, int n, const View& D, const View& U, double* logdet, double* chols,
+                       int* status, int* where, cudaStream_t s) {
+  return wide_dispatch(n, [&](auto tag) -> int {
+    constexpr int NM = decltype(tag)::value;
+    const size_t bytes = wide::WarpWs<NM>::DOUBLES * 8;
+    GVP_CUDA(cudaFuncSetAttribute(wide::logdet_kernel<NM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+    wide::logdet_kernel<NM><<<nplans, 32, bytes, s>>>(K, n, D, U, logdet, chols, status, where);
+    GVP_CUDA(cudaGetLastError());
+    return GVP_OK;
+  });
+}
+
+int launch_wide_step(const WideStep& q, cudaStream_t s) {
+  wide::StepArgs a;
+  std::memset(&a, 0, sizeof(a));
+  a.mean = q.mean; a.diag = q.diag; a.off = q.off; a.kdiag = q.kdiag; a.koff = q.koff; a.info = q.info;
+  a.gmu = q.gmu; a.gdiag = q.gdiag; a.goff = q.goff; a.has_goff = q.has_goff;
+  a.n = q.n; a.K = q.K;
+  a.o_mean = q.o_mean; a.o_diag = q.o_diag; a.o_off = q.o_off; a.o_cov = q.o_cov; a.o_cross = q.o_cross;
+  a.B = q.nplans; a.active = q.active; a.status = q.status; a.where = q.where; a.nprobes = q.nprobes;
+  a.beta = q.beta; a.kl = q.kl; a.ld_next = q.ld_next; a.temp = q.temp; a.ld_cur = q.ld_cur;
+  a.kl_bound = q.kl_bound; a.beta_min = q.beta_min; a.beta_max = q.beta_max;
+  a.probe_log = q.probe_log; a.max_probes = q.max_probes; a.scratch = q.scratch; a.fixed = q.fixed ? 1 : 0;
+  return wide_dispatch(q.n, [&](auto tag) -> int {
+    constexpr int NM = decltype(tag)::value;
+    constexpr int W = wide::slots<NM>();
+    const size_t bytes = (2 * W * wide::WarpWs<NM>::DOUBLES + 16 + 8 * W + 8) * 8;
+    GVP_CUDA(cudaFuncSetAttribute(wide::step_kernel<NM, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+    wide::step_kernel<NM, W><<<q.nplans, 64 * W, bytes, s>>>(a);
+    GVP_CUDA(cudaGetLastError());
+    return GVP_OK;
+  });
+}
+
+}  // namespace gvp

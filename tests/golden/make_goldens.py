@@ -396,6 +396,62 @@ def slr_py():
     np.savez_compressed(os.path.join(HERE, "slr_py.npz"), **out)
 
 
+def wide():
+    """Wide blocks (SURVEY.md §8c golden (2): n = 14, the 7-DOF arm state; plus
+    n = 10 and n = 20): chain drop-ins and one select_step_size on a 7-DOF
+    double-integrator prior."""
+    out = {}
+    for tag, seed, K, n in [("w14", 41, 51, 14), ("w10", 43, 30, 10), ("w20", 47, 12, 20)]:
+        rng = np.random.default_rng(seed)
+        prec = random_spd_bt(rng, K, n)
+        eta = rng.normal(size=K * n)
+        d, o = stack_bt(prec)
+        marg = gbp_marginals(prec)
+        out[f"{tag}_diag"], out[f"{tag}_off"] = d, o
+        out[f"{tag}_eta"] = eta.reshape(K, n)
+        out[f"{tag}_covs"] = np.stack(marg.covs)
+        out[f"{tag}_crosses"] = np.stack(marg.crosses)
+        out[f"{tag}_mean"] = gbp_mean_solve(prec, eta).reshape(K, n)
+        out[f"{tag}_logdet"] = np.array(logdet_block_tridiag(prec))
+    # select_step_size at n = 14 (7-DOF double integrator, N = 30)
+    from gvplan.dynamics import LTVStep, LTVSystem
+    A = np.zeros((14, 14))
+    A[:7, 7:] = np.eye(7)
+    B = np.zeros((14, 7))
+    B[7:, :] = np.eye(7)
+    sys_ltv = LTVSystem(steps=tuple([LTVStep(A=A, a=np.zeros(14), B=B)] * 31), dt=0.1, n=14, m=7)
+    goal = np.concatenate([np.linspace(0.5, 1.5, 7), np.zeros(7)])
+    prior = assemble_prior(sys_ltv, np.zeros(14), goal, 1.0, 1e-3)
+    cfg = OptimizerConfig(kl_bound=5e-2)
+    state = ref_opt.initial_state(prior, cfg)
+    rng = np.random.default_rng(53)
+    K, n = prior.nsteps + 1, prior.n
+    g_mu = 3.0 * rng.normal(size=K * n)
+    gs = BlockTridiagonalMatrix.zeros(K, n)
+    for i in range(1, K - 1):
+        a = 0.1 * rng.normal(size=(n, n))
+        gs.diag[i] = a @ a.T
+    log, restore = probe_log()
+    sel = select_step_size(state, prior, g_mu, gs, cfg, temp=1.0)
+    restore()
+    pd, po = stack_bt(prior.prec)
+    cd, co = stack_bt(state.prec)
+    gd, _ = stack_bt(gs)
+    nd, no = stack_bt(sel.next_state.prec)
+    prox = ref_opt.proximal_update(state, prior, g_mu, gs, 0.05, 1.0)
+    xd, xo = stack_bt(prox.prec)
+    out.update({"s14_kdiag": pd, "s14_koff": po, "s14_info": prior.info.reshape(K, n),
+                "s14_mean": state.mean.reshape(K, n), "s14_diag": cd, "s14_off": co,
+                "s14_gmu": g_mu.reshape(K, n), "s14_gdiag": gd,
+                "s14_cfg": np.array([cfg.kl_bound, cfg.beta_min, cfg.beta_max, 1.0]),
+                "s14_beta": np.array(sel.beta), "s14_kl": np.array(sel.kl),
+                "s14_nmean": sel.next_state.mean.reshape(K, n), "s14_ndiag": nd, "s14_noff": no,
+                "s14_ncovs": np.stack(sel.marginals.covs), "s14_ncrosses": np.stack(sel.marginals.crosses),
+                "s14_probes": np.array(log),
+                "s14_prox_mean": prox.mean.reshape(K, n), "s14_prox_diag": xd, "s14_prox_off": xo})
+    np.savez_compressed(os.path.join(HERE, "wide.npz"), **out)
+
+
 if __name__ == "__main__":
     which = sys.argv[1:] or ["rules", "factors", "chain", "steps", "priors", "maps", "runs", "slr"]
     for name in which:
