@@ -40,7 +40,7 @@ extern "C" {
 #define GVP_ERR_NO_FEASIBLE_STEP 3 /* RuntimeError "no feasible step size" (optimizer.py:217-221) */
 #define GVP_ERR_SQRT 4             /* gaussian_sqrt needed its eigh root (quadrature.py:178-181) */
 #define GVP_ERR_ARG -1             /* bad argument (ValueError) */
-#define GVP_ERR_UNSUPPORTED -2     /* block size n outside 1..8, or grid ndim not 2/3 */
+#define GVP_ERR_UNSUPPORTED -2     /* block size n outside the supported range, or grid ndim not 2/3 */
 #define GVP_ERR_CUDA -3            /* CUDA runtime failure; see gvp_last_error() */
 #define GVP_ERR_NO_DEVICE -4       /* no CUDA device visible */
 
@@ -87,6 +87,11 @@ int gvp_evaluate_factors(const double* mean, const double* covs, int64_t nblocks
                          const double* origin, double cell_size, double radius_eps,
                          double sigma_obs, double* e_psi, double* g_mu, double* g_sigma,
                          int64_t* oob, int64_t* where);
+
+/* The block-chain drop-ins below (marginals, mean solve, log det, forward
+ * Schur chols, proximal update, select_step_size) take 1 <= n <= 32: n <= 8
+ * on the register-block kernels, 9 <= n <= 32 (e.g. the 7-DOF arm's n = 14)
+ * on the warp-per-chain kernels of csrc/wide_kernels.cu. */
 
 /* Marginal covariance blocks of an SPD block-tridiagonal precision by exact
  * chain GBP. Replaces gvplan.gbp.gbp_marginals (gbp.py:43-80). covs (nblocks,
@@ -268,6 +273,23 @@ int gvp_arm_factor_expectations(int64_t nfac, const double* means, const double*
                                 const double* base, int32_t nspheres, const int32_t* sphere_link,
                                 const double* sphere_geom, double radius_eps, double sigma_obs, double* e0,
                                 double* e1, double* e2, int64_t* oob);
+
+/* Device-resident arm collision model for the planner loop (the factor stage
+ * of evaluate_all_factors, factors.py:167-225, for the arm): created once
+ * with the grid, arm and the rule's projection tables (as above), then per
+ * call: covariances -> gaussian_sqrt (quadrature.py:164-181, GVP_ERR_SQRT if
+ * the eigh root would be needed) -> moments -> _moment_gradients
+ * (factors.py:95-104). means (F,14), covs (F,14,14); out e_psi (F) =
+ * max(e0, 0), g_mu (F,14), g_sigma (F,14,14), oob. GVP_ERR_NONFINITE /
+ * GVP_ERR_SQRT: *where = position of the factor in the call. */
+typedef struct gvp_arm gvp_arm;
+int gvp_arm_create(gvp_arm** out, const double* grid, const int64_t* shape, const double* origin, double cell,
+                   const double* dh, const double* base, int32_t nspheres, const int32_t* sphere_link,
+                   const double* sphere_geom, double radius_eps, double sigma_obs, int32_t nproj,
+                   const double* proj, const double* mom, const int32_t* cnt);
+void gvp_arm_destroy(gvp_arm* h);
+int gvp_arm_factor_grads(gvp_arm* h, int64_t nfac, const double* means, const double* covs, double* e_psi,
+                         double* g_mu, double* g_sigma, int64_t* oob, int64_t* where);
 
 /* ------------------------------------------------ batched device kernels (tests) */
 /* All pointers device memory, plan-minor layout with nplans plans, async on

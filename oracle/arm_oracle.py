@@ -86,3 +86,23 @@ def arm_factor_expectations(means, chols, points, weights, grid, origin, cell, d
             e1[f] += w * dx[l]
             e2[f] += w * np.outer(dx[l], dx[l])
     return e0, e1, e2, oob
+
+
+def arm_evaluate_factors(mean, covs, points, weights, grid, origin, cell, dh, base, sphere_link, sphere_geom,
+                         radius_eps, sigma_obs):
+    """The factor stage (factors.py:167-225) with the arm potential: interior
+    knots 1..K-2, gaussian_sqrt roots, moments, _moment_gradients; returns
+    (e_psi (F,), g_mu (F, n), g_sigma (F, n, n), oob)."""
+    from gvp_oracle import gaussian_sqrt, moment_gradients
+
+    mean = np.asarray(mean, float)
+    covs = np.asarray(covs, float)
+    K, n = mean.shape
+    F = max(K - 2, 0)
+    chols = np.stack([gaussian_sqrt(covs[i]) for i in range(1, K - 1)]) if F else np.zeros((0, n, n))
+    e0, e1, e2, oob = arm_factor_expectations(mean[1:K - 1], chols, points, weights, grid, origin, cell, dh, base,
+                                              sphere_link, sphere_geom, radius_eps, sigma_obs)
+    g_mu, g_s = np.zeros((F, n)), np.zeros((F, n, n))
+    for f in range(F):
+        g_mu[f], g_s[f] = moment_gradients(e0[f], e1[f], e2[f], covs[f + 1])
+    return np.maximum(e0, 0.0), g_mu, g_s, oob

@@ -497,10 +497,12 @@ def assemble_prior(As, avs, Bs, dt, x0, goal, q_c, sigma_b):
 def run_pgvimp(prior, grid, origin, cell, radius_eps, sigma_obs, points, weights,
                kl_bound=0.1, beta_min=1e-4, beta_max=0.9, temp_low=1.0, temp_high=10.0,
                collision_tol=None, max_iters=200, tol_mean=1e-5, tol_cost=1e-6,
-               init_cov_scale=0.1, x0=None, goal=None, init_mean=None, trace=None):
+               init_cov_scale=0.1, x0=None, goal=None, init_mean=None, trace=None, factor_fn=None):
     """Device-free restatement of run_pgvimp (optimizer.py:299-401) for one
     plan with an environment. Returns dict(mean, diag, off, covs, crosses,
-    records, converged, iterations, switch_iteration)."""
+    records, converged, iterations, switch_iteration). factor_fn(mean, covs) ->
+    (e_psi, g_mu, g_sigma, oob) replaces the point-robot factor stage (the
+    7-DOF arm oracle, arm_oracle.arm_evaluate_factors)."""
     k_diag, k_off, info, pmean = prior["diag"], prior["off"], prior["info"], prior["mean"]
     K, n = pmean.shape
     N = K - 1
@@ -524,15 +526,16 @@ def run_pgvimp(prior, grid, origin, cell, radius_eps, sigma_obs, points, weights
     g_off = np.zeros_like(k_off)
     for it in range(1, max_iters + 1):
         if cached is None:
-            e_psi, gm, gs, _ = evaluate_factors(mean, covs, points, weights, grid, origin,
-                                                cell, radius_eps, sigma_obs)
+            e_psi, gm, gs, _ = (factor_fn(mean, covs) if factor_fn else
+                                evaluate_factors(mean, covs, points, weights, grid, origin, cell, radius_eps,
+                                                 sigma_obs))
             cached = (e_psi, gm, gs)
         g_mu, g_diag = joint_gradients(cached[1], cached[2], K)
         beta, nm, nd, no, kl, cv, cr = select_step(mean, diag, off, k_diag, k_off, info,
                                                    g_mu, g_diag, g_off, temp, kl_bound,
                                                    beta_min, beta_max, trace=trace)
-        e_psi, gm, gs, _ = evaluate_factors(nm, cv, points, weights, grid, origin,
-                                            cell, radius_eps, sigma_obs)
+        e_psi, gm, gs, _ = (factor_fn(nm, cv) if factor_fn else
+                            evaluate_factors(nm, cv, points, weights, grid, origin, cell, radius_eps, sigma_obs))
         cached = (e_psi, gm, gs)
         pc, cc, ec = cost_breakdown(nm, nd, no, pmean, k_diag, k_off, cv, cr, e_psi, temp)
         total = pc + cc + ec

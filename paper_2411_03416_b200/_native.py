@@ -94,6 +94,10 @@ _SIGS = {
     "gvp_arm_factor_expectations": (C.c_int, [C.c_int64, _dp, _dp, C.c_int32, _dp, _dp, _i32p, _dp, _i64p, _dp,
                                               C.c_double, _dp, _dp, C.c_int32, _i32p, _dp, C.c_double,
                                               C.c_double, _dp, _dp, _dp, _i64p]),
+    "gvp_arm_create": (C.c_int, [C.POINTER(C.c_void_p), _dp, _i64p, _dp, C.c_double, _dp, _dp, C.c_int32, _i32p,
+                                 _dp, C.c_double, C.c_double, C.c_int32, _dp, _dp, _i32p]),
+    "gvp_arm_destroy": (None, [C.c_void_p]),
+    "gvp_arm_factor_grads": (C.c_int, [C.c_void_p, C.c_int64, _dp, _dp, _dp, _dp, _dp, _i64p, _i64p]),
     "gvp_slr_quadrotor": (C.c_int, [C.c_int32, C.c_int32, _dp, _dp, _dp, _dp, C.c_int32, C.c_double, _dp, _dp,
                                     _dp, _i32p, _i32p]),
     "gvp_prior_assemble": (C.c_int, [C.c_int32, C.c_int32, C.c_int32, C.c_int32, _dp, _dp, _dp, C.c_double,

@@ -125,3 +125,89 @@ def arm_factor_expectations(means, chols, rule: QuadratureRule, sdf: SignedDista
     if code != N.GVP_OK:
         raise RuntimeError(f"gvp_arm_factor_expectations: {N.last_error()}")
     return e0, e1, e2, int(oob[0])
+
+
+class ArmEnvironment:
+    """Collision environment of the 7-DOF sphere arm for ``run_pgvimp`` (the
+    reference's ``Environment(sdf, model)`` with the arm's forward kinematics):
+    the 3D map, the arm and the rule's projection tables stay resident on the
+    device (gvp_arm_create); every factor stage is one call
+    (gvp_arm_factor_grads: gaussian_sqrt -> moments -> moment gradients)."""
+
+    def __init__(self, sdf: SignedDistanceField, model: CollisionModel, arm: SphereArm):
+        if sdf.values.ndim != 3:
+            raise ValueError("the arm needs a 3D signed-distance field")
+        self.sdf, self.model, self.arm = sdf, model, arm
+        self._handle = None
+        self._rule_id = None
+
+    def _bind(self, rule: QuadratureRule):
+        if self._handle is not None and self._rule_id == id(rule):
+            return self._handle
+        self.close()
+        tab = arm_projection_tables(rule)
+        grid = N.f64(self.sdf.values)
+        h = N.C.c_void_p()
+        lib = N.load()
+        code = lib.gvp_arm_create(
+            N.C.byref(h), N.ptr(grid), N.ptr(np.asarray(grid.shape, dtype=np.int64)), N.ptr(N.f64(self.sdf.origin)),
+            float(self.sdf.cell_size), N.ptr(N.f64(self.arm.dh)), N.ptr(N.f64(self.arm.base)),
+            len(self.arm.sphere_link), N.ptr(np.ascontiguousarray(self.arm.sphere_link, dtype=np.int32)),
+            N.ptr(N.f64(self.arm.geom)), float(self.model.radius_eps), float(self.model.sigma_obs), len(tab.proj),
+            N.ptr(N.f64(tab.proj)), N.ptr(N.f64(tab.mom)), N.ptr(np.ascontiguousarray(tab.cnt, dtype=np.int32)))
+        N.check(code, "gvp_arm_create")
+        if code != N.GVP_OK:
+            raise RuntimeError(f"gvp_arm_create: {N.last_error()}")
+        self._handle, self._rule_id, self._rule = h, id(rule), rule
+        return h
+
+    def factor_gradients(self, joint_mean, covs, rule: QuadratureRule):
+        """(e_psi (F,), g_mu (F, 14), g_sigma (F, 14, 14)) of the interior
+        knots 1..K-2 (factors.py:159-225 with the arm's potential)."""
+        from .factors import FactorEvaluationError
+
+        covs = np.asarray(covs, dtype=np.float64)
+        K = covs.shape[0]
+        mean = np.asarray(joint_mean, dtype=np.float64).reshape(K, 2 * NQ)
+        F = max(K - 2, 0)
+        e_psi, g_mu, g_s = np.zeros(F), np.zeros((F, 2 * NQ)), np.zeros((F, 2 * NQ, 2 * NQ))
+        if F == 0:
+            return e_psi, g_mu, g_s
+        h = self._bind(rule)
+        oob, where = np.zeros(1, dtype=np.int64), np.zeros(1, dtype=np.int64)
+        code = N.load().gvp_arm_factor_grads(h, F, N.ptr(N.f64(mean[1:K - 1])), N.ptr(N.f64(covs[1:K - 1])),
+                                             N.ptr(e_psi), N.ptr(g_mu), N.ptr(g_s), N.ptr(oob), N.ptr(where))
+        N.check(code, "gvp_arm_factor_grads")
+        if code == N.GVP_ERR_NONFINITE:
+            raise FactorEvaluationError(int(where[0]) + 1, "non-finite expectation")
+        if code == N.GVP_ERR_SQRT:
+            raise NotImplementedError(f"factor {int(where[0]) + 1}: covariance needs the eigh root of gaussian_sqrt")
+        if code != N.GVP_OK:
+            raise RuntimeError(f"gvp_arm_factor_grads: {N.last_error()}")
+        self.sdf.note_oob(int(oob[0]))
+        return e_psi, g_mu, g_s
+
+    def close(self):
+        if self._handle is not None:
+            N.load().gvp_arm_destroy(self._handle)
+            self._handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def joint_double_integrator(nsteps: int, dt: float):
+    """Joint-space double integrator of the 7-DOF arm (the point_robot_lti
+    construction of dynamics.py:66-87 at 7 joints): state (q, q_dot), n = 14,
+    A = [[0, I], [0, 0]], a = 0, B = [0; I]."""
+    from .dynamics import LTVStep, LTVSystem
+
+    A = np.zeros((2 * NQ, 2 * NQ))
+    A[:NQ, NQ:] = np.eye(NQ)
+    B = np.zeros((2 * NQ, NQ))
+    B[NQ:, :] = np.eye(NQ)
+    step = LTVStep(A=A, a=np.zeros(2 * NQ), B=B)
+    return LTVSystem(steps=tuple([step] * (nsteps + 1)), dt=dt, n=2 * NQ, m=NQ)

@@ -15,6 +15,7 @@
 #include <vector>
 
 #include "gvp_internal.cuh"
+#include "wide_block.cuh"
 
 namespace gvp {
 namespace arm {
@@ -163,6 +164,156 @@ __global__ void __launch_bounds__(128) arm_factor_kernel(int64_t nfac, const dou
   }
 }
 
+// gaussian_sqrt (quadrature.py:164-181) of each factor's covariance, one warp
+// per factor: np.linalg.cholesky (lower triangle, no pivot floor), one
+// +1e-10 I retry; a failure of both is the eigh branch, reported (GVP_ERR_SQRT)
+__global__ void __launch_bounds__(128) arm_chol_kernel(int64_t nfac, const double* __restrict__ covs,
+                                                       double* __restrict__ chols, int* status, int* where) {
+  using WS = wide::WarpWs<16>;
+  constexpr int LD = WS::LD;
+  extern __shared__ __align__(16) double sm[];
+  const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t f = (int64_t)blockIdx.x * 4 + wid;
+  if (f >= nfac) return;
+  WS w(sm + wid * WS::DOUBLES);
+  const double* C = covs + f * NX * NX;
+  double pm = 1.0;
+  int pe = 0;
+  wide::stage<16>(w.T, NX, [&](int a, int b) { return C[a * NX + b]; });
+  bool ok = wide::chol<16, false, false>(w.T, w.L, NX, pm, pe);
+  if (!ok) {
+    wide::stage<16>(w.T, NX, [&](int a, int b) { return C[a * NX + b] + (a == b ? 1e-10 : 0.0); });
+    ok = wide::chol<16, false, false>(w.T, w.L, NX, pm, pe);
+  }
+  if (!ok) {
+    if (lane == 0) {
+      atomicMax(status, GVP_ERR_SQRT);
+      atomicMin(where, (int)f);
+    }
+    return;
+  }
+  for (int idx = lane; idx < NX * NX; idx += 32) {
+    const int a = idx / NX, b = idx - a * NX;
+    chols[f * NX * NX + idx] = b <= a ? w.L[a * LD + b] : 0.0;
+  }
+}
+
+// _moment_gradients (factors.py:95-104) from the factor's Cholesky root:
+// P = L^-T L^-1, g_mu = P e1, g_Sigma = sym(-1/2 P e0 + 1/2 P e2 P);
+// e_psi = max(e0, 0) (factors.py:218-224); non-finite moments -> GVP_ERR_NONFINITE
+__global__ void __launch_bounds__(128) arm_grads_kernel(int64_t nfac, const double* __restrict__ chols,
+                                                        const double* __restrict__ e0, const double* __restrict__ e1,
+                                                        const double* __restrict__ e2, double* __restrict__ epsi,
+                                                        double* __restrict__ gmu, double* __restrict__ gsig,
+                                                        int* status, int* where) {
+  using WS = wide::WarpWs<16>;
+  constexpr int LD = WS::LD;
+  extern __shared__ __align__(16) double sm[];
+  const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t f = (int64_t)blockIdx.x * 4 + wid;
+  if (f >= nfac) return;
+  WS w(sm + wid * WS::DOUBLES);
+  bool fin = isfinite(e0[f]);
+  for (int idx = lane; idx < NX * NX; idx += 32) fin = fin && isfinite(e2[f * NX * NX + idx]);
+  if (lane < NX) fin = fin && isfinite(e1[f * NX + lane]);
+  fin = __all_sync(0xffffffffu, fin);
+  if (!fin) {
+    if (lane == 0) {
+      atomicMax(status, GVP_ERR_NONFINITE);
+      atomicMin(where, (int)f);
+    }
+    return;
+  }
+  wide::stage<16>(w.L, NX, [&](int a, int b) { return chols[f * NX * NX + a * NX + b]; });
+  wide::trinv<16>(w.L, w.Li, NX);
+  wide::ltl<16>(w.Li, w.X, NX);                                                   // X = P
+  wide::stage<16>(w.U, NX, [&](int a, int b) { return e2[f * NX * NX + a * NX + b]; });  // U = e2
+  const int r = lane;
+  const double ee0 = e0[f];
+  // row r of (1/2 P) e2 -> T
+  double t[16];
+#pragma unroll
+  for (int c = 0; c < 16; ++c) {
+    double a = 0.0;
+    if (r < NX && c < NX) {
+#pragma unroll
+      for (int k = 0; k < NX; ++k) a += (0.5 * w.X[r * LD + k]) * w.U[k * LD + c];
+    }
+    t[c] = a;
+  }
+#pragma unroll
+  for (int c = 0; c < 16; ++c)
+    if (r < NX && c < NX) w.T[r * LD + c] = t[c];
+  __syncwarp();
+  // G = -1/2 P e0 + ((1/2 P) e2) P -> U (e2 no longer needed)
+#pragma unroll
+  for (int c = 0; c < 16; ++c) {
+    double a = 0.0;
+    if (r < NX && c < NX) {
+#pragma unroll
+      for (int k = 0; k < NX; ++k) a += w.T[r * LD + k] * w.X[k * LD + c];
+      a = (-0.5 * w.X[r * LD + c]) * ee0 + a;
+    }
+    t[c] = a;
+  }
+  __syncwarp();
+#pragma unroll
+  for (int c = 0; c < 16; ++c)
+    if (r < NX && c < NX) w.U[r * LD + c] = t[c];
+  __syncwarp();
+  if (r < NX) {
+    double g = 0.0;
+#pragma unroll
+    for (int k = 0; k < NX; ++k) g += w.X[r * LD + k] * e1[f * NX + k];
+    gmu[f * NX + r] = g;
+#pragma unroll
+    for (int c = 0; c < NX; ++c) gsig[(f * NX + r) * NX + c] = 0.5 * (w.U[r * LD + c] + w.U[c * LD + r]);
+  }
+  if (lane == 0) epsi[f] = ee0 > 0.0 ? ee0 : 0.0;
+}
+
+// device-resident arm collision model: grid (corner-packed), arm constants,
+// the rule's projection tables and per-call buffers (gvp_arm_create)
+struct ArmCtx {
+  Field field;
+  ArmConst A{};
+  double re = 0.0, so = 0.0;
+  int nproj = 0;
+  double *proj = nullptr, *mom = nullptr;
+  int* cnt = nullptr;
+  int64_t cap = 0;
+  double *means = nullptr, *covs = nullptr, *chols = nullptr, *e0 = nullptr, *e1 = nullptr, *e2 = nullptr,
+         *epsi = nullptr, *gmu = nullptr, *gsig = nullptr;
+  int* st = nullptr;
+  unsigned long long* oob = nullptr;
+  cudaStream_t s = nullptr;
+  ~ArmCtx() {
+    for (void* p : {(void*)proj, (void*)mom, (void*)cnt, (void*)means, (void*)covs, (void*)chols, (void*)e0,
+                    (void*)e1, (void*)e2, (void*)epsi, (void*)gmu, (void*)gsig, (void*)st, (void*)oob})
+      if (p) cudaFree(p);
+    if (s) cudaStreamDestroy(s);
+  }
+  int reserve(int64_t F) {
+    if (F <= cap) return GVP_OK;
+    for (double** p : {&means, &covs, &chols, &e0, &e1, &e2, &epsi, &gmu, &gsig}) {
+      if (*p) cudaFree(*p);
+      *p = nullptr;
+    }
+    const size_t v = F * NX * 8, m = F * NX * NX * 8, sc = F * 8;
+    GVP_CUDA(cudaMalloc(&means, v));
+    GVP_CUDA(cudaMalloc(&covs, m));
+    GVP_CUDA(cudaMalloc(&chols, m));
+    GVP_CUDA(cudaMalloc(&e0, sc));
+    GVP_CUDA(cudaMalloc(&e1, v));
+    GVP_CUDA(cudaMalloc(&e2, m));
+    GVP_CUDA(cudaMalloc(&epsi, sc));
+    GVP_CUDA(cudaMalloc(&gmu, v));
+    GVP_CUDA(cudaMalloc(&gsig, m));
+    cap = F;
+    return GVP_OK;
+  }
+};
+
 }  // namespace arm
 }  // namespace gvp
 
@@ -248,4 +399,111 @@ extern "C" int gvp_arm_factor_expectations(int64_t nfac, const double* means, co
   }
   for (void* p : bufs) cudaFree(p);
   return r;
+}
+
+// ---------------------------------------------------------------- arm model handle
+extern "C" int gvp_arm_create(gvp_arm** out, const double* grid, const int64_t* shape, const double* origin,
+                              double cell, const double* dh, const double* base, int32_t nspheres,
+                              const int32_t* sphere_link, const double* sphere_geom, double radius_eps,
+                              double sigma_obs, int32_t nproj, const double* proj, const double* mom,
+                              const int32_t* cnt) {
+  using namespace gvp::arm;
+  if (!out || nproj < 1 || nproj > kMaxProj || nspheres < 0 || nspheres > kMaxSpheres || !grid || !shape ||
+      !origin || !(cell > 0) || !dh || !base || !proj || !mom || !cnt) {
+    set_error("gvp_arm_create: bad argument");
+    return GVP_ERR_ARG;
+  }
+  for (int s = 0; s < nspheres; ++s)
+    if (sphere_link[s] < 0 || sphere_link[s] > NQ) return set_error("sphere_link must be in 0..7"), GVP_ERR_ARG;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+    set_error("no CUDA device visible");
+    return GVP_ERR_NO_DEVICE;
+  }
+  auto* c = new ArmCtx();
+  for (int j = 0; j < NQ; ++j)
+    for (int k = 0; k < 4; ++k) c->A.dh[j][k] = dh[j * 4 + k];
+  for (int k = 0; k < 3; ++k) c->A.base[k] = base[k];
+  c->A.nsph = nspheres;
+  for (int s = 0; s < nspheres; ++s) {
+    c->A.link[s] = sphere_link[s];
+    for (int k = 0; k < 4; ++k) c->A.geom[s][k] = sphere_geom[s * 4 + k];
+  }
+  c->re = radius_eps;
+  c->so = sigma_obs;
+  c->nproj = nproj;
+  int r = GVP_OK;
+  auto fail = [&](int code) {
+    delete c;
+    return code;
+  };
+  if (cudaStreamCreateWithFlags(&c->s, cudaStreamNonBlocking) != cudaSuccess) return fail(GVP_ERR_CUDA);
+  if ((r = c->field.build(grid, 3, shape, origin, cell, c->s))) return fail(r);
+  if (cudaMalloc(&c->proj, (size_t)nproj * NQ * 8) != cudaSuccess ||
+      cudaMalloc(&c->mom, (size_t)nproj * NM * 8) != cudaSuccess || cudaMalloc(&c->cnt, (size_t)nproj * 4) != cudaSuccess ||
+      cudaMalloc(&c->st, 8) != cudaSuccess || cudaMalloc(&c->oob, 8) != cudaSuccess) {
+    set_error("cudaMalloc failed");
+    return fail(GVP_ERR_CUDA);
+  }
+  cudaMemcpy(c->proj, proj, (size_t)nproj * NQ * 8, cudaMemcpyHostToDevice);
+  cudaMemcpy(c->mom, mom, (size_t)nproj * NM * 8, cudaMemcpyHostToDevice);
+  cudaMemcpy(c->cnt, cnt, (size_t)nproj * 4, cudaMemcpyHostToDevice);
+  *out = reinterpret_cast<gvp_arm*>(c);
+  return GVP_OK;
+}
+
+extern "C" void gvp_arm_destroy(gvp_arm* h) { delete reinterpret_cast<gvp::arm::ArmCtx*>(h); }
+
+// The factor stage of evaluate_all_factors (factors.py:167-225) for the arm:
+// per factor covariance -> gaussian_sqrt -> moments -> gradients, all on the
+// device. means (F,14), covs (F,14,14) of the factors' knots; out e_psi (F),
+// g_mu (F,14), g_sigma (F,14,14), oob. GVP_ERR_SQRT / GVP_ERR_NONFINITE with
+// *where = the factor's position in the batch.
+extern "C" int gvp_arm_factor_grads(gvp_arm* h, int64_t nfac, const double* means, const double* covs,
+                                    double* e_psi, double* g_mu, double* g_sigma, int64_t* oob, int64_t* where) {
+  using namespace gvp::arm;
+  auto* c = reinterpret_cast<ArmCtx*>(h);
+  if (!c || nfac < 0) return set_error("gvp_arm_factor_grads: bad argument"), GVP_ERR_ARG;
+  if (oob) *oob = 0;
+  if (where) *where = -1;
+  if (nfac == 0) return GVP_OK;
+  int r = c->reserve(nfac);
+  if (r) return r;
+  cudaStream_t s = c->s;
+  const size_t v = nfac * NX * 8, m = nfac * NX * NX * 8;
+  const int init[2] = {GVP_OK, 0x7fffffff};
+  GVP_CUDA(cudaMemcpyAsync(c->means, means, v, cudaMemcpyHostToDevice, s));
+  GVP_CUDA(cudaMemcpyAsync(c->covs, covs, m, cudaMemcpyHostToDevice, s));
+  GVP_CUDA(cudaMemcpyAsync(c->st, init, 8, cudaMemcpyHostToDevice, s));
+  GVP_CUDA(cudaMemsetAsync(c->oob, 0, 8, s));
+  const unsigned nb = (unsigned)((nfac + 3) / 4);
+  const size_t wbytes = 4 * gvp::wide::WarpWs<16>::DOUBLES * 8;
+  arm_chol_kernel<<<nb, 128, wbytes, s>>>(nfac, c->covs, c->chols, c->st, c->st + 1);
+  int hst[2];
+  GVP_CUDA(cudaMemcpyAsync(hst, c->st, 8, cudaMemcpyDeviceToHost, s));
+  GVP_CUDA(cudaStreamSynchronize(s));
+  if (hst[0] != GVP_OK) {
+    if (where) *where = hst[1];
+    set_error("covariance needs the eigendecomposition root");
+    return hst[0];
+  }
+  arm_factor_kernel<<<nb, 128, 0, s>>>(nfac, c->means, c->chols, c->nproj, c->proj, c->mom, c->cnt, c->field.dev,
+                                       c->A, c->re, c->so, c->e0, c->e1, c->e2, c->oob);
+  arm_grads_kernel<<<nb, 128, wbytes, s>>>(nfac, c->chols, c->e0, c->e1, c->e2, c->epsi, c->gmu, c->gsig, c->st,
+                                           c->st + 1);
+  GVP_CUDA(cudaGetLastError());
+  unsigned long long ho = 0;
+  GVP_CUDA(cudaMemcpyAsync(hst, c->st, 8, cudaMemcpyDeviceToHost, s));
+  GVP_CUDA(cudaMemcpyAsync(&ho, c->oob, 8, cudaMemcpyDeviceToHost, s));
+  GVP_CUDA(cudaMemcpyAsync(e_psi, c->epsi, nfac * 8, cudaMemcpyDeviceToHost, s));
+  GVP_CUDA(cudaMemcpyAsync(g_mu, c->gmu, v, cudaMemcpyDeviceToHost, s));
+  GVP_CUDA(cudaMemcpyAsync(g_sigma, c->gsig, m, cudaMemcpyDeviceToHost, s));
+  GVP_CUDA(cudaStreamSynchronize(s));
+  if (oob) *oob = (int64_t)ho;
+  if (hst[0] != GVP_OK) {
+    if (where) *where = hst[1];
+    set_error("non-finite expectation");
+    return hst[0];
+  }
+  return GVP_OK;
 }

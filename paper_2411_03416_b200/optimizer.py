@@ -262,15 +262,84 @@ def _raise_plan_status(status: int, where: int, cfg: OptimizerConfig):
         raise RuntimeError(f"plan failed with status {status}")
 
 
+def _run_pgvimp_host(prior: DiscretePrior, env, cfg: OptimizerConfig, t0: float) -> RunResult:
+    """Algorithm 1 (optimizer.py:299-401) as the reference's host loop, every
+    kernel on the GPU: for block sizes the fused engine does not cover (the
+    7-DOF arm's n = 14 runs on the wide-block chain kernels) and for the arm
+    environment. Per iteration: factor stage, device bisection
+    (select_step_size), factor stage of the accepted state, costs."""
+    from .arm import ArmEnvironment
+    from .factors import assemble_joint_gradients, evaluate_all_factors, interior_collision_maps
+
+    K, n = prior.nsteps + 1, prior.n
+    collision_tol = cfg.collision_tol if cfg.collision_tol is not None else 1e-4 * prior.nsteps
+    rule = smolyak_rule(cfg.k_q, n) if env is not None else None
+    maps = interior_collision_maps(K)
+
+    def factors(joint: JointGaussian, marg: ChainMarginals):
+        if isinstance(env, ArmEnvironment):
+            e_psi, g_mu, g_s = env.factor_gradients(joint.mean, np.stack(marg.covs), rule)
+            return [FactorGradient(e_psi=float(e), g_mu=gm, g_sigma=gs) for e, gm, gs in zip(e_psi, g_mu, g_s)]
+        return evaluate_all_factors(joint.mean, joint.prec, env.sdf, env.model, rule, threads=cfg.threads,
+                                    marginals=marg)
+
+    cur = initial_state(prior, cfg)
+    temp = cfg.temp_low
+    result = RunResult(final=cur, marginals=gbp_marginals(cur.prec))
+    prev_total = prev_temp = None
+    switched = False
+    cached = None
+    for it in range(1, cfg.max_iters + 1):
+        t_iter = time.perf_counter()
+        if env is not None:
+            fv = cached if cached is not None else factors(cur, result.marginals)
+            g_mu, g_sigma = assemble_joint_gradients(fv, maps, K, n)
+        else:
+            g_mu, g_sigma = np.zeros(K * n), BlockTridiagonalMatrix.zeros(K, n)
+        step = select_step_size(cur, prior, g_mu, g_sigma, cfg, temp)
+        nxt = step.next_state
+        nxt_f = factors(nxt, step.marginals) if env is not None else []
+        cached = nxt_f if env is not None else None
+        costs = cost_breakdown(nxt, prior, temp, marginals=step.marginals, factor_values=nxt_f)
+        mean_shift = float(np.linalg.norm(nxt.mean - cur.mean))
+        result.records.append({"type": "iter", "iter": it, "beta": step.beta, "temperature": temp,
+                               "prior_cost": costs.prior_cost, "collision_cost": costs.collision_cost,
+                               "entropy_cost": costs.entropy_cost, "total_cost": costs.total,
+                               "kl_step": step.kl, "mean_shift": mean_shift,
+                               "wall_time_ms": (time.perf_counter() - t_iter) * 1e3})
+        cur = nxt
+        result.final, result.marginals, result.iterations = cur, step.marginals, it
+        same_temp = prev_temp is not None and prev_temp == temp
+        total_change = abs(costs.total - prev_total) if prev_total is not None else np.inf
+        if same_temp and mean_shift < cfg.tol_mean and total_change < cfg.tol_cost:
+            result.converged = True
+            break
+        prev_total = costs.total if same_temp or prev_temp is None else None
+        prev_temp = temp
+        if not switched and costs.collision_cost < collision_tol and temp != cfg.temp_high:
+            temp = cfg.temp_high
+            switched = True
+            result.switch_iteration = it
+            prev_total = None
+    result.wall_time_ms = (time.perf_counter() - t0) * 1e3
+    return result
+
+
 def run_pgvimp(sys_ltv: LTVSystem, env: Environment | None, cfg: OptimizerConfig, x0, goal,
                q_c: float, sigma_b: float, prior: DiscretePrior | None = None,
                spec_lanes: int = 0) -> RunResult:
-    """Algorithm 1 (optimizer.py:299-401) on the GPU engine."""
+    """Algorithm 1 (optimizer.py:299-401) on the GPU engine (n in {2, 4, 6}
+    with a planar/volumetric SDF); other block sizes and the 7-DOF arm
+    environment run the reference's host loop over the device kernels."""
+    from .arm import ArmEnvironment
+
     cfg.validate()
     t0 = time.perf_counter()
     if prior is None:
         prior = assemble_prior(sys_ltv, x0, goal, q_c, sigma_b)
     K, n = prior.nsteps + 1, prior.n
+    if n not in (2, 4, 6) or isinstance(env, ArmEnvironment):
+        return _run_pgvimp_host(prior, env, cfg, t0)
     rule = smolyak_rule(cfg.k_q, n)
     sdf = env.sdf if env is not None else far_field()
     model = env.model if env is not None else CollisionModel(0.0, 1.0)

@@ -109,3 +109,75 @@ def test_arm_kernel_clear_of_obstacles_is_zero(gpu):
     e0, e1, e2, oob = P.arm_factor_expectations(means, chols, P.smolyak_rule(3, 14), sdf, arm,
                                                 P.CollisionModel(0.05, 10.0))
     assert np.all(e0 == 0) and np.all(e1 == 0) and np.all(e2 == 0)
+
+
+def _joint_factors(F, seed):
+    means, chols = _factors(F, seed)
+    K = F + 2
+    joint = np.zeros((K, 14))
+    joint[1:K - 1] = means
+    covs = np.stack([np.eye(14)] + [L @ L.T for L in chols] + [np.eye(14)])
+    return joint, covs
+
+
+@pytest.mark.gpu
+def test_arm_factor_gradients_match_oracle(gpu):
+    """gvp_arm_factor_grads (gaussian_sqrt -> moments -> _moment_gradients on
+    the device) against the oracle's factor stage."""
+    import paper_2411_03416_b200 as P
+
+    sdf, model = _scene(P)
+    arm = P.panda_like()
+    rule = P.smolyak_rule(3, 14)
+    env = P.ArmEnvironment(sdf, model, arm)
+    joint, covs = _joint_factors(6, 4)
+    e_psi, g_mu, g_s = env.factor_gradients(joint, covs, rule)
+    r_e, r_gm, r_gs, _ = AO.arm_evaluate_factors(joint, covs, rule.points, rule.weights, sdf.values, sdf.origin,
+                                                 sdf.cell_size, arm.dh, arm.base, arm.sphere_link, arm.geom,
+                                                 model.radius_eps, model.sigma_obs)
+    assert np.any(r_e > 0)
+    assert rel_err(e_psi, r_e) <= 1e-10
+    assert rel_err(g_mu, r_gm) <= 1e-9
+    assert rel_err(g_s, r_gs) <= 1e-9
+    env.close()
+
+
+@pytest.mark.gpu
+def test_arm_run_pgvimp_matches_oracle(gpu):
+    """C3 shape at a test size: the 7-DOF arm (n = 14) planned end to end on
+    the GPU (wide-block chain kernels + the arm factor stage) against the
+    oracle's run_pgvimp with the arm factor stage: identical beta sequence,
+    records within 1e-8 relative."""
+    import gvp_oracle as O
+    import paper_2411_03416_b200 as P
+
+    sdf, model = _scene(P)
+    arm = P.panda_like()
+    N, dt = 10, 0.1
+    x0 = np.zeros(14)
+    goal = np.concatenate([[0.9, 0.6, 0.0, -0.8, 0.0, 1.0, 0.0], np.zeros(7)])
+    cfg = P.OptimizerConfig(k_q=3, kl_bound=10.0, beta_max=0.5, max_iters=5)
+    env = P.ArmEnvironment(sdf, model, arm)
+    res = P.run_pgvimp(P.joint_double_integrator(N, dt), env, cfg, x0, goal, 1.0, 1e-3)
+    env.close()
+    rule = P.smolyak_rule(3, 14)
+    A = np.zeros((14, 14))
+    A[:7, 7:] = np.eye(7)
+    B = np.zeros((14, 7))
+    B[7:, :] = np.eye(7)
+    prior = O.assemble_prior([A] * (N + 1), [np.zeros(14)] * (N + 1), [B] * (N + 1), dt, x0, goal, 1.0, 1e-3)
+    fn = lambda m, c: AO.arm_evaluate_factors(m, c, rule.points, rule.weights, sdf.values, sdf.origin,  # noqa: E731
+                                              sdf.cell_size, arm.dh, arm.base, arm.sphere_link, arm.geom,
+                                              model.radius_eps, model.sigma_obs)
+    ref = O.run_pgvimp(prior, None, None, None, None, None, rule.points, rule.weights, kl_bound=cfg.kl_bound,
+                       beta_min=cfg.beta_min, beta_max=cfg.beta_max, temp_low=cfg.temp_low,
+                       temp_high=cfg.temp_high, collision_tol=cfg.collision_tol, max_iters=cfg.max_iters,
+                       tol_mean=cfg.tol_mean, tol_cost=cfg.tol_cost, init_cov_scale=cfg.init_cov_scale, x0=x0,
+                       goal=goal, factor_fn=fn)
+    assert res.iterations == ref["iterations"]
+    assert any(r["collision_cost"] > 0 for r in ref["records"])
+    for got, exp in zip(res.records, ref["records"]):
+        assert got["beta"] == exp["beta"]
+        for k in ("prior_cost", "collision_cost", "entropy_cost", "total_cost", "kl_step", "mean_shift"):
+            assert abs(got[k] - exp[k]) <= 1e-8 * max(1.0, abs(exp[k])), k
+    assert rel_err(res.final.mean, ref["mean"].reshape(-1)) <= 1e-8
