@@ -301,6 +301,7 @@ def main():
     ap.add_argument("--plans", type=int, default=4096, help="plans per GPU")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-c1", action="store_true")
+    ap.add_argument("--no-c3", action="store_true")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference_arm(args)
@@ -504,6 +505,26 @@ def main():
                                       "ms": min(runs), "ms_runs": runs, "iterations": r1.iterations,
                                       "converged": r1.converged, "reference_iterations": 94,
                                       "ms_per_iteration": min(runs) / max(r1.iterations, 1)}
+    # ---------------- C3 (7-DOF sphere arm, n = 14, N = 200): wall time per planner iteration, rank 0
+    if rank == 0 and not args.no_c3:
+        sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), "tools"))
+        from c3_run import c3_scene
+        sdf3, model3 = c3_scene()
+        env3 = P.ArmEnvironment(sdf3, model3, P.panda_like())
+        goal3 = np.concatenate([[0.9, 0.6, 0.0, -0.8, 0.0, 1.0, 0.0], np.zeros(7)])
+        sys3 = P.joint_double_integrator(200, 4.0 / 200)
+        pr3 = P.assemble_prior(sys3, np.zeros(14), goal3, 1.0, 1e-3)
+        cfg3 = P.OptimizerConfig(k_q=3, kl_bound=10.0, beta_max=0.5, max_iters=3)
+        P.run_pgvimp(sys3, env3, cfg3, np.zeros(14), goal3, 1.0, 1e-3, prior=pr3)  # warm
+        cfg3 = P.OptimizerConfig(k_q=3, kl_bound=10.0, beta_max=0.5, max_iters=20)
+        t0 = time.perf_counter()
+        r3 = P.run_pgvimp(sys3, env3, cfg3, np.zeros(14), goal3, 1.0, 1e-3, prior=pr3)
+        w3 = (time.perf_counter() - t0) * 1e3
+        env3.close()
+        result["c3"] = {"config": "C3: 7-DOF sphere arm (panda_like, 14 spheres), n=14, N=200, k_q=3 (421 points, "
+                                  "113 joint projections), 128^3 map, kl_bound=10, beta_max=0.5",
+                        "iterations": r3.iterations, "ms": w3, "ms_per_iteration": w3 / max(r3.iterations, 1),
+                        "path": "run_pgvimp host loop over the wide-block chain kernels + device arm factor stage"}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cb, err = cpu_baseline_reference(1)
         result["cpu_baseline"] = cb if cb else {"value": None, "error": err}

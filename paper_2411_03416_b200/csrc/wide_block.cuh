@@ -42,10 +42,21 @@ struct WarpWs {
 // dst[r][c] = f(r, c) for the n x n block, lanes over the flattened entries
 template <int NM, class F>
 GVP_DEV void stage(double* dst, int n, F f) {
-  constexpr int LD = Tile<NM>::LD;
-  for (int idx = lane(); idx < n * n; idx += 32) {
+  // all of a lane's loads are issued before its first shared store, so one
+  // block costs one global-memory latency, not NM*NM/32 of them
+  constexpr int LD = Tile<NM>::LD, IT = (NM * NM + 31) / 32;
+  double v[IT];
+#pragma unroll
+  for (int it = 0; it < IT; ++it) {
+    const int idx = lane() + 32 * it;
     const int r = idx / n, c = idx - r * n;
-    dst[r * LD + c] = f(r, c);
+    v[it] = idx < n * n ? f(r, c) : 0.0;
+  }
+#pragma unroll
+  for (int it = 0; it < IT; ++it) {
+    const int idx = lane() + 32 * it;
+    const int r = idx / n, c = idx - r * n;
+    if (idx < n * n) dst[r * LD + c] = v[it];
   }
   __syncwarp();
 }

@@ -298,6 +298,13 @@ GVP_DEV int chain_mean(const Src& src, int64_t K, int n, double* lg, double* zg,
   return -1;
 }
 
+// NM = 16 / 32: any n up to NM (runtime guards); other NM are exact-size
+// instantiations (n = NM at compile time: no guards, constant strides)
+template <int NM>
+GVP_DEV constexpr int exact_n(int n) {
+  return (NM == 16 || NM == 32) ? n : NM;
+}
+
 // ------------------------------------------------------------------ sources
 struct BtSrc {  // a stored block-tridiagonal matrix (+ rhs)
   View D, U, E;
@@ -334,9 +341,10 @@ struct NoTr {
 
 // ------------------------------------------------------------------ drop-in kernels (one warp per plan)
 template <int NM>
-__global__ void __launch_bounds__(32) marginals_kernel(int64_t K, int n, View D, View U, MutView cov, MutView cross,
+__global__ void __launch_bounds__(32) marginals_kernel(int64_t K, int n_in, View D, View U, MutView cov, MutView cross,
                                                        double* logdet, double* scratch, int* status, int* where) {
   extern __shared__ __align__(16) double sm[];
+  const int n = exact_n<NM>(n_in);
   WarpWs<NM> w(sm);
   const int64_t b = blockIdx.x;
   BtSrc src{D, U, View{nullptr, 0, 0, 0}, b, n};
@@ -351,9 +359,10 @@ __global__ void __launch_bounds__(32) marginals_kernel(int64_t K, int n, View D,
 }
 
 template <int NM>
-__global__ void __launch_bounds__(32) mean_solve_kernel(int64_t K, int n, View D, View U, View E, MutView x,
+__global__ void __launch_bounds__(32) mean_solve_kernel(int64_t K, int n_in, View D, View U, View E, MutView x,
                                                         double* scratch, int* status, int* where) {
   extern __shared__ __align__(16) double sm[];
+  const int n = exact_n<NM>(n_in);
   WarpWs<NM> w(sm);
   const int64_t b = blockIdx.x;
   BtSrc src{D, U, E, b, n};
@@ -371,10 +380,11 @@ __global__ void __launch_bounds__(32) mean_solve_kernel(int64_t K, int n, View D
 // W = L_{i-1}^-1 U_{i-1}; chol_spd without symmetrising (LAPACK reads the
 // lower triangle); log det = 2 sum log diag L
 template <int NM>
-__global__ void __launch_bounds__(32) logdet_kernel(int64_t K, int n, View D, View U, double* logdet, double* chols,
+__global__ void __launch_bounds__(32) logdet_kernel(int64_t K, int n_in, View D, View U, double* logdet, double* chols,
                                                     int* status, int* where) {
   constexpr int LD = Tile<NM>::LD;
   extern __shared__ __align__(16) double sm[];
+  const int n = exact_n<NM>(n_in);
   WarpWs<NM> w(sm);
   const int64_t b = blockIdx.x;
   const int r = lane();
@@ -491,11 +501,16 @@ struct ProbeSrcB {  // S = K / T + Lambda / beta; rhs = (-g / T + eta / T) + (La
   GVP_DEV double rhs(int64_t i, int r) const {
     const int n = a->n;
     double mv = 0.0;  // blocktri matvec of Lambda * (1/beta): D_i mu_i + U_i mu_{i+1} + U_{i-1}' mu_{i-1}
+#pragma unroll 8
     for (int q = 0; q < n; ++q) mv += (a->diag(b, i, r * n + q) * inv_b) * a->mean(b, i, q);
-    if (i + 1 < a->K)
+    if (i + 1 < a->K) {
+#pragma unroll 8
       for (int q = 0; q < n; ++q) mv += (a->off(b, i, r * n + q) * inv_b) * a->mean(b, i + 1, q);
-    if (i > 0)
+    }
+    if (i > 0) {
+#pragma unroll 8
       for (int q = 0; q < n; ++q) mv += (a->off(b, i - 1, q * n + r) * inv_b) * a->mean(b, i - 1, q);
+    }
     return ((-a->gmu(b, i, r)) / temp + a->info(b, i, r) / temp) + mv;
   }
 };
@@ -512,7 +527,7 @@ __global__ void __launch_bounds__(64 * W) step_kernel(const __grid_constant__ St
   extern __shared__ __align__(16) double sm[];
   const int tid = threadIdx.x, warp = tid >> 5, slot = warp >> 1, role = warp & 1;
   const int64_t b = blockIdx.x;
-  const int n = a.n;
+  const int n = exact_n<NM>(a.n);
   const int64_t K = a.K;
   WarpWs<NM> w(sm + warp * WarpWs<NM>::DOUBLES);
   double* tail = sm + 2 * W * WarpWs<NM>::DOUBLES;
@@ -638,6 +653,7 @@ int64_t wide_scratch_doubles(int nplans, int64_t K, int n) {
 
 template <class F>
 static int wide_dispatch(int n, F f) {
+  if (n == 14) return f(std::integral_constant<int, 14>{});  // the 7-DOF arm (q, q_dot)
   if (n >= 9 && n <= 16) return f(std::integral_constant<int, 16>{});
   if (n >= 17 && n <= 32) return f(std::integral_constant<int, 32>{});
   set_error("wide block kernels support 9 <= n <= 32");
