@@ -487,6 +487,7 @@ def main():
                     "what": "gvp_engine_load from pinned host + steps + records D2H, one C-ABI call chain"},
             "clocks": clk.summary(),
         }
+    eng.close()  # release the C5 batch before the single-plan (latency-bound) measurements
     # ---------------- time-to-converge of one plan (C1 pinned), rank 0
     if rank == 0 and not args.no_c1:
         sdf1 = P.rasterize([P.sdf.Disc(center=np.array([1.1, 0.55]), radius=0.45)], bounds=[[-2, 4], [-2, 4]],
@@ -530,7 +531,6 @@ def main():
         result["cpu_baseline"] = cb if cb else {"value": None, "error": err}
     if rank == 0:
         print(json.dumps(result))
-    eng.close()
     if world > 1:
         dist.destroy_process_group()
 
