@@ -628,19 +628,7 @@ extern "C" int gvp_engine_set_map_bank(gvp_engine* e, int32_t nmaps, const doubl
   GVP_CUDA(cudaMalloc(&raw, sizeof(double) * cells * nmaps));
   cudaError_t ce = cudaMemcpyAsync(raw, grids, sizeof(double) * cells * nmaps, cudaMemcpyHostToDevice, e->stream);
   // Lipschitz bound over every map of the bank (the factor kernel's clear-cloud shortcut)
-  double gx = 0.0, gy = 0.0, gz = 0.0;
-  bool finite = true;
-  for (int m = 0; m < nmaps; ++m)
-    for (int64_t iz = 0; iz < f.nz; ++iz)
-      for (int64_t iy = 0; iy < f.ny; ++iy)
-        for (int64_t ix = 0; ix < f.nx; ++ix) {
-          const double* g = grids + (size_t)m * cells + (iz * f.ny + iy) * f.nx + ix;
-          finite = finite && std::isfinite(g[0]);
-          if (ix + 1 < f.nx) gx = std::max(gx, std::fabs(g[1] - g[0]));
-          if (iy + 1 < f.ny) gy = std::max(gy, std::fabs(g[f.nx] - g[0]));
-          if (f.ndim == 3 && iz + 1 < f.nz) gz = std::max(gz, std::fabs(g[f.nx * f.ny] - g[0]));
-        }
-  const double lip = finite ? std::sqrt(gx * gx + gy * gy + gz * gz) / f.cell * (1.0 + 1e-12) : INFINITY;
+  const double lip = field_lipschitz(grids, nmaps, f.ndim, f.nx, f.ny, f.nz, f.cell);
   int r = ce == cudaSuccess ? install_bank(e, nmaps, raw, plan_map, lip) : GVP_ERR_CUDA;
   if (ce != cudaSuccess) set_error(cudaGetErrorString(ce));
   cudaStreamSynchronize(e->stream);

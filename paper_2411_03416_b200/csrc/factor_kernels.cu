@@ -29,6 +29,36 @@
 
 namespace gvp {
 
+// Inside a cell the x-derivative of the multilinear interpolant interpolates
+// the cell's x-edge differences, so |grad| <= sqrt(sum over axes of (max |edge
+// difference| on that axis)^2) / cell, exact in 2D where each component is
+// affine in the other coordinate; the maximum over cells is the Lipschitz
+// constant. An SDF gives ~1 (a global per-axis bound gives sqrt(2) in 2D).
+double field_lipschitz(const double* grids, int64_t nmaps, int ndim, int64_t nx, int64_t ny, int64_t nz,
+                       double cell) {
+  const int64_t sx = 1, sy = nx, sz = nx * ny, cells = nx * ny * nz;
+  for (int64_t i = 0; i < cells * nmaps; ++i)
+    if (!std::isfinite(grids[i])) return INFINITY;
+  const int64_t cz = ndim == 3 ? nz - 1 : 1;
+  const int nc = ndim == 3 ? 2 : 1;
+  double l2 = 0.0;
+  for (int64_t m = 0; m < nmaps; ++m)
+    for (int64_t iz = 0; iz < cz; ++iz)
+      for (int64_t iy = 0; iy + 1 < ny; ++iy)
+        for (int64_t ix = 0; ix + 1 < nx; ++ix) {
+          const double* g = grids + m * cells + iz * sz + iy * sy + ix;
+          double mx = 0.0, my = 0.0, mz = 0.0;
+          for (int c = 0; c < nc; ++c)
+            for (int r = 0; r < 2; ++r) {
+              mx = std::max(mx, std::fabs(g[c * sz + r * sy + sx] - g[c * sz + r * sy]));  // x-edges
+              my = std::max(my, std::fabs(g[c * sz + r * sx + sy] - g[c * sz + r * sx]));  // y-edges
+              if (ndim == 3) mz = std::max(mz, std::fabs(g[r * sx + c * sy + sz] - g[r * sx + c * sy]));
+            }
+          l2 = std::max(l2, mx * mx + my * my + mz * mz);
+        }
+  return std::sqrt(l2) / cell * (1.0 + 1e-12);
+}
+
 // ======================================================================= Field
 Field::~Field() {
   if (d_corners) cudaFree(d_corners);
@@ -54,20 +84,7 @@ int Field::build(const double* grid, int ndim, const int64_t* shape, const doubl
   f.oz = ndim == 3 ? origin[2] : 0.0;
   f.cell = cell;
   f.inv_cell = 1.0 / cell;
-  {  // Lipschitz bound of the multilinear interpolant: per axis max |adjacent difference| / cell
-    double gx = 0.0, gy = 0.0, gz = 0.0;
-    bool finite = true;
-    for (int64_t iz = 0; iz < f.nz; ++iz)
-      for (int64_t iy = 0; iy < f.ny; ++iy)
-        for (int64_t ix = 0; ix < f.nx; ++ix) {
-          const double* g = grid + (iz * f.ny + iy) * f.nx + ix;
-          finite = finite && std::isfinite(g[0]);
-          if (ix + 1 < f.nx) gx = std::max(gx, std::fabs(g[1] - g[0]));
-          if (iy + 1 < f.ny) gy = std::max(gy, std::fabs(g[f.nx] - g[0]));
-          if (ndim == 3 && iz + 1 < f.nz) gz = std::max(gz, std::fabs(g[f.nx * f.ny] - g[0]));
-        }
-    f.lip = finite ? std::sqrt(gx * gx + gy * gy + gz * gz) / cell * (1.0 + 1e-12) : INFINITY;
-  }
+  f.lip = field_lipschitz(grid, 1, ndim, f.nx, f.ny, f.nz, cell);
   std::vector<double> packed;
   if (ndim == 2) {
     // corner-packed cells: (iy, ix) -> {g[iy][ix], g[iy][ix+1], g[iy+1][ix], g[iy+1][ix+1]}
@@ -235,6 +252,48 @@ GVP_DEV double interp2(const FieldDev& F, double px, double py, bool& out) {
   r = fadd<EXACT>(r, fmul<EXACT>(fmul<EXACT>(b.x, gx), fy));
   r = fadd<EXACT>(r, fmul<EXACT>(fmul<EXACT>(b.y, fx), fy));
   return r;
+}
+
+// interp2 for a point the caller has proven strictly inside the grid (the
+// factor kernel's cloud test): no clamping or OOB flag, the cell index is a
+// truncation, and the bilinear form is three lerps
+GVP_DEV double interp2_in(const FieldDev& F, double px, double py) {
+  const double u = (px - F.ox) * F.inv_cell, v = (py - F.oy) * F.inv_cell;
+  const int ix = __double2int_rz(u), iy = __double2int_rz(v);
+  const double fx = u - (double)ix, fy = v - (double)iy;
+  const double2* c = reinterpret_cast<const double2*>(F.corners) + 2 * (size_t)(unsigned)(iy * (int)(F.nx - 1) + ix);
+  const double2 a = __ldg(c), b = __ldg(c + 1);
+  const double top = fma(fx, a.y - a.x, a.x), bot = fma(fx, b.y - b.x, b.x);
+  return fma(fy, bot - top, top);
+}
+
+// interp2<false> with 32-bit cell indices and the bilinear form as three lerps
+// (the engine's quadrature; ~30 fewer instructions per lookup). Same clamping
+// and out-of-bounds flag; the grid has < 2^31 cells.
+GVP_DEV double interp2_clamped(const FieldDev& F, double px, double py, bool& out) {
+  double u = (px - F.ox) * F.inv_cell, v = (py - F.oy) * F.inv_cell;
+  const double tx = (double)(F.nx - 1), ty = (double)(F.ny - 1);
+  out = (u < 0.0) || (u > tx) || (v < 0.0) || (v > ty);
+  u = fmin(fmax(u, 0.0), tx);
+  v = fmin(fmax(v, 0.0), ty);
+  const int ix = min(__double2int_rz(u), (int)F.nx - 2), iy = min(__double2int_rz(v), (int)F.ny - 2);
+  const double fx = u - (double)ix, fy = v - (double)iy;
+  const double2* c = reinterpret_cast<const double2*>(F.corners) + 2 * (size_t)(unsigned)(iy * (int)(F.nx - 1) + ix);
+  const double2 a = __ldg(c), b = __ldg(c + 1);
+  const double top = fma(fx, a.y - a.x, a.x), bot = fma(fx, b.y - b.x, b.x);
+  return fma(fy, bot - top, top);
+}
+
+// the out-of-bounds flag interp2_clamped / interp3<false> would raise at (px, py[, pz])
+template <int P>
+GVP_DEV bool outside_grid(const FieldDev& F, const double (&pos)[P]) {
+  const double u = (pos[0] - F.ox) * F.inv_cell, v = (pos[1] - F.oy) * F.inv_cell;
+  bool o = (u < 0.0) || (u > (double)(F.nx - 1)) || (v < 0.0) || (v > (double)(F.ny - 1));
+  if (P == 3) {
+    const double w = (pos[P - 1] - F.oz) * F.inv_cell;
+    o = o || (w < 0.0) || (w > (double)(F.nz - 1));
+  }
+  return o;
 }
 
 // trilinear (_kernels.pyx:48-90): two bilinear planes combined in z
@@ -439,40 +498,76 @@ factor_grads_kernel(int nplans, int64_t nfac, View mean, View covs, RuleDev R, F
     // rule tables live in the kernel's parameter space: every projection
     // coordinate and moment is a constant-bank operand of its DFMA (no loads),
     // the loop is fully unrolled and the accumulation is branch-free
-    // Provably clear: every sigma position lies within Rad = |L[:P,:P]|_F * max_j |xi_j[:P]| of
+    // Provably clear: every sigma position lies within Rad = |L[:P,:P]| * max_j |xi_j[:P]| of
     // mu[:P] and the interpolated field is F.lip-Lipschitz, so if d(mu) - lip * Rad exceeds
     // radius_eps (margin 1e-9 >> rounding) no point can hit; with the cloud inside the grid no
     // point is out of bounds either. One gather instead of NP — the same zeros as below.
-    if (F.lip < INFINITY) {
-      double fr = 0.0;
+    double fr = 0.0;
+    if (P == 2) {
+      // spectral norm of L[:2,:2]: |L_pp xi| <= sqrt(lambda_max(L_pp L_pp')) |xi|, and
+      // L_pp L_pp' = S[:2,:2] (the Cholesky's leading block), closed form; up to sqrt(2)
+      // tighter than the Frobenius bound for a round cloud. (1 + 1e-12) covers rounding.
+      const double a = S[0][0], c = S[1][1], h = 0.5 * (a - c);
+      fr = (0.5 * (a + c) + sqrt(h * h + S[1][0] * S[1][0])) * (1.0 + 1e-12);
+    } else {
 #pragma unroll
       for (int r = 0; r < P; ++r)
 #pragma unroll
         for (int k = 0; k <= r; ++k) fr += L[r][k] * L[r][k];
-      const double Rad = sqrt(fr) * R.proj_radius;
-      const double slack = 1e-9 * F.cell;
-      bool inside = (mu[0] - Rad > F.ox + slack) && (mu[0] + Rad < F.ox + (double)(F.nx - 1) * F.cell - slack) &&
-                    (mu[1] - Rad > F.oy + slack) && (mu[1] + Rad < F.oy + (double)(F.ny - 1) * F.cell - slack);
-      if (P == 3)
-        inside = inside && (mu[P - 1] - Rad > F.oz + slack) &&
-                 (mu[P - 1] + Rad < F.oz + (double)(F.nz - 1) * F.cell - slack);
-      if (inside) {
-        bool oc;
-        const double dc = (P == 2) ? interp2<false>(F, mu[0], mu[1], oc)
-                                   : interp3<false>(F, mu[0], mu[1], mu[P - 1], oc);
-        if (dc - F.lip * Rad - radius_eps > 1e-9) {
+    }
+    const double Rad = sqrt(fr) * R.proj_radius;
+    const double slack = 1e-9 * F.cell;
+    bool inside = (mu[0] - Rad > F.ox + slack) && (mu[0] + Rad < F.ox + (double)(F.nx - 1) * F.cell - slack) &&
+                  (mu[1] - Rad > F.oy + slack) && (mu[1] + Rad < F.oy + (double)(F.ny - 1) * F.cell - slack);
+    if (P == 3)
+      inside = inside && (mu[P - 1] - Rad > F.oz + slack) &&
+               (mu[P - 1] + Rad < F.oz + (double)(F.nz - 1) * F.cell - slack);
+    // The test also holds for clouds that leave the grid: every lookup clamps its point to the
+    // grid box (a 1-Lipschitz projection), so clamp(p_j) stays within Rad of clamp(mu) and
+    // the interpolant is lip-Lipschitz on the box. Only the OOB count then needs the points.
+    if (F.lip < INFINITY) {
+      bool oc;
+      const double dc = (P == 2) ? interp2_clamped(F, mu[0], mu[1], oc)
+                                 : interp3<false>(F, mu[0], mu[1], mu[P - 1], oc);
+      if (dc - F.lip * Rad - radius_eps > 1e-9) {
+        if (!inside) {  // bounds test of every projection, as the quadrature below does it
 #pragma unroll
-          for (int r = 0; r < N; ++r) out.g_mu.p[knot * out.g_mu.sk + b * out.g_mu.sp + r * out.g_mu.se] = 0.0;
+          for (int j = 0; j < NP; ++j) {
+            double pos[P];
 #pragma unroll
-          for (int k = 0; k < T; ++k)
-            out.g_diag.p[knot * out.g_diag.sk + b * out.g_diag.sp + k * out.g_diag.se] = 0.0;
-          out.e_psi(b, f, 0) = 0.0;
-          return;
+            for (int r = 0; r < P; ++r) {
+              double acc = 0.0;
+#pragma unroll
+              for (int k = 0; k <= r; ++k) acc += L[r][k] * RC.proj[j * P + k];
+              pos[r] = mu[r] + acc;
+            }
+            nout += outside_grid<P>(F, pos) ? (unsigned long long)RC.cnt[j] : 0ull;
+          }
+          if (nout) atomicAdd(out.oob + b, nout);
         }
+#pragma unroll
+        for (int r = 0; r < N; ++r) out.g_mu.p[knot * out.g_mu.sk + b * out.g_mu.sp + r * out.g_mu.se] = 0.0;
+#pragma unroll
+        for (int k = 0; k < T; ++k)
+          out.g_diag.p[knot * out.g_diag.sk + b * out.g_diag.sp + k * out.g_diag.se] = 0.0;
+        out.e_psi(b, f, 0) = 0.0;
+        return;
       }
     }
     double psi[NP];
     bool any_hit = false;
+    if (P == 2 && __all_sync(__activemask(), inside)) {
+      // the whole cloud is strictly inside the grid: no clamping, no OOB count (warp-uniform,
+      // so a warp never runs both loops)
+#pragma unroll
+      for (int j = 0; j < NP; ++j) {
+        const double px = mu[0] + L[0][0] * RC.proj[j * P];
+        const double py = mu[1] + (L[1][0] * RC.proj[j * P] + L[1][1] * RC.proj[j * P + 1]);
+        const double gap = radius_eps - interp2_in(F, px, py);
+        psi[j] = gap > 0.0 ? sigma_obs * gap * gap : 0.0;
+        any_hit = any_hit || (gap > 0.0);
+      }
+    } else {
 #pragma unroll
     for (int j = 0; j < NP; ++j) {
       double pos[P];
@@ -484,12 +579,13 @@ factor_grads_kernel(int nplans, int64_t nfac, View mean, View covs, RuleDev R, F
         pos[r] = mu[r] + acc;
       }
       bool o;
-      const double d = (P == 2) ? interp2<false>(F, pos[0], pos[1], o)
+      const double d = (P == 2) ? interp2_clamped(F, pos[0], pos[1], o)
                                 : interp3<false>(F, pos[0], pos[1], pos[P - 1], o);
       nout += o ? (unsigned long long)RC.cnt[j] : 0ull;
       const double gap = radius_eps - d;
       psi[j] = gap > 0.0 ? sigma_obs * gap * gap : 0.0;
       any_hit = any_hit || (gap > 0.0);
+    }
     }
     if (!any_hit) {  // clear of every obstacle: all moments, gradients and e_psi are zero
       if (nout) atomicAdd(out.oob + b, nout);
@@ -527,7 +623,7 @@ factor_grads_kernel(int nplans, int64_t nfac, View mean, View covs, RuleDev R, F
         for (int k = 0; k <= r; ++k) acc += L[r][k] * __ldg(R.proj + j * P + k);
         pos[r] = mu[r] + acc;
       }
-      dist[u] = (P == 2) ? interp2<false>(F, pos[0], pos[1], o[u])
+      dist[u] = (P == 2) ? interp2_clamped(F, pos[0], pos[1], o[u])
                          : interp3<false>(F, pos[0], pos[1], pos[P - 1], o[u]);
     }
 #pragma unroll

@@ -44,6 +44,11 @@ struct FieldDev {
 // corner-pack raw grids on the device (nmaps maps of the geometry in f) into dst
 int pack_field_maps(const FieldDev& f, int nmaps, const double* raw_dev, double* dst_dev, cudaStream_t s);
 int64_t packed_field_doubles(const FieldDev& f);
+// Lipschitz constant of the multilinear interpolant of nmaps row-major grids
+// (nz, ny, nx) with spacing cell (the clear-cloud shortcut of the factor
+// kernel); INFINITY if any node is non-finite
+double field_lipschitz(const double* grids, int64_t nmaps, int ndim, int64_t nx, int64_t ny, int64_t nz,
+                       double cell);
 // rasterize primitive unions on the device (sdf.py:134-185): per map m the
 // primitives [prim_off[m], prim_off[m+1]) of kinds (0 disc/sphere, 1 box) with
 // params [center(dim) | radius or halfextents(dim)] (2*dim doubles each);
