@@ -438,7 +438,19 @@ struct RuleConst {
   int cnt[NP];
 };
 
-template <int N, int P, bool GRID2D, int NP>
+// Moment entries that vanish for a rule symmetric under xi_k -> -xi_k in every non-position
+// coordinate k >= P (Smolyak/Gauss-Hermite rules are): within a group of points sharing one
+// position projection, sum w xi_k = 0 and sum w xi_r xi_c = 0 for r != c with max(r, c) >= P.
+// Packed lower index t = r(r+1)/2 + c. The grouped tables hold these as rounding residues
+// (<= 1.4e-16 at k_q = 3/5, n = 4/6); grads_impl checks them before SYM is chosen.
+__host__ __device__ constexpr bool sym_zero2(int r, int c, int P) { return r != c && (r >= P || c >= P); }
+__host__ __device__ constexpr bool sym_zero_tri(int t, int P) {
+  int r = 0;
+  while ((r + 1) * (r + 2) / 2 <= t) ++r;
+  return sym_zero2(r, t - r * (r + 1) / 2, P);
+}
+
+template <int N, int P, bool GRID2D, int NP, bool SYM>
 __global__ void __launch_bounds__(128, GVP_FACTOR_MINBLOCKS)
 factor_grads_kernel(int nplans, int64_t nfac, View mean, View covs, RuleDev R, FieldDev F,
                     double radius_eps, double sigma_obs, FactorOut out,
@@ -601,9 +613,11 @@ factor_grads_kernel(int nplans, int64_t nfac, View mean, View covs, RuleDev R, F
     for (int j = 0; j < NP; ++j) {
       e0 += psi[j] * RC.mom[j * M];
 #pragma unroll
-      for (int r = 0; r < N; ++r) E1[r] += psi[j] * RC.mom[j * M + 1 + r];
+      for (int r = 0; r < N; ++r)
+        if (!SYM || r < P) E1[r] += psi[j] * RC.mom[j * M + 1 + r];
 #pragma unroll
-      for (int k = 0; k < T; ++k) E2[k] += psi[j] * RC.mom[j * M + 1 + N + k];
+      for (int k = 0; k < T; ++k)
+        if (!SYM || !sym_zero_tri(k, P)) E2[k] += psi[j] * RC.mom[j * M + 1 + N + k];
     }
   } else {
   // projections in chunks of CH: all CH cell gathers are issued before any
@@ -664,7 +678,8 @@ factor_grads_kernel(int nplans, int64_t nfac, View mean, View covs, RuleDev R, F
   for (int r = 0; r < N; ++r) {
     double acc = 0.0;
 #pragma unroll
-    for (int k = r; k < N; ++k) acc += Li[k][r] * E1[k];
+    for (int k = r; k < N; ++k)
+      if (!SYM || k < P) acc += Li[k][r] * E1[k];
     out.g_mu.p[knot * out.g_mu.sk + b * out.g_mu.sp + r * out.g_mu.se] = acc;
   }
   // W = E2 L^{-1}  (E2 symmetric, packed)
@@ -675,7 +690,8 @@ factor_grads_kernel(int nplans, int64_t nfac, View mean, View covs, RuleDev R, F
     for (int c = 0; c < N; ++c) {
       double acc = 0.0;
 #pragma unroll
-      for (int k = c; k < N; ++k) acc += E2[r >= k ? tri_idx(r, k) : tri_idx(k, r)] * Li[k][c];
+      for (int k = c; k < N; ++k)
+        if (!SYM || !sym_zero2(r, k, P)) acc += E2[r >= k ? tri_idx(r, k) : tri_idx(k, r)] * Li[k][c];
       W[r][c] = acc;
     }
   const double h0 = -0.5 * e0;
@@ -704,6 +720,20 @@ static int grads_impl(int nplans, int64_t K, const View& mean, const View& covs,
   const int tpb = 128;
   constexpr int M = 1 + N + N * (N + 1) / 2;
   const Rule* host = static_cast<const Rule*>(R.host);
+  // SYM: the rule's grouped moments carry the sign symmetry of sym_zero_tri (residues at
+  // the rounding level only), so the kernel skips those products
+  bool sym = false;
+  if (host && (int64_t)host->h_mom.size() == R.nproj * M) {
+    double big = 0.0, odd = 0.0;
+    for (int64_t j = 0; j < R.nproj; ++j) {
+      const double* m = &host->h_mom[(size_t)(j * M)];
+      for (int t = 0; t < M; ++t) big = std::max(big, std::fabs(m[t]));
+      for (int r = P; r < N; ++r) odd = std::max(odd, std::fabs(m[1 + r]));
+      for (int t = 0; t < N * (N + 1) / 2; ++t)
+        if (sym_zero_tri(t, P)) odd = std::max(odd, std::fabs(m[1 + N + t]));
+    }
+    sym = odd <= 1e-15 * big;
+  }
   auto go = [&](auto np_tag) {
     constexpr int NPc = decltype(np_tag)::value;
     RuleConst<(NPc > 0 ? NPc : 1), P, M> rc{};
@@ -712,15 +742,25 @@ static int grads_impl(int nplans, int64_t K, const View& mean, const View& covs,
       std::memcpy(rc.mom, host->h_mom.data(), sizeof(rc.mom));
       std::memcpy(rc.cnt, host->h_cnt.data(), sizeof(rc.cnt));
     }
+    auto launch = [&](auto sym_tag) {
+      constexpr bool S = decltype(sym_tag)::value;
     if (nplans >= 64 && nfac <= 65535) {
       const dim3 grid((unsigned)((nplans + tpb - 1) / tpb), (unsigned)nfac);
-      factor_grads_kernel<N, P, true, NPc><<<grid, tpb, 0, s>>>(nplans, nfac, mean, covs, R, F, re,
-                                                                so, out, active, rc);
+      factor_grads_kernel<N, P, true, NPc, S><<<grid, tpb, 0, s>>>(nplans, nfac, mean, covs, R, F, re,
+                                                                   so, out, active, rc);
     } else {
       const int64_t total = nfac * nplans;
-      factor_grads_kernel<N, P, false, NPc><<<(unsigned)((total + tpb - 1) / tpb), tpb, 0, s>>>(
+      factor_grads_kernel<N, P, false, NPc, S><<<(unsigned)((total + tpb - 1) / tpb), tpb, 0, s>>>(
           nplans, nfac, mean, covs, R, F, re, so, out, active, rc);
     }
+    };
+    if constexpr (NPc > 0) {
+      if (sym) {
+        launch(std::true_type{});
+        return;
+      }
+    }
+    launch(std::false_type{});
   };
   // specialisations for the configurations of SURVEY §8d: 13 projections
   // (k_q = 3, P = 2) and 57 (k_q = 5, P = 2); anything else takes the loop
