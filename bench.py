@@ -439,9 +439,11 @@ def main():
         probe_kernel = "probe_split_kernel" if -(-B // P_cols) < 2 * 148 else "probe_fused_kernel"
         traffic = None
         tpath = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "ncu_traffic.json")
+        fac_traffic = None
         if os.path.exists(tpath):
             with open(tpath) as fh:
-                traffic = json.load(fh).get(probe_kernel)
+                tj = json.load(fh)
+            traffic, fac_traffic = tj.get(probe_kernel), tj.get("factor_grads_kernel")
         #  factor stage: 8 (n^2 + 3n + 1) = 232 B per factor
         fac_bytes = B * F * 232
         fac_ach = fac_bytes / (fac_ms / 1e3) / 1e9 if fac_ms > 0 else None
@@ -481,7 +483,8 @@ def main():
                                         "_pred_on.sum.peak_sustained) x 2 x sm_max_mhz (MEASURED_PEAKS.json)",
                          "factor_grads": {"bound": "hbm", "achieved": fac_ach, "peak": hbm, "unit": "GB/s",
                                           "frac": (fac_ach / hbm) if fac_ach else None,
-                                          "bytes_per_factor": 232}},
+                                          "bytes_per_factor": 232, "traffic": fac_traffic,
+                                          "traffic_unit": "bytes/launch (ncu dram read+write, C5 mid-run)"}},
             "e2e": {"value": e2e_value, "unit": "factor-evals/s", "h2d_bytes_per_step": h2d // max(args.steps, 1),
                     "d2h_bytes_per_step": d2h // max(args.steps, 1),
                     "what": "gvp_engine_load from pinned host + steps + records D2H, one C-ABI call chain"},
