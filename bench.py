@@ -184,112 +184,265 @@ def measured_peaks():
         return {"hbm_gbs": 6650.0, "fallback": True}
 
 
-def cpu_baseline_reference(steps_iters: int = 1):
-    """The reference (oracle/_ref, built from /root/reference sources) on one
-    C5 plan, single process, for `steps_iters` iterations of run_pgvimp
-    (threads=1). Returns factor evals/s and the sample description."""
-    ref = os.path.join(REPO, "oracle", "_ref")
-    code = f"""
-import sys, time, json, numpy as np
-sys.path.insert(0, {ref!r})
-import gvplan
-from gvplan.sdf import Box
-from gvplan import optimizer as O
-sdf = gvplan.rasterize([Box(center=np.array([5.0,1.2]), halfextents=np.array([0.3,3.4])),
-                        Box(center=np.array([5.0,8.8]), halfextents=np.array([0.3,3.4]))],
-                       bounds=[[-2,12],[-2,12]], cell_size=0.05)
-env = O.Environment(sdf=sdf, model=gvplan.CollisionModel(0.2, 8.0))
-rng = np.random.default_rng({SEED})
-goal = np.array([10.0,10.0,0,0]); goal[:2] += rng.uniform(-0.5,0.5,size=(1,2))[0]
-sys_ltv = gvplan.point_robot_lti(2)({N_INTERVALS}, {T_TOTAL}/{N_INTERVALS})
-prior = gvplan.assemble_prior(sys_ltv, np.zeros(4), goal, 1.0, 1e-3)
-cfg = gvplan.OptimizerConfig(k_q=3, kl_bound=10.0, beta_max=0.5, max_iters={steps_iters}, threads=1)
-t0 = time.perf_counter()
-res = gvplan.run_pgvimp(sys_ltv, env, cfg, np.zeros(4), goal, 1.0, 1e-3, prior=prior)
-dt = time.perf_counter() - t0
-print(json.dumps({{"seconds": dt, "iterations": res.iterations, "ext": gvplan.HAVE_EXTENSION}}))
-"""
-    env = dict(os.environ, OMP_NUM_THREADS="1", OPENBLAS_NUM_THREADS="1", MKL_NUM_THREADS="1")
-    out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env, timeout=900)
-    if out.returncode != 0:
-        return None, out.stderr[-500:]
-    r = json.loads(out.stdout.strip().splitlines()[-1])
-    # factor evals: the initial factor stage + one per iteration (optimizer.py:338-357)
-    evals = (N_INTERVALS - 1) * (r["iterations"] + 1)
-    return {"value": evals / r["seconds"], "unit": "factor-evals/s", "cores": 1, "kind": "reference",
-            "sample": f"1 C5 plan (N={N_INTERVALS}, k_q=3) x {r['iterations']} run_pgvimp iteration(s) "
-                      f"incl. initial marginals+factor stage, gvplan from oracle/_ref "
-                      f"(Cython kernel: {r['ext']}), threads=1, {r['seconds']:.2f} s"}, None
+def _ref_bench():
+    """oracle/ref_bench.py: the reference-side legs (cpu_baseline, --impl reference)."""
+    sys.path.insert(0, os.path.join(REPO, "oracle"))
+    import ref_bench
+
+    return ref_bench
+
+
+def fp64_peak():
+    """Measured fp64 FMA throughput (profiles/fp64_peak.txt, tools/micro/lat.cu
+    on the B200 box: 148 SMs x 64 DFMA/clk x 2 at 1965 MHz); falls back to the
+    ncu peak_sustained arithmetic at the recorded max SM clock."""
+    path = os.path.join(REPO, "profiles", "fp64_peak.txt")
+    try:
+        for line in open(path):
+            if line.startswith("DFMA throughput:"):
+                return float(line.split(":")[1].split()[0]), "measured (profiles/fp64_peak.txt, tools/micro/lat.cu)"
+    except OSError:
+        pass
+    mhz = float(measured_peaks().get("sm_max_mhz", 1965.0))
+    return 148 * 64 * 2 * mhz * 1e6 / 1e12, "derived: 148 SMs x 64 DFMA/clk x 2 x sm_max_mhz"
 
 
 def run_reference_arm(args):
-    """--impl reference: the reference's CPU implementation of the path on
-    all host cores (one plan per process), rank 0 only."""
+    """--impl reference: the reference's CPU implementation of the path on all
+    host cores, rank 0 only. One worker process per core, each owning one C5
+    plan; a step = one steady-state iteration of the
+    reference's own loop body on every plan (oracle/ref_bench.py), counted as
+    F = N - 1 factor-expectation evals per plan-iteration like the GPU arm."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    import multiprocessing as mp
-
-    lanes = len(os.sched_getaffinity(0))
-    total_steps = args.warmup + args.steps
-    ref = os.path.join(REPO, "oracle", "_ref")
-    if not os.path.isdir(os.path.join(ref, "gvplan")):
+    R = _ref_bench()
+    if not R.available():
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built (run oracle/build_ref.sh)"}))
         return
-    ctx = mp.get_context("spawn")
-    with ctx.Pool(lanes, initializer=_ref_worker_init, initargs=(ref,)) as pool:
-        pool.map(_ref_worker_warm, range(lanes))  # prior assembly per worker, untimed
-        times = []
-        evals = 0
-        for step in range(total_steps):
-            t0 = time.perf_counter()
-            res = pool.map(_ref_worker_step, [(step, w) for w in range(lanes)])
-            dt = time.perf_counter() - t0
-            if step >= args.warmup:
-                times.append(dt)
-                evals += sum(res)
-    wall = sum(times)
-    value = evals / wall
+    lanes = len(os.sched_getaffinity(0))
+    out = R.run_parallel(lanes, args.steps, args.warmup)
+    wall = sum(out["times"])
+    value = out["evals"] / wall
     line = {"metric": "factor-expectation evals/s", "value": value, "unit": "factor-evals/s",
             "impl": "reference", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": 1e3 * wall / len(times), "higher_is_better": True, "scaling": "weak",
+            "ms_per_step": 1e3 * wall / len(out["times"]), "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"C5 sample: {lanes} independent point2d plans (one per host core) x 1 "
-                                   f"run_pgvimp iteration per step, N={N_INTERVALS}, k_q=3, C2 map",
+            "config": {"workload": f"C5 sample: {lanes} independent point2d plans (one per host core, plans "
+                                   f"0..{lanes - 1} of the bench workload), N={N_INTERVALS}, k_q=3, C2 map; step = "
+                                   "one steady-state iteration of every plan",
                        "plans_per_step": lanes, "N": N_INTERVALS, "k_q": K_Q},
             "cpu_baseline": {"value": value, "unit": "factor-evals/s", "cores": lanes, "kind": "reference",
-                             "sample": f"{lanes} plans x 1 iteration per step, multiprocessing, gvplan from oracle/_ref"},
+                             "sample": f"{lanes} plans x 1 iteration per step, one process per plan, gvplan "
+                                       "from oracle/_ref (Cython kernel), steady state"},
             "e2e": {"value": value, "unit": "factor-evals/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line))
 
 
-_REF = {}
+def _spawn_ranks(args) -> int:
+    """--gpus N without a launcher: re-run this script under torch.distributed.run,
+    one rank per GPU (NCCL), rendezvous on 127.0.0.1."""
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    os.makedirs(os.path.join(REPO, "gpurun_out"), exist_ok=True)
+    env.setdefault("NCCL_DEBUG_FILE", os.path.join(REPO, "gpurun_out", "nccl.%h.%p.log"))
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.run(cmd, env=env).returncode
 
 
-def _ref_worker_init(ref):
-    os.environ["OMP_NUM_THREADS"] = "1"
-    sys.path.insert(0, ref)
+def time_to_converge(P, args, B, goals, prior, info, pmean, init, dev):
+    """C5: the whole 4096-plan batch from initial_state until every plan hit the
+    reference's termination (optimizer.py:386-392) or max_iters = 600;
+    C2: one plan (N = 500, k_q = 5) the same way. Wall clock around the calls,
+    inputs already resident / built (setup untimed)."""
+    import torch
+
+    from paper_2411_03416_b200.engine import to_plan_minor
+
+    K, n = N_INTERVALS + 1, 4
+    out = {}
+    eng = P.PlanBatch(B, K, n, c2_map(P), P.CollisionModel(0.2, 8.0), P.smolyak_rule(K_Q, n), c5_cfg(P, 600),
+                      shared_prior=True)
+    try:
+        t = [torch.from_numpy(np.ascontiguousarray(x)).to(dev) for x in
+             (prior.prec.diag_stack, prior.prec.off_stack, to_plan_minor(info), to_plan_minor(pmean),
+              to_plan_minor(init))]
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        eng.load_device(*[x.data_ptr() for x in t])
+        done = eng.run(check_every=25)
+        wall = (time.perf_counter() - t0) * 1e3
+        sm = eng.summary()
+    finally:
+        eng.close()
+    its = sm["iterations"].astype(np.int64)
+    conv = sm["converged"].astype(bool)
+    out["C5"] = {"config": f"C5: {B} plans, N={N_INTERVALS}, k_q=3, max_iters=600", "ms": wall,
+                 "iterations_launched": int(done), "converged_fraction": float(conv.mean()),
+                 "iterations_median": float(np.median(its)), "iterations_max": int(its.max()),
+                 "iterations_median_converged": float(np.median(its[conv])) if conv.any() else None,
+                 "failed": int((sm["status"] != 0).sum()),
+                 "ms_per_plan_amortized": wall / B}
+    sys2 = P.point_robot_lti(2)(500, 10.0 / 500)
+    env2 = P.Environment(c2_map(P), P.CollisionModel(0.2, 8.0))
+    g2 = np.array([10.0, 10.0, 0, 0])
+    pr2 = P.assemble_prior(sys2, np.zeros(4), g2, 1.0, 1e-3)
+    cfg2 = P.OptimizerConfig(k_q=5, kl_bound=10.0, beta_max=0.5, max_iters=600)
+    P.run_pgvimp(sys2, env2, P.OptimizerConfig(k_q=5, kl_bound=10.0, beta_max=0.5, max_iters=2), np.zeros(4), g2,
+                 1.0, 1e-3, prior=pr2)  # warm
+    t0 = time.perf_counter()
+    r2 = P.run_pgvimp(sys2, env2, cfg2, np.zeros(4), g2, 1.0, 1e-3, prior=pr2)
+    w2 = (time.perf_counter() - t0) * 1e3
+    out["C2"] = {"config": "C2: point2d N=500, k_q=5 (385 points), narrow gap, max_iters=600", "ms": w2,
+                 "iterations": r2.iterations, "converged": r2.converged, "ms_per_iteration": w2 / max(r2.iterations, 1),
+                 "reference_s_per_iteration_survey": 2.29}
+    return out
 
 
-def _ref_worker_warm(w):
-    import gvplan
-    from gvplan import optimizer as O
-    from gvplan.sdf import Box
-    sdf = gvplan.rasterize([Box(center=np.array([5.0, 1.2]), halfextents=np.array([0.3, 3.4])),
-                            Box(center=np.array([5.0, 8.8]), halfextents=np.array([0.3, 3.4]))],
-                           bounds=[[-2, 12], [-2, 12]], cell_size=0.05)
-    goal = c5_goals(w + 1)[w]
-    sys_ltv = gvplan.point_robot_lti(2)(N_INTERVALS, T_TOTAL / N_INTERVALS)
-    _REF.update(env=O.Environment(sdf=sdf, model=gvplan.CollisionModel(0.2, 8.0)), goal=goal, sys=sys_ltv,
-                prior=gvplan.assemble_prior(sys_ltv, np.zeros(4), goal, 1.0, 1e-3), gvplan=gvplan)
-    return w
+def c1_legs(P, args, world):
+    """C1 pinned plan: GPU run_pgvimp to convergence, the reference's own run on
+    this host (rank 0, N = 1 only), and the reference-format CSV rows
+    (bench.py:26: serial = reference CPU at 1 thread, parallel = this engine)."""
+    from paper_2411_03416_b200 import runio
+
+    sdf1 = P.rasterize([P.sdf.Disc(center=np.array([1.1, 0.55]), radius=0.45)], bounds=[[-2, 4], [-2, 4]],
+                       cell_size=0.05)
+    env1 = P.Environment(sdf1, P.CollisionModel(0.2, 8.0))
+    sys1 = P.point_robot_lti(2)(50, 3.0 / 50)
+    g1 = np.array([2.0, 1.5, 0, 0])
+    cfg1 = P.OptimizerConfig(k_q=3, kl_bound=10.0, beta_max=0.5, max_iters=600)
+    pr1 = P.assemble_prior(sys1, np.zeros(4), g1, 1.0, 1e-3)
+    P.run_pgvimp(sys1, env1, cfg1, np.zeros(4), g1, 1.0, 1e-3, prior=pr1)  # warm
+    runs = []
+    for _ in range(3):  # wall clock of the whole call (engine setup, iterations, fetch)
+        t0 = time.perf_counter()
+        r1 = P.run_pgvimp(sys1, env1, cfg1, np.zeros(4), g1, 1.0, 1e-3, prior=pr1)
+        runs.append((time.perf_counter() - t0) * 1e3)
+    ttc = {"config": "C1 pinned: point2d N=50, k_q=3, kl_bound=10, beta_max=0.5", "ms": min(runs), "ms_runs": runs,
+           "iterations": r1.iterations, "converged": r1.converged, "reference_iterations": 94,
+           "ms_per_iteration": min(runs) / max(r1.iterations, 1)}
+    # our factor stage / GBP marginals at C1 (median of 10 / 3, like the reference's bench_factors)
+    rule = P.smolyak_rule(3, 4)
+    st = P.optimizer.initial_state(pr1, cfg1)
+    marg = P.gbp_marginals(st.prec)
+
+    def med(fn, reps):
+        fn()
+        ts = []
+        for _ in range(reps):
+            t = time.perf_counter()
+            fn()
+            ts.append((time.perf_counter() - t) * 1e3)
+        return float(np.median(ts))
+
+    fac_ms = med(lambda: P.evaluate_all_factors(st.mean, st.prec, sdf1, env1.model, rule, marginals=marg), 10)
+    gbp_ms = med(lambda: P.gbp_marginals(pr1.prec), 3)
+    rows = []
+    R = _ref_bench()
+    if world == 1 and R.available():
+        try:
+            ref = R.c1_full(threads=1)
+        except Exception as exc:  # the reference leg is a reported baseline, not the product
+            ttc["reference"] = {"error": str(exc)[-300:]}
+        else:
+            ttc["reference"] = {"ms": ref["ms"], "iterations": ref["iterations"], "converged": ref["converged"],
+                                "threads": 1, "where": "this host, gvplan from oracle/_ref"}
+            rows = [runio.bench_row("factors", 50, 4, 3, ref["factor_stage_ms"], fac_ms),
+                    runio.bench_row("gbp", 50, 4, 0, ref["dense_inverse_ms"], gbp_ms),
+                    runio.bench_row("full", 50, 4, 3, ref["ms"], min(runs))]
+            if args.csv:
+                os.makedirs(os.path.dirname(os.path.abspath(args.csv)), exist_ok=True)
+                with open(args.csv, "w") as fh:
+                    fh.write(runio.rows_to_csv(rows))
+    return {"ttc": ttc, "rows": rows}
 
 
-def _ref_worker_step(arg):
-    g = _REF["gvplan"]
-    cfg = g.OptimizerConfig(k_q=K_Q, kl_bound=10.0, beta_max=0.5, max_iters=1, threads=1)
-    res = g.run_pgvimp(_REF["sys"], _REF["env"], cfg, np.zeros(4), _REF["goal"], 1.0, 1e-3, prior=_REF["prior"])
-    return (N_INTERVALS - 1) * res.iterations
+def cpu_baseline_leg():
+    """The reference on ONE host core: C5 plan 0 in steady state (oracle/ref_bench.py),
+    2 timed iterations after 1 warm-up (~15 s of CPU)."""
+    R = _ref_bench()
+    if not R.available():
+        return {"value": None, "error": "oracle/_ref not built"}
+    try:
+        r = R.cpu_baseline(iters=2, warm=1)
+    except Exception as exc:
+        return {"value": None, "error": str(exc)[-300:]}
+    return {"value": r["evals"] / r["seconds"], "unit": "factor-evals/s", "cores": 1, "kind": "reference",
+            "sample": f"1 C5 plan (N={N_INTERVALS}, k_q=3) x {r['iterations']} steady-state iterations of the "
+                      f"reference's loop body, gvplan from oracle/_ref (Cython kernel: {r['ext']}), threads=1, "
+                      f"{r['seconds']:.2f} s"}
+
+
+def timed_steps(eng, steps, F, sync, start, stop, dev=None, marks=None):
+    """The contract's timed region: barrier + synchronize on both sides, exactly
+    `steps` iterations of every plan on the rank, the rank's time from
+    start()/stop() (CUDA events on the engine stream), then the max over ranks
+    and the work (plan-iterations x F factor evals) summed over ranks."""
+    from paper_2411_03416_b200 import dist as D
+
+    it_before = eng.summary()["iterations"].astype(np.int64)
+    D.barrier()
+    sync()
+    if marks:
+        marks[0]()
+    start()
+    eng.step(steps)
+    ms = stop()
+    sync()
+    if marks:
+        marks[1]()
+    D.barrier()
+    it_after = eng.summary()["iterations"].astype(np.int64)
+    evals = float((it_after - it_before).sum() * F)
+    return {"ms": ms, "evals": evals, "it_after": it_after, "ms_max": D.reduce_max(ms, device=dev),
+            "evals_all": D.reduce_sum(evals, device=dev)}
+
+
+class StubBatch:
+    """--stub-engine: CPU stand-in with PlanBatch's step/summary surface, so the
+    launcher, sharding and cross-rank reductions run without a GPU (gloo)."""
+
+    def __init__(self, B):
+        self.iters = np.zeros(B, dtype=np.int32)
+
+    def step(self, k, sync=False):
+        time.sleep(0.005 * k)
+        self.iters += k
+
+    def summary(self):
+        return {"iterations": self.iters.copy()}
+
+
+def run_stub(args):
+    import torch.distributed as dist
+
+    from paper_2411_03416_b200.dist import shard
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    if world > 1:
+        dist.init_process_group("gloo")
+    lo, hi = shard(args.plans * world, world, rank)
+    eng = StubBatch(hi - lo)
+    eng.step(args.warmup)
+    t = {}
+    tr = timed_steps(eng, args.steps, N_INTERVALS - 1, lambda: None, lambda: t.setdefault("t0", time.perf_counter()),
+                     lambda: (time.perf_counter() - t["t0"]) * 1e3)
+    if rank == 0:
+        print(json.dumps({"metric": "factor-expectation evals/s", "value": tr["evals_all"] / (tr["ms_max"] / 1e3),
+                          "unit": "factor-evals/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+                          "ms_per_step": tr["ms_max"] / args.steps, "stub": True,
+                          "evals_all": tr["evals_all"], "plans_total": args.plans * world}))
+    if world > 1:
+        dist.destroy_process_group()
 
 
 def main():
@@ -302,9 +455,17 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-c1", action="store_true")
     ap.add_argument("--no-c3", action="store_true")
+    ap.add_argument("--stub-engine", action="store_true", help=argparse.SUPPRESS)  # CPU launcher test
+    ap.add_argument("--no-converge", action="store_true", help="skip the C5/C2 time-to-converge runs")
+    ap.add_argument("--csv", default=os.path.join(REPO, "gpurun_out", "bench.csv"),
+                    help="reference-format bench CSV rows (bench.py:26 header)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference_arm(args)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(_spawn_ranks(args))
+    if args.stub_engine:
+        return run_stub(args)
 
     import torch
     import torch.distributed as dist
@@ -312,6 +473,8 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}: launch one rank per GPU")
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
@@ -361,26 +524,19 @@ def main():
     # ---------------- timed region: K steps, inputs resident in HBM
     load_device()
     eng.step(args.warmup, sync=True)
-    it_before = eng.summary()["iterations"].astype(np.int64)
     launches_before = eng.launches()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clk:
-        barrier()
-        torch.cuda.synchronize()
-        clk.mark_start()
-        ev0.record(stream)
-        eng.step(args.steps)
+
+    def ev_stop():
         ev1.record(stream)
         ev1.synchronize()
-        torch.cuda.synchronize()
-        clk.mark_end()
-        barrier()
-    ms = ev0.elapsed_time(ev1)
+        return ev0.elapsed_time(ev1)
+
+    with ClockSampler(local) as clk:
+        tr = timed_steps(eng, args.steps, F, torch.cuda.synchronize, lambda: ev0.record(stream), ev_stop, dev,
+                         marks=(clk.mark_start, clk.mark_end))
     launches = eng.launches() - launches_before
-    it_after = eng.summary()["iterations"].astype(np.int64)
-    evals = float((it_after - it_before).sum() * F)
-    ms_max = max_over_ranks(ms)
-    evals_all = sum_over_ranks(evals)
+    it_after, ms_max, evals_all = tr["it_after"], tr["ms_max"], tr["evals_all"]
     value = evals_all / (ms_max / 1e3)
 
     # ---------------- per-kernel device times (events around each kernel) and
@@ -400,21 +556,24 @@ def main():
     h_kd, h_ko = pin(prior.prec.diag_stack), pin(prior.prec.off_stack)
     h_info, h_pm, h_m0 = pin(to_plan_minor(info)), pin(to_plan_minor(pmean)), pin(to_plan_minor(init))
     h_rec = torch.empty((max_iters, B, 8), dtype=torch.float64).pin_memory().numpy()
+    # the results a caller needs: records, final means and marginal covariances (packed)
+    h_mean = torch.empty((K, n, B), dtype=torch.float64).pin_memory().numpy()
+    h_cov = torch.empty((K, n * (n + 1) // 2, B), dtype=torch.float64).pin_memory().numpy()
     h2d = h_kd.nbytes + h_ko.nbytes + h_info.nbytes + h_pm.nbytes + h_m0.nbytes
     barrier()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     t_wall = time.perf_counter()
     e0.record(stream)
-    eng.load(h_kd, h_ko, info, pmean, init) if False else \
-        eng.lib.gvp_engine_load(eng.handle, _native.ptr(h_kd), _native.ptr(h_ko), _native.ptr(h_info),
-                                _native.ptr(h_pm), _native.ptr(h_m0))
+    eng.lib.gvp_engine_load(eng.handle, _native.ptr(h_kd), _native.ptr(h_ko), _native.ptr(h_info),
+                            _native.ptr(h_pm), _native.ptr(h_m0))
     eng.step(args.steps)
     eng.lib.gvp_engine_get_records(eng.handle, _native.ptr(h_rec))
+    eng.packed_into(mean=h_mean, covs=h_cov)
     e1.record(stream)
     e1.synchronize()
     e2e_ms = max_over_ranks(max(e0.elapsed_time(e1), (time.perf_counter() - t_wall) * 1e3))
-    d2h = h_rec.nbytes
+    d2h = h_rec.nbytes + h_mean.nbytes + h_cov.nbytes
     e2e_evals = sum_over_ranks(float(np.isfinite(h_rec[:, :, 0]).sum() * F))
     e2e_value = e2e_evals / (e2e_ms / 1e3)
 
@@ -429,8 +588,7 @@ def main():
         # on device) x knots x algorithmic flops per probe-knot / kernel time;
         # speculative probes that the reference would not make are not counted.
         fl = probe_flops_per_knot(n)
-        sm_mhz = float(peaks.get("sm_max_mhz", 1965.0))
-        fp64_peak = 148 * 64 * 2 * sm_mhz * 1e6 / 1e12  # 64 DFMA/clk/SM (ncu peak_sustained)
+        fp64_pk, fp64_src = fp64_peak()
         bis_flops = probes / steps_prof * K * fl["total"]
         ach = bis_flops / (bis_ms / 1e3) / 1e12
         # the engine runs the split probe kernel while the grid is below 2 CTAs per SM
@@ -473,42 +631,30 @@ def main():
             "kernel_ms_per_step": {"bisection": bis_ms, "commit": com_ms, "factor_grads": fac_ms,
                                    "control": ctl_ms},
             "roofline": {"kernel": f"bisection ({probe_kernel})", "bound": "fp64", "achieved": ach,
-                         "peak": fp64_peak, "unit": "TFLOP/s", "frac": ach / fp64_peak, "traffic": traffic,
+                         "peak": fp64_pk, "unit": "TFLOP/s", "frac": ach / fp64_pk, "traffic": traffic,
                          "traffic_unit": "bytes/launch (ncu dram read+write)",
                          "flops_per_probe_knot": fl["total"], "probes_per_plan_iter": probes / max(1, B * steps_prof),
                          "lanes_per_plan": lanes,
                          "plans_per_cta": (min(P_cols, max(2, -(-(-(-B // 296)) // 2) * 2))
                                            if probe_kernel == "probe_split_kernel" else P_cols),
-                         "peak_source": "148 SMs x 64 DFMA/clk (ncu sm__sass_thread_inst_executed_op_dfma"
-                                        "_pred_on.sum.peak_sustained) x 2 x sm_max_mhz (MEASURED_PEAKS.json)",
+                         "peak_source": fp64_src,
                          "factor_grads": {"bound": "hbm", "achieved": fac_ach, "peak": hbm, "unit": "GB/s",
                                           "frac": (fac_ach / hbm) if fac_ach else None,
                                           "bytes_per_factor": 232, "traffic": fac_traffic,
                                           "traffic_unit": "bytes/launch (ncu dram read+write, C5 mid-run)"}},
             "e2e": {"value": e2e_value, "unit": "factor-evals/s", "h2d_bytes_per_step": h2d // max(args.steps, 1),
                     "d2h_bytes_per_step": d2h // max(args.steps, 1),
-                    "what": "gvp_engine_load from pinned host + steps + records D2H, one C-ABI call chain"},
+                    "what": "gvp_engine_load from pinned host + steps + D2H of the records, final means and packed marginal covariances, one C-ABI call chain"},
             "clocks": clk.summary(),
         }
-    eng.close()  # release the C5 batch before the single-plan (latency-bound) measurements
-    # ---------------- time-to-converge of one plan (C1 pinned), rank 0
+    eng.close()  # release the timed batch
+    # ---------------- time-to-converge (optimizer.py:386-392 termination), rank 0
+    if rank == 0 and not args.no_converge:
+        result["time_to_converge"] = time_to_converge(P, args, B, goals, prior, info, pmean, init, dev)
     if rank == 0 and not args.no_c1:
-        sdf1 = P.rasterize([P.sdf.Disc(center=np.array([1.1, 0.55]), radius=0.45)], bounds=[[-2, 4], [-2, 4]],
-                           cell_size=0.05)
-        env1 = P.Environment(sdf1, P.CollisionModel(0.2, 8.0))
-        sys1 = P.point_robot_lti(2)(50, 3.0 / 50)
-        cfg1 = P.OptimizerConfig(k_q=3, kl_bound=10.0, beta_max=0.5, max_iters=600)
-        pr1 = P.assemble_prior(sys1, np.zeros(4), np.array([2.0, 1.5, 0, 0]), 1.0, 1e-3)
-        P.run_pgvimp(sys1, env1, cfg1, np.zeros(4), np.array([2.0, 1.5, 0, 0]), 1.0, 1e-3, prior=pr1)  # warm
-        runs = []
-        for _ in range(3):  # wall clock of the whole call (engine setup, 94 iterations, fetch)
-            t0 = time.perf_counter()
-            r1 = P.run_pgvimp(sys1, env1, cfg1, np.zeros(4), np.array([2.0, 1.5, 0, 0]), 1.0, 1e-3, prior=pr1)
-            runs.append((time.perf_counter() - t0) * 1e3)
-        result["time_to_converge"] = {"config": "C1 pinned: point2d N=50, k_q=3, kl_bound=10, beta_max=0.5",
-                                      "ms": min(runs), "ms_runs": runs, "iterations": r1.iterations,
-                                      "converged": r1.converged, "reference_iterations": 94,
-                                      "ms_per_iteration": min(runs) / max(r1.iterations, 1)}
+        c1 = c1_legs(P, args, world)
+        result.setdefault("time_to_converge", {})["C1"] = c1["ttc"]
+        result["bench_csv"] = c1["rows"]
     # ---------------- C3 (7-DOF sphere arm, n = 14, N = 200): wall time per planner iteration, rank 0
     if rank == 0 and not args.no_c3:
         sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), "tools"))
@@ -530,8 +676,7 @@ def main():
                         "iterations": r3.iterations, "ms": w3, "ms_per_iteration": w3 / max(r3.iterations, 1),
                         "path": "run_pgvimp host loop over the wide-block chain kernels + device arm factor stage"}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cb, err = cpu_baseline_reference(1)
-        result["cpu_baseline"] = cb if cb else {"value": None, "error": err}
+        result["cpu_baseline"] = cpu_baseline_leg()
     if rank == 0:
         print(json.dumps(result))
     if world > 1:

@@ -201,6 +201,11 @@ int gvp_engine_active(gvp_engine* e, int32_t* nactive);
  * covs like diag; crosses like off; any pointer may be NULL. */
 int gvp_engine_get_state(gvp_engine* e, double* mean, double* diag, double* off, double* covs,
                          double* crosses);
+/* The same results without the host-side unpacking, straight into caller
+ * (ideally pinned) buffers: mean (nknots, n, nplans) and the marginal
+ * covariances packed lower-symmetric (nknots, n(n+1)/2, nplans), entry
+ * r(r+1)/2 + c holding Sigma_ii[r][c], c <= r. Either pointer may be NULL. */
+int gvp_engine_get_packed(gvp_engine* e, double* mean, double* covs_packed);
 /* Per-plan summary: converged, iterations, switch_iteration (-1 = none),
  * status, where (each int32[B]). */
 int gvp_engine_get_summary(gvp_engine* e, int32_t* converged, int32_t* iterations,
@@ -237,6 +242,15 @@ int gvp_rasterize(int32_t dim, const int64_t* counts, const double* origin, doub
  * max_probes each. Enable before the first step. */
 int gvp_engine_trace_probes(gvp_engine* e, int32_t max_probes);
 int gvp_engine_get_probes(gvp_engine* e, double* log, int32_t* counts);
+/* One iteration (synchronous) in which every plan with a finite beta[b]
+ * (host, nplans entries; NaN = searched) takes that step size instead of the
+ * searched one: proximal_update at a given beta (optimizer.py:129-161) inside
+ * the engine. The search still runs and is traced, so a known step sequence
+ * (e.g. the reference's) can be replayed while each search is compared. */
+int gvp_engine_step_beta(gvp_engine* e, const double* beta);
+/* Per-plan count (int64[nplans]) of sigma points clamped at the SDF border
+ * over every factor stage so far (sdf.py:53-56 note_oob). */
+int gvp_engine_get_oob(gvp_engine* e, int64_t* oob);
 
 /* ------------------------------------------------ iP-GVIMP on the device */
 /* Statistical linearisation of the planar quadrotor (slr.py:69-92) for B

@@ -30,5 +30,10 @@ rm -rf "$OUT"
 mkdir -p "$OUT"
 cp -r "$SCRATCH/src/gvplan" "$OUT/gvplan"
 rm -rf "$OUT/gvplan/__pycache__" "$OUT/gvplan"/*.c "$OUT/gvplan"/*.pyx
+# the reference's own test suite, unmodified, so tools/run_reference_suite.py
+# can run it against paper_2411_03416_b200 on the GPU box (git-ignored like
+# the rest of oracle/_ref)
+cp -r "$REF/tests" "$OUT/tests"
+rm -rf "$OUT/tests/__pycache__"
 echo "built reference into $OUT:"
-ls "$OUT/gvplan"
+ls "$OUT/gvplan" "$OUT/tests"

@@ -791,11 +791,14 @@ extern "C" int gvp_select_step_size(const double* mean, const double* diag, cons
     GVP_TRY(h2d(scal, nan2, 2, s));
     GVP_CUDA(cudaStreamSynchronize(s));
   }
-  // rhs piece Lambda mu, and log det of the current precision from the same
-  // backward Schur pivots the probes use (consistent KL)
+  // rhs piece Lambda mu; the current precision's SPD check (backward sweep) and
+  // its log det by the probes' own forward Schur recursion (kl_joint's
+  // logdet_cur: the KL is the difference of two nearby log dets, so both come
+  // from the same recursion)
   GVP_TRY(launch_lam_mu(2, K, n, 2, ld, lo, mu, v, s));
   GVP_TRY(launch_marginals_packed(1, K, n, 2, ld, lo, ocov, ocr, scal + 10, st, st + 1, scr,
                                   nullptr, s));
+  GVP_TRY(launch_logdet_fwd_packed(1, K, n, 2, ld, lo, scal + 10, nullptr, st, st + 1, s));
   int64_t w0 = -1;
   if (fetch_status(C, st, &w0) != GVP_OK) {
     if (where) *where = w0;
@@ -813,6 +816,7 @@ extern "C" int gvp_select_step_size(const double* mean, const double* diag, cons
   q.status = st; q.where = st + 2;
   q.probe_log = probe_log ? plog : nullptr; q.max_probes = max_probes; q.nprobes = st + 4;
   q.scratch = scr; q.active = nullptr;
+  q.search_kl = true; q.fixkl = nullptr;  // step.kl: the accepted probe's KL
   GVP_TRY(launch_select_step_v2(q, s));
   int stv[5];
   GVP_TRY(d2h(stv, st, 5, s));

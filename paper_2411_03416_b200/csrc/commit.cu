@@ -76,6 +76,11 @@ struct Args {
   int *status, *where;
   double* scratch;
   const int* active;
+  // search_kl: the search already wrote the accepted probe's KL and forward
+  // log det (step.kl, optimizer.py:209-211); the commit writes its own only
+  // where fixkl[b] != 0 (a step size that was not probed, gvp_engine_step_beta)
+  int search_kl;
+  const int* fixkl;
 };
 
 template <int N>
@@ -495,8 +500,10 @@ __global__ void __launch_bounds__(128, 1) commit_kernel(const __grid_constant__ 
       const double mh = xch[2 * 32 + p], sh2 = xch[3 * 32 + p];
       const double tr = xch[4 * 32 + p], ptr = xch[5 * 32 + p], pq = xch[6 * 32 + p];
       const double x = 0.5 * ((((tr + mh) - (double)(K * N)) + ld) - ldc);
-      a.kl[b] = (0.0 > x) ? 0.0 : x;  // python max(x, 0.0): NaN stays NaN
-      a.ld_next[b] = ld;
+      if (!a.search_kl || (a.fixkl && a.fixkl[b])) {
+        a.kl[b] = (0.0 > x) ? 0.0 : x;  // python max(x, 0.0): NaN stays NaN
+        a.ld_next[b] = ld;
+      }
       a.shift[b] = sqrt(sh2);
       if (a.prior_cost) a.prior_cost[b] = 0.5 * pq + 0.5 * ptr;
     }
@@ -533,6 +540,8 @@ int launch_commit_split(const V2Launch& q, cudaStream_t s) {
   a.status = q.status; a.where = q.where;
   a.scratch = q.scratch;
   a.active = q.active;
+  a.search_kl = q.search_kl ? 1 : 0;
+  a.fixkl = q.fixkl;
   const unsigned grid = (unsigned)((q.nplans + 31) / 32);
 #define GVP_V5_KS(NN, KK)                                                                              \
   {                                                                                                    \

@@ -31,8 +31,11 @@ namespace {
 constexpr double kLog2Pi = 1.8378770664093453;  // log(2 pi), optimizer.py:38
 
 struct PlanState {
-  double *temp, *logdet, *beta, *kl, *shift, *prior_cost, *prev_total, *prev_temp, *total;
+  // logdet: forward-Schur log det of the current precision (the probes' ld_cur);
+  // logdet_next: the accepted state's, written by the search (or the commit)
+  double *temp, *logdet, *beta, *kl, *shift, *prior_cost, *prev_total, *prev_temp, *total, *logdet_next;
   int *active, *status, *where, *converged, *iters, *switch_it, *switched, *fstatus, *fwhere;
+  int* fixkl;  // gvp_engine_step_beta: the pinned beta was not probed (commit supplies KL / log det)
   unsigned long long* oob;
   int* nactive;
 };
@@ -54,6 +57,8 @@ __global__ void init_plans_kernel(int B, PlanState ps, double temp_low) {
   ps.fstatus[b] = 0;
   ps.fwhere[b] = INT_MAX;
   ps.oob[b] = 0;
+  ps.fixkl[b] = 0;
+  ps.logdet_next[b] = NAN;
 }
 
 // full (K, n, n, sw) -> packed (K, T, dw) times `scale`; a shared prior
@@ -94,6 +99,8 @@ __global__ void control_kernel(int B, int64_t F, int n64dim, const double* __res
     return;
   }
   const int it = ps.iters[b] + 1;
+  const double ld_new = ps.logdet_next[b];
+  ps.logdet[b] = ld_new;  // the accepted state becomes the current one
   double coll = 0.0;  // sum(f.e_psi), ascending factor order (optimizer.py:274)
   {
     // the loads of a chunk are all in flight before its (sequential, in order) adds
@@ -110,7 +117,7 @@ __global__ void control_kernel(int B, int64_t F, int n64dim, const double* __res
   }
   const double temp = ps.temp[b];
   const double dim = (double)n64dim;
-  const double entropy = 0.5 * (dim * (kLog2Pi + 1.0) - ps.logdet[b]);  // optimizer.py:234-235
+  const double entropy = 0.5 * (dim * (kLog2Pi + 1.0) - ld_new);  // optimizer.py:234-235
   const double ent_cost = -temp * entropy;
   const double prior = ps.prior_cost[b];
   const double total = prior + coll + ent_cost;
@@ -153,6 +160,26 @@ __global__ void fill_kernel(double* p, int64_t count, double v) {
   if (t < count) p[t] = v;
 }
 
+// plans with a finite entry take that step size instead of the searched one;
+// fixkl marks those whose pinned step the search did not accept (its KL and
+// log det then come from the commit and the forward log det kernel)
+__global__ void pin_beta_kernel(int B, const double* __restrict__ pinned, const int* __restrict__ active,
+                                double* __restrict__ beta, int* __restrict__ status, int* __restrict__ where,
+                                int* __restrict__ fixkl) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= B || !active[b]) return;
+  const double v = pinned[b];
+  fixkl[b] = 0;
+  if (isfinite(v)) {
+    fixkl[b] = (status[b] != GVP_OK || beta[b] != v) ? 1 : 0;
+    beta[b] = v;
+    if (status[b] == GVP_ERR_NO_FEASIBLE_STEP) {  // the search found nothing; the pinned step is taken anyway
+      status[b] = GVP_OK;
+      where[b] = -1;
+    }
+  }
+}
+
 __global__ void count_active_kernel(int B, const int* active, int* out) {
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b < B && active[b]) atomicAdd(out, 1);
@@ -188,6 +215,7 @@ struct gvp_engine {
   // optional per-iteration probe trace (the reference's select_step trace)
   double* plog = nullptr;
   int* pcount = nullptr;
+  double* pinned = nullptr;  // gvp_engine_step_beta: per-plan step sizes (NaN = searched)
   int max_probes = 0;
   int iters_launched = 0;
   int64_t launches = 0;
@@ -229,9 +257,10 @@ struct gvp_engine {
     q.g = gmu; q.eta = info; q.v = v; q.mu = mean; q.pmean = pmean;
     q.kshared = shared_prior;
     q.o_mu = mean; q.o_ld = diag; q.o_lo = off; q.o_cov = covs; q.o_cr = crosses; q.o_v = v;
-    q.beta = ps.beta; q.kl = ps.kl; q.ld_next = ps.logdet; q.shift = ps.shift;
+    q.beta = ps.beta; q.kl = ps.kl; q.ld_next = ps.logdet_next; q.shift = ps.shift;
     q.prior_cost = ps.prior_cost;
     q.temp = ps.temp; q.ld_cur = ps.logdet;
+    q.search_kl = true; q.fixkl = ps.fixkl;
     q.kl_bound = cfg.kl_bound; q.beta_min = cfg.beta_min; q.beta_max = cfg.beta_max;
     q.status = ps.status; q.where = ps.where;
     q.probe_log = plog; q.max_probes = max_probes; q.nprobes = pcount;
@@ -340,17 +369,18 @@ extern "C" int gvp_engine_create(gvp_engine** out, int32_t nplans, int64_t nknot
       (r = e->alloc(&e->epsi, std::max<int64_t>(K - 2, 1) * B)) ||
       (r = e->alloc(&e->kfull_d, K * N2 * kb)) || (r = e->alloc(&e->scratch, (size_t)scr)) ||
       (r = e->alloc(&e->records, (size_t)cfg->max_iters * B * GVP_NREC)) ||
-      (r = e->alloc(&e->scal, 9 * B)) || (r = e->alloc(&e->ints, 10 * B + 1)) ||
+      (r = e->alloc(&e->scal, 10 * B)) || (r = e->alloc(&e->ints, 10 * B + 1)) ||
       (r = e->alloc(&e->oob, B)))
     return fail(r);
   PlanState& ps = e->ps;
   double* s = e->scal;
   ps.temp = s; ps.logdet = s + B; ps.beta = s + 2 * B; ps.kl = s + 3 * B; ps.shift = s + 4 * B;
   ps.prior_cost = s + 5 * B; ps.prev_total = s + 6 * B; ps.prev_temp = s + 7 * B; ps.total = s + 8 * B;
+  ps.logdet_next = s + 9 * B;
   int* q = e->ints;
   ps.active = q; ps.status = q + B; ps.where = q + 2 * B; ps.converged = q + 3 * B;
   ps.iters = q + 4 * B; ps.switch_it = q + 5 * B; ps.switched = q + 6 * B; ps.fstatus = q + 7 * B;
-  ps.fwhere = q + 8 * B; ps.nactive = q + 10 * B;
+  ps.fwhere = q + 8 * B; ps.fixkl = q + 9 * B; ps.nactive = q + 10 * B;
   ps.oob = e->oob;
   *out = e;
   return GVP_OK;
@@ -382,6 +412,11 @@ static int engine_reset(gvp_engine* e) {
   int r = launch_marginals_packed((int)B, K, e->n, B, e->diag, e->off, e->covs, e->crosses,
                                   e->ps.logdet, e->ps.status, e->ps.where, e->scratch, nullptr, s);
   if (r) return r;
+  // ld_cur of the first search: forward Schur, the probes' own recursion (the
+  // backward-sweep value above differs by ~cond * eps, which the KL would see)
+  if ((r = launch_logdet_fwd_packed((int)B, K, e->n, B, e->diag, e->off, e->ps.logdet, nullptr, e->ps.status,
+                                    e->ps.where, s)))
+    return r;
   if ((r = launch_lam_mu((int)B, K, e->n, B, e->diag, e->off, e->mean, e->v, s))) return r;
   // first factor sweep (optimizer.py:338-344)
   if ((r = e->factors())) return r;
@@ -499,6 +534,45 @@ extern "C" int gvp_engine_step_profiled(gvp_engine* e, int32_t iters, double* ms
   return GVP_OK;
 }
 
+// One iteration in which every plan with a finite beta[b] (host, nplans
+// entries) takes that step size instead of the searched one. The search still
+// runs (and is traced): a caller can replay a known step sequence, e.g. the
+// reference's, and compare each search's decisions against it.
+extern "C" int gvp_engine_step_beta(gvp_engine* e, const double* beta) {
+  if (!e || !beta) return GVP_ERR_ARG;
+  if (e->iters_launched >= e->cfg.max_iters) return GVP_OK;
+  cudaStream_t s = e->stream;
+  int r;
+  if (!e->pinned && (r = e->alloc(&e->pinned, (size_t)e->B))) return r;
+  std::vector<double> h(e->B);
+  for (int b = 0; b < e->B; ++b) h[b] = beta[b < e->nreal ? b : 0];
+  GVP_CUDA(cudaMemcpyAsync(e->pinned, h.data(), sizeof(double) * e->B, cudaMemcpyHostToDevice, s));
+  if ((r = launch_select_bisect(e->step_args(), s))) return r;
+  pin_beta_kernel<<<nblk(e->B, 128), 128, 0, s>>>(e->B, e->pinned, e->ps.active, e->ps.beta, e->ps.status,
+                                                  e->ps.where, e->ps.fixkl);
+  GVP_CUDA(cudaGetLastError());
+  if ((r = launch_select_commit(e->step_args(), s))) return r;
+  if ((r = launch_logdet_fwd_packed(e->B, e->K, e->n, e->B, e->diag, e->off, e->ps.logdet_next, e->ps.fixkl,
+                                    nullptr, nullptr, s)))
+    return r;
+  e->launches += 5;  // residual + bisection probes + pin + commit + log det
+  if ((r = e->factors())) return r;
+  if ((r = e->control())) return r;
+  GVP_CUDA(cudaMemsetAsync(e->ps.fixkl, 0, sizeof(int) * e->B, s));
+  ++e->iters_launched;
+  GVP_CUDA(cudaStreamSynchronize(s));
+  return GVP_OK;
+}
+
+// Per-plan count of sigma points that left the SDF grid (clamped, sdf.py:53-56)
+// over every factor stage so far.
+extern "C" int gvp_engine_get_oob(gvp_engine* e, int64_t* oob) {
+  if (!e || !oob) return GVP_ERR_ARG;
+  GVP_CUDA(cudaMemcpyAsync(oob, e->ps.oob, sizeof(int64_t) * e->nreal, cudaMemcpyDeviceToHost, e->stream));
+  GVP_CUDA(cudaStreamSynchronize(e->stream));
+  return GVP_OK;
+}
+
 extern "C" void* gvp_engine_stream(gvp_engine* e) { return (void*)e->stream; }
 
 extern "C" int gvp_engine_sync(gvp_engine* e) {
@@ -551,6 +625,15 @@ extern "C" int gvp_engine_get_state(gvp_engine* e, double* mean, double* diag, d
     int r = fetch_sym(e, covs, e->covs);
     if (r) return r;
   }
+  return GVP_OK;
+}
+
+extern "C" int gvp_engine_get_packed(gvp_engine* e, double* mean, double* covs_packed) {
+  if (!e) return GVP_ERR_ARG;
+  int r;
+  if (mean && (r = get_cols(e, mean, e->mean, e->K * e->n))) return r;
+  if (covs_packed && (r = get_cols(e, covs_packed, e->covs, e->K * e->T))) return r;
+  GVP_CUDA(cudaStreamSynchronize(e->stream));
   return GVP_OK;
 }
 

@@ -186,7 +186,16 @@ struct V2Launch {
   int* nprobes;
   double* scratch;
   const int* active;
+  // true: the search writes kl / ld_next (the accepted probe's KL and
+  // forward-Schur log det); the commit overwrites them only where fixkl[b]
+  bool search_kl;
+  const int* fixkl;
 };
+// forward-Schur log det of packed precisions (plan-minor, stride Bp), the
+// probes' own recursion: a bit-identical ld_cur for the next search. mask
+// (nullable): only plans with mask[b] != 0.
+int launch_logdet_fwd_packed(int nplans, int64_t K, int n, int64_t Bp, const double* ld, const double* lo,
+                             double* logdet, const int* mask, int* status, int* where, cudaStream_t s);
 // ---- wide blocks, 9 <= n <= 32 (wide_kernels.cu): one warp per chain, lanes over rows
 struct WideStep {
   int nplans;

@@ -106,6 +106,7 @@ GVP_DEV double sym_at(const double (&A)[T_<N>], int r, int c) {
 struct PlanSt {
   double lo, hi, best, kl_lo, kl_hi, prev, temp, ldc;
   int phase, nprobe;
+  double ld_best;  // forward-Schur log det of Lambda'(best) (the probe's)
 };
 static_assert(sizeof(PlanSt) <= 80, "PlanSt must fit 10 doubles");
 
@@ -135,6 +136,7 @@ GVP_DEV void search_init(const A& a, PlanSt* pst, int P, int64_t b0, bool commit
   S.temp = ok ? a.temp[bb] : 1.0;
   S.ldc = ok ? a.ld_cur[bb] : 0.0;
   S.nprobe = 0;
+  S.ld_best = NAN;
 }
 
 struct Pick {
@@ -263,7 +265,7 @@ GVP_DEV Pick search_pick(const A& a, const PlanSt* pst, int P, int LP, int lcol,
 template <class A>
 GVP_DEV void search_decide(const A& a, PlanSt* pst, int j, int base, int kl, int64_t b0, bool commit,
                            const double* r_beta, const double* r_kl, const int* r_res,
-                           const int* r_fail, const int* r_on) {
+                           const int* r_fail, const int* r_on, const double* r_ld = nullptr) {
   const int64_t bj = b0 + j;
   PlanSt D = pst[j];
   auto log_probe = [&](int q) {
@@ -304,6 +306,7 @@ GVP_DEV void search_decide(const A& a, PlanSt* pst, int j, int base, int kl, int
         D.lo = mid;
         D.best = mid;
         D.kl_lo = r_kl[q];
+        if (r_ld) D.ld_best = r_ld[q];
       } else {
         D.hi = mid;
         D.kl_hi = r_res[q] == 1 ? INFINITY : r_kl[q];
@@ -320,6 +323,8 @@ GVP_DEV void search_decide(const A& a, PlanSt* pst, int j, int base, int kl, int
       fail(GVP_ERR_NOT_SPD, r_fail[q0] | GVP_WHERE_MEAN_SOLVE_BIAS);
     } else if (feasible(q0)) {
       D.best = a.beta_max;
+      D.kl_lo = r_kl[q0];
+      if (r_ld) D.ld_best = r_ld[q0];
       D.phase = 3;
     } else if (kl == 1) {
       D.kl_hi = r_res[q0] == 1 ? INFINITY : r_kl[q0];
@@ -335,6 +340,7 @@ GVP_DEV void search_decide(const A& a, PlanSt* pst, int j, int base, int kl, int
         D.lo = a.beta_min;
         D.hi = a.beta_max;
         D.kl_lo = r_kl[q1];
+        if (r_ld) D.ld_best = r_ld[q1];
         D.kl_hi = r_res[q0] == 1 ? INFINITY : r_kl[q0];
         if (walk()) D.phase = ((D.hi - D.lo) > 1e-3 * D.hi) ? 2 : 3;
       }
@@ -350,6 +356,7 @@ GVP_DEV void search_decide(const A& a, PlanSt* pst, int j, int base, int kl, int
       D.lo = a.beta_min;
       D.hi = a.beta_max;
       D.kl_lo = r_kl[q0];
+      if (r_ld) D.ld_best = r_ld[q0];
       if (walk()) D.phase = ((D.hi - D.lo) > 1e-3 * D.hi) ? 2 : 3;
     }
   } else if (D.phase == 2) {
@@ -357,6 +364,10 @@ GVP_DEV void search_decide(const A& a, PlanSt* pst, int j, int base, int kl, int
   }
   if (!commit && D.phase == 3) {  // search finished: hand beta to the commit kernel
     a.beta[bj] = D.best;
+    if (r_ld) {  // the accepted probe's KL (kl_joint of step.kl) and forward-Schur log det
+      a.kl[bj] = D.kl_lo;
+      a.ld_next[bj] = D.ld_best;
+    }
     a.status[bj] = GVP_OK;
     a.where[bj] = -1;
     if (a.nprobes) a.nprobes[bj] = D.nprobe;

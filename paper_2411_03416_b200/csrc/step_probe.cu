@@ -98,11 +98,13 @@ struct Args {
   const double *temp, *ld_cur;
   double kl_bound, beta_min, beta_max;
   double* beta;
+  double *kl, *ld_next;  // the accepted probe's KL and forward-Schur log det (search end)
   int *status, *where, *nprobes;
   double* probe_log;
   int max_probes;
   const int* active;
   int ppc;  // plans per CTA (<= the layout's P = 32 / L)
+  int rotate;  // split kernel: rotate the warp roles by the CTA's SM residency slot
 };
 
 template <int N>
@@ -126,7 +128,22 @@ __global__ void __launch_bounds__(128, probe_minb<N>()) probe_split_kernel(const
   extern __shared__ __align__(1024) double smem[];
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + LO::BAR);
   const int tid = threadIdx.x;
-  const int role = tid >> 5;            // warp-uniform
+  // The four roles carry unequal fp64 work (tangent of the S chain the most)
+  // and warp w of every resident CTA lands on sub-partition w % 4, so with
+  // identical role maps one scheduler's fp64 pipe sets the step time while the
+  // others idle at the barrier. Rotating the role map by the CTA's residency
+  // slot (its first warp's hardware slot / 4) mixes the roles on each
+  // sub-partition. Any rotation is correct; it only changes the balance.
+  // (kept in the result area's spare ints: no static shared memory, whose
+  // extra bytes would cost the second resident CTA)
+  int* s_rot = reinterpret_cast<int*>(smem + LO::RES + 64) + 96;
+  if (tid == 0) {
+    unsigned wid = 0;
+    if (a.rotate) asm volatile("mov.u32 %0, %%warpid;" : "=r"(wid));
+    *s_rot = (int)(((wid >> 2) & 1u) * 2u + ((wid >> 3) & 1u));
+  }
+  __syncthreads();
+  const int role = ((tid >> 5) + *s_rot) & 3;  // warp-uniform
   const int chain = role >> 1;          // 0: Lambda', 1: S
   const bool tangent = (role & 1) != 0;
   const int lcol = tid & 31;            // lane slot
@@ -403,7 +420,7 @@ __global__ void __launch_bounds__(128, probe_minb<N>()) probe_split_kernel(const
     }
     __syncthreads();
     if (my_rank >= 0)
-      v3::search_decide(a, pst, tid, pk.dbase, pk.dkl, b0, false, r_beta, r_kl, r_res, r_fail, r_on);
+      v3::search_decide(a, pst, tid, pk.dbase, pk.dkl, b0, false, r_beta, r_kl, r_res, r_fail, r_on, xch);
     __syncthreads();
   }
 }
@@ -641,7 +658,8 @@ __global__ void __launch_bounds__(64) probe_fused_kernel(const __grid_constant__
     }
     __syncthreads();
     if (my_rank >= 0)
-      v3::search_decide(a, pst, tid, pk.dbase, pk.dkl, b0, false, r_beta, r_kl, r_res, r_fail, r_on);
+      v3::search_decide(a, pst, tid, pk.dbase, pk.dkl, b0, false, r_beta, r_kl, r_res, r_fail, r_on,
+                        xch + 64);
     __syncthreads();
   }
 }
@@ -692,7 +710,75 @@ __global__ void __launch_bounds__(128, 4) residual_kernel(int B, int64_t K, int6
   }
 }
 
+// Forward-Schur log det of packed precisions, the probes' chain-0 recursion
+// op for op (W rows as rank-1 updates, chol_inv, normalised pivot product),
+// so ld_cur and the probes' log dets of nearby Lambda' carry correlated
+// rounding (the KL is their difference). Thread per plan; NaN on a non-SPD pivot.
+template <int N>
+__global__ void logdet_fwd_packed_kernel(int B, int64_t K, int64_t Bp, const double* __restrict__ ld,
+                                         const double* __restrict__ lo, double* __restrict__ out,
+                                         const int* __restrict__ mask, int* status, int* where) {
+  constexpr int T = T_<N>, N2 = N * N;
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= B || (mask && !mask[b])) return;
+  double Li[T], pm = 1.0;
+  int acc_e = 0;
+  for (int64_t i = 0; i < K; ++i) {
+    double M[T];
+#pragma unroll
+    for (int q = 0; q < T; ++q) M[q] = ld[(i * T + q) * Bp + b];
+    if (i > 0) {
+      double Mo[N2];
+#pragma unroll
+      for (int q = 0; q < N2; ++q) Mo[q] = lo[((i - 1) * N2 + q) * Bp + b];
+#pragma unroll
+      for (int k = 0; k < N; ++k) {
+        double wk[N];
+#pragma unroll
+        for (int q = 0; q < N; ++q) {
+          double t = 0.0;
+#pragma unroll
+          for (int j = 0; j <= k; ++j) t += Li[tri_idx(k, j)] * Mo[j * N + q];
+          wk[q] = t;
+        }
+#pragma unroll
+        for (int r = 0; r < N; ++r)
+#pragma unroll
+          for (int q = 0; q <= r; ++q) M[tri_idx(r, q)] -= wk[r] * wk[q];
+      }
+    }
+    double pp;
+    if (!v3::chol_inv<N>(M, Li, pp)) {
+      out[b] = NAN;
+      if (status) {
+        status[b] = GVP_ERR_NOT_SPD;
+        where[b] = (int)i;
+      }
+      return;
+    }
+    int ex;
+    pm = frexp(pm * pp, &ex);
+    acc_e += ex;
+  }
+  out[b] = 2.0 * (log(pm) + (double)acc_e * 0.6931471805599453);
+}
+
 }  // namespace v4
+
+int launch_logdet_fwd_packed(int nplans, int64_t K, int n, int64_t Bp, const double* ld, const double* lo,
+                             double* logdet, const int* mask, int* status, int* where, cudaStream_t s) {
+  const unsigned nb = (unsigned)((nplans + 63) / 64);
+  switch (n) {
+    case 2: v4::logdet_fwd_packed_kernel<2><<<nb, 64, 0, s>>>(nplans, K, Bp, ld, lo, logdet, mask, status, where); break;
+    case 4: v4::logdet_fwd_packed_kernel<4><<<nb, 64, 0, s>>>(nplans, K, Bp, ld, lo, logdet, mask, status, where); break;
+    case 6: v4::logdet_fwd_packed_kernel<6><<<nb, 64, 0, s>>>(nplans, K, Bp, ld, lo, logdet, mask, status, where); break;
+    default:
+      set_error("packed log det supports n in {2, 4, 6}");
+      return GVP_ERR_UNSUPPORTED;
+  }
+  GVP_CUDA(cudaGetLastError());
+  return GVP_OK;
+}
 
 int64_t probe_residual_offset(int nplans, int64_t K, int n) {
   const int64_t T = (int64_t)n * (n + 1) / 2;
@@ -736,6 +822,8 @@ int launch_probe(const V2Launch& q, const int L, cudaStream_t s) {
   a.beta_min = q.beta_min;
   a.beta_max = q.beta_max;
   a.beta = q.beta;
+  a.kl = q.kl;
+  a.ld_next = q.ld_next;
   a.status = q.status;
   a.where = q.where;
   a.nprobes = q.nprobes;
@@ -743,6 +831,11 @@ int launch_probe(const V2Launch& q, const int L, cudaStream_t s) {
   a.max_probes = q.max_probes;
   a.active = q.active;
   a.ppc = P;
+  static const int rot_env = [] {
+    const char* e = std::getenv("GVP_PROBE_ROT");
+    return e ? std::atoi(e) : 1;
+  }();
+  a.rotate = rot_env;
   const unsigned grid = (unsigned)((q.nplans + P - 1) / P);
   // split chains (4 warps) while the grid is far from filling the GPU, fused
   // chains (2 warps, fewer barriers) once every SM has several CTAs;

@@ -108,6 +108,22 @@ class PlanBatch:
     def step(self, iters: int = 1, sync: bool = False):
         self._ok(self.lib.gvp_engine_step(self.handle, int(iters), int(sync)), "gvp_engine_step")
 
+    def step_beta(self, beta):
+        """One iteration (synchronous) in which plan b takes step size beta[b]
+        where it is finite (NaN: the searched one). The search still runs and
+        is traced (`probes`), so a known step sequence can be replayed while
+        every search is compared against it."""
+        b = np.ascontiguousarray(np.asarray(beta, dtype=np.float64).reshape(-1))
+        if b.shape != (self.B,):
+            raise ValueError(f"beta needs {self.B} entries")
+        self._ok(self.lib.gvp_engine_step_beta(self.handle, N.ptr(b)), "gvp_engine_step_beta")
+
+    def oob(self) -> np.ndarray:
+        """Per-plan count of sigma points clamped at the SDF border so far."""
+        out = np.zeros(self.B, dtype=np.int64)
+        self._ok(self.lib.gvp_engine_get_oob(self.handle, N.ptr(out)), "gvp_engine_get_oob")
+        return out
+
     def step_profiled(self, iters: int = 1) -> np.ndarray:
         """Kernel-by-kernel iterations with CUDA events; returns summed device
         ms of (bisection, commit, factor_grads, control)."""
@@ -205,6 +221,22 @@ class PlanBatch:
         return {"mean": from_plan_minor(mean), "diag": from_plan_minor(diag),
                 "off": from_plan_minor(off), "covs": from_plan_minor(covs),
                 "crosses": from_plan_minor(crosses)}
+
+    def packed_into(self, mean=None, covs=None):
+        """Fetch into caller buffers without host unpacking (pinned buffers
+        make this a straight DMA): mean (K, n, B) plan-minor, covs packed
+        lower-symmetric (K, n(n+1)/2, B)."""
+        for a, shape in ((mean, (self.K, self.n, self.B)), (covs, (self.K, self.n * (self.n + 1) // 2, self.B))):
+            if a is not None and (a.shape != shape or a.dtype != np.float64 or not a.flags.c_contiguous):
+                raise ValueError(f"buffer must be C-contiguous float64 {shape}")
+        self._ok(self.lib.gvp_engine_get_packed(self.handle, N.ptr(mean), N.ptr(covs)), "gvp_engine_get_packed")
+
+    def mean(self) -> np.ndarray:
+        """Joint means only, (B, K, n)."""
+        m = np.empty((self.K, self.n, self.B))
+        self._ok(self.lib.gvp_engine_get_state(self.handle, N.ptr(m), None, None, None, None),
+                 "gvp_engine_get_state")
+        return from_plan_minor(m)
 
     def summary(self):
         B = self.B

@@ -351,8 +351,11 @@ def run_pgvimp(sys_ltv: LTVSystem, env: Environment | None, cfg: OptimizerConfig
         st = eng.state()
         sm = eng.summary()
         rec = eng.records()[0]
+        oob = int(eng.oob()[0])
     finally:
         eng.close()
+    if env is not None:
+        env.sdf.note_oob(oob)  # every factor stage's clamped points (factors.py:206)
     status, where = int(sm["status"][0]), int(sm["where"][0])
     _raise_plan_status(status, where, cfg)
     iters = int(sm["iterations"][0])
@@ -410,8 +413,11 @@ def run_pgvimp_batch(sys_ltv: LTVSystem, env: Environment | None, cfg: Optimizer
         st = eng.state()
         sm = eng.summary()
         rec = eng.records()
+        oob = eng.oob()
     finally:
         eng.close()
+    if env is not None:
+        env.sdf.note_oob(int(oob.sum()))
     return BatchResult(records=rec, converged=sm["converged"].astype(bool),
                        iterations=sm["iterations"], switch_iteration=sm["switch_iteration"],
                        status=sm["status"], wall_time_ms=(time.perf_counter() - t0) * 1e3, **st)

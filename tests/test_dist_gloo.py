@@ -61,3 +61,32 @@ def test_two_ranks_gloo():
     assert n0 == n1 == 4097            # work summed over ranks
     assert plans0 == plans1 == list(range(4097))  # gather in plan order
     assert ranks0[:2049] == [0] * 2049 and ranks0[2049:] == [1] * 2048
+
+
+@pytest.mark.timeout(300)
+def test_bench_gpus_flag_spawns_ranks():
+    """`bench.py --gpus 2` without a launcher re-runs itself under
+    torch.distributed.run (one rank per device), and its timed region takes
+    the max time over ranks and sums the work: driven here on CPU (gloo) with
+    the CPU stand-in engine (--stub-engine)."""
+    import json
+    import subprocess
+    import sys
+
+    repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    out = subprocess.run([sys.executable, os.path.join(repo, "bench.py"), "--gpus", "2", "--stub-engine",
+                          "--steps", "3", "--warmup", "1", "--plans", "64"],
+                         capture_output=True, text=True, env=env, timeout=280)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, out.stdout  # rank 0 alone prints
+    line = json.loads(lines[0])
+    assert line["n_gpus"] == 2 and line["plans_total"] == 128
+    assert line["evals_all"] == 128 * 3 * 999  # every plan of both shards, 3 iterations, F = N - 1
+    assert line["value"] == pytest.approx(line["evals_all"] / (line["ms_per_step"] * 3 / 1e3))
+    # the world size must match --gpus
+    env.update(WORLD_SIZE="1", RANK="0", LOCAL_RANK="0")
+    bad = subprocess.run([sys.executable, os.path.join(repo, "bench.py"), "--gpus", "2", "--stub-engine"],
+                         capture_output=True, text=True, env=env, timeout=120)
+    assert bad.returncode != 0 and "WORLD_SIZE" in bad.stderr
