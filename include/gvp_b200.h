@@ -248,6 +248,13 @@ int gvp_engine_get_probes(gvp_engine* e, double* log, int32_t* counts);
  * the engine. The search still runs and is traced, so a known step sequence
  * (e.g. the reference's) can be replayed while each search is compared. */
 int gvp_engine_step_beta(gvp_engine* e, const double* beta);
+/* Replace the iterate (mean, precision) of nsel selected plans and redo what
+ * an iteration leaves for the next one (marginals, log det, Lambda mu, factor
+ * stage); records and iteration counts are kept. Host, batch-major over the
+ * selected plans: mean (nsel, nknots, n), diag (nsel, nknots, n, n), off
+ * (nsel, nknots-1, n, n). E.g. restart from another implementation's state. */
+int gvp_engine_set_state(gvp_engine* e, int32_t nsel, const int32_t* plans, const double* mean,
+                         const double* diag, const double* off);
 /* Per-plan count (int64[nplans]) of sigma points clamped at the SDF border
  * over every factor stage so far (sdf.py:53-56 note_oob). */
 int gvp_engine_get_oob(gvp_engine* e, int64_t* oob);

@@ -255,3 +255,94 @@ def _c1_inproc(threads):
     return {"ms": ms, "iterations": res.iterations, "converged": bool(res.converged), "threads": threads,
             "factor_stage_ms": fac_ms, "gbp_ms": gbp_ms, "dense_inverse_ms": dense_ms,
             "records_beta": [r["beta"] for r in res.records][:5]}
+
+
+def exact_solve(S, rhs, x0, sweeps: int = 3):
+    """Iterative refinement of S x = rhs (the reference's own double-precision
+    S and rhs, block tridiagonal) with residuals in 80-bit long double: the
+    exact solution of the reference's system to ~1e-12 relative, the arbiter for
+    the ill-conditioned mean solve (cond ~1e10 at N = 1000)."""
+    gv = _gv()
+    D = np.stack(S.diag).astype(np.longdouble)
+    U = np.stack(S.off).astype(np.longdouble)
+    K, n = D.shape[0], D.shape[1]
+    b = np.asarray(rhs, dtype=np.longdouble).reshape(K, n)
+    x = np.asarray(x0, dtype=np.longdouble).reshape(K, n)
+    for _ in range(sweeps):
+        y = np.einsum("kij,kj->ki", D, x)
+        y[:-1] += np.einsum("kij,kj->ki", U, x[1:])
+        y[1:] += np.einsum("kji,kj->ki", U, x[:-1])
+        r = b - y
+        dx = gv.gbp_mean_solve(S, np.asarray(r, dtype=np.float64).reshape(-1)).reshape(K, n)
+        x = x + dx.astype(np.longdouble)
+    return np.asarray(x, dtype=np.float64)
+
+
+def trace_states(b: int, iters: int) -> list:
+    """The reference's own trajectory of C5 plan b (bench construction, RefPlan),
+    per iteration: the state it starts from, the accepted beta, the record, the
+    next mean and the exact solution of the reference's own mean system at that
+    beta (exact_solve). For the one-step parity test."""
+    plan = RefPlan(b, threads=1)
+    O = plan.O
+    o_solve = O.gbp_mean_solve
+    captured = {}
+
+    def solve(S, rhs):
+        x = o_solve(S, rhs)
+        captured[len(captured)] = (S, np.array(rhs), x)
+        return x
+
+    out = []
+    for _ in range(iters):
+        from gvplan.factors import assemble_joint_gradients
+
+        cur, temp = plan.cur, plan.temp
+        captured.clear()
+        O.gbp_mean_solve = solve
+        try:
+            g_mu, g_sigma = assemble_joint_gradients(plan.factors, plan.maps, plan.nblocks, plan.n)
+            step = O.select_step_size(cur, plan.prior, g_mu, g_sigma, plan.cfg, temp)
+        finally:
+            O.gbp_mean_solve = o_solve
+        # the accepted probe's mean system (bitwise: its solution is step.next_state.mean)
+        S, rhs, x = next(v for v in captured.values() if np.array_equal(v[2], step.next_state.mean))
+        exact = exact_solve(S, rhs, x)
+        nxt = step.next_state
+        nxt_f = plan._factors(nxt, step.marginals)
+        costs = O.cost_breakdown(nxt, plan.prior, temp, marginals=step.marginals, factor_values=nxt_f)
+        rec = [step.beta, temp, costs.prior_cost, costs.collision_cost, costs.entropy_cost, costs.total, step.kl,
+               float(np.linalg.norm(nxt.mean - cur.mean))]
+        out.append({"beta": step.beta, "temp": temp, "mean": cur.mean.reshape(plan.nblocks, plan.n),
+                    "diag": np.stack(cur.prec.diag), "off": np.stack(cur.prec.off),
+                    "next_mean": nxt.mean.reshape(plan.nblocks, plan.n),
+                    "next_exact": exact.reshape(plan.nblocks, plan.n), "record": np.array(rec)})
+        plan.cur, plan.factors = nxt, nxt_f
+        if not plan.switched and costs.collision_cost < plan.collision_tol and plan.temp != plan.cfg.temp_high:
+            plan.temp, plan.switched = plan.cfg.temp_high, True
+    return out
+
+
+def _trace_worker(args):
+    os.environ["OMP_NUM_THREADS"] = "1"
+    return args[0], trace_states(*args)
+
+
+def trace_states_many(plans, iters: int, procs: int | None = None) -> dict:
+    """trace_states for several plans, one process each (spawned: single-threaded BLAS)."""
+    import multiprocessing as mp
+
+    procs = procs or min(len(plans), len(os.sched_getaffinity(0)))
+    saved = {k: os.environ.get(k) for k in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS")}
+    for k in saved:
+        os.environ[k] = "1"
+    try:
+        with mp.get_context("spawn").Pool(procs) as pool:
+            res = pool.map(_trace_worker, [(int(b), iters) for b in plans], chunksize=1)
+    finally:
+        for k, v in saved.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+    return dict(res)

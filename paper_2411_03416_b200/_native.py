@@ -104,9 +104,13 @@ _SIGS = {
                                      C.c_double, C.c_double, _dp, _dp, _dp, _dp, C.c_int32, _dp, _dp, _dp, _dp,
                                      _dp, _dp, _i32p, _i32p]),
     "gvp_engine_get_probes": (C.c_int, [C.c_void_p, _dp, _i32p]),
+    "gvp_prior_assemble_reg": (C.c_int, [C.c_int32, C.c_int32, C.c_int32, C.c_int32, _dp, _dp, _dp, C.c_double,
+                                         C.c_double, C.c_double, _dp, _dp, _dp, _dp, C.c_int32, C.c_double, _dp,
+                                         _dp, _dp, _dp, _dp, _dp, _i32p, _i32p]),
     "gvp_engine_step_beta": (C.c_int, [C.c_void_p, _dp]),
     "gvp_engine_get_oob": (C.c_int, [C.c_void_p, _i64p]),
     "gvp_engine_get_packed": (C.c_int, [C.c_void_p, _dp, _dp]),
+    "gvp_engine_set_state": (C.c_int, [C.c_void_p, C.c_int32, _i32p, _dp, _dp, _dp]),
     "gvp_set_step_lanes": (C.c_int, [C.c_int32]),
     "gvp_chain_scratch_doubles": (C.c_int64, [C.c_int32, C.c_int64, C.c_int32, C.c_int32]),
     "gvp_gbp_marginals_dev": (C.c_int, [C.c_int32, C.c_int64, C.c_int32, C.c_void_p, C.c_void_p,

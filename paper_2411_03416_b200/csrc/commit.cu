@@ -39,7 +39,7 @@ struct Lay {
   static constexpr int S_PHI = 0, S_LIPSI = T, S_Y = 2 * T;
   static constexpr int P = 32, Pb = 32, Kb = KS ? 2 : 32;
   static constexpr int gP = cx_gran(Pb), gK = cx_gran(Kb);
-  // pass B plan rows: LD T | GD T | G N | ETA N | V N | LO N2
+  // pass B plan rows: LD T | GD T | E N | (unused N | unused N) | LO N2
   static constexpr int B0 = 0, B1 = cx_round(T, gP), B2 = cx_round(B1 + T, gP), B3 = cx_round(B2 + N, gP),
                        B4 = cx_round(B3 + N, gP), B5 = cx_round(B4 + N, gP), BR = cx_round(B5 + N2, gP);
   // pass F plan rows: LD T | GD T | MU N | PM N | LO N2
@@ -61,12 +61,12 @@ struct Lay {
   static constexpr int AH = NS - 3;  // pass F: side warps still read knots s-1 and s-2
   static constexpr int RING = NS * STAGE, XCH = RING + RING_D, BAR = XCH + 8 * 32;
   static constexpr size_t BYTES = (size_t)(BAR + 16) * 8;
-  static constexpr uint32_t TX_B = ((2 * T + 3 * N + N2) * Pb + (T + N2) * Kb) * 8;
+  static constexpr uint32_t TX_B = ((2 * T + N + N2) * Pb + (T + N2) * Kb) * 8;
   static constexpr uint32_t TX_F = ((2 * T + 2 * N + N2) * Pb + (T + N2) * Kb + (2 * T + N) * Pb) * 8;
 };
 
 struct Args {
-  CUtensorMap m_ld, m_lo, m_kd, m_ko, m_gd, m_g, m_eta, m_v, m_mu, m_pm, m_phi, m_psiy;
+  CUtensorMap m_ld, m_lo, m_kd, m_ko, m_gd, m_e, m_mu, m_pm, m_phi, m_psiy;
   int B;
   int64_t K, Bp, BLp;
   double *o_mu, *o_ld, *o_lo, *o_cov, *o_cr, *o_v;
@@ -131,9 +131,7 @@ __global__ void __launch_bounds__(128, 1) commit_kernel(const __grid_constant__ 
     if (passB) {
       v3::tma3(st + LO::B0 * Pb, &a.m_ld, (int)b0, 0, (int)i, bar);
       v3::tma3(st + LO::B1 * Pb, &a.m_gd, (int)b0, 0, (int)i, bar);
-      v3::tma3(st + LO::B2 * Pb, &a.m_g, (int)b0, 0, (int)i, bar);
-      v3::tma3(st + LO::B3 * Pb, &a.m_eta, (int)b0, 0, (int)i, bar);
-      v3::tma3(st + LO::B4 * Pb, &a.m_v, (int)b0, 0, (int)i, bar);
+      v3::tma3(st + LO::B2 * Pb, &a.m_e, (int)b0, 0, (int)i, bar);
       v3::tma3(st + LO::B5 * Pb, &a.m_lo, (int)b0, 0, (int)i, bar);
     } else {
       v3::tma3(st + LO::F0 * Pb, &a.m_ld, (int)b0, 0, (int)i, bar);
@@ -171,12 +169,14 @@ __global__ void __launch_bounds__(128, 1) commit_kernel(const __grid_constant__ 
 #pragma unroll
         for (int q = 0; q < T; ++q)
           A_[q] = ((pv(LO::B1 + q) * two_t + kv(LO::K0 + q) * inv_t) + pv(LO::B0 + q) * inv_b) * c;
-      } else {  // S diag block and rhs (optimizer.py:155-159)
+      } else {  // S diag block (optimizer.py:155-159); the system is solved for the
+                // step delta = mu - mu' = S^-1 e, e = S mu - rhs = (K mu + g - eta) / T
+                // (beta-free, the probes' residual): |delta| << |mu| keeps the
+                // cond(S) ~ 1e10 rounding relative to the step, not the iterate
 #pragma unroll
         for (int q = 0; q < T; ++q) A_[q] = kv(LO::K0 + q) * inv_t + pv(LO::B0 + q) * inv_b;
 #pragma unroll
-        for (int r = 0; r < N; ++r)
-          rhs[r] = ((-pv(LO::B2 + r)) * inv_t + pv(LO::B3 + r) * inv_t) + pv(LO::B4 + r) * inv_b;
+        for (int r = 0; r < N; ++r) rhs[r] = pv(LO::B2 + r) * inv_t;
       }
       if (i < K - 1) {
         const double sc_ = role == 0 ? c : 1.0;
@@ -286,13 +286,13 @@ __global__ void __launch_bounds__(128, 1) commit_kernel(const __grid_constant__ 
         auto pv = [&](int row) { return sg[row * Pb + p]; };
         auto kv = [&](int row) { return pr[row * Kb + kcol]; };
         if (role == 1) {
-          // ---- mean: mu'_i = Li^T (y_i - Li S_{i-1,i}^T mu'_{i-1})
+          // ---- step: delta_i = Li^T (y_i - Li S_{i-1,i}^T delta_{i-1}); mu'_i = mu_i - delta_i
           const double* sp = slot(s - 1);
           const double* prp = sp + LO::OFF_PRIOR;
           auto pvp = [&](int row) { return sp[row * Pb + p]; };
           auto kvp = [&](int row) { return prp[row * Kb + kcol]; };
           auto psi = [&](int q) { return sg[LO::OFF_PSIY + q * Pb + p]; };  // LIPSI rows then Y rows
-          double m[N];
+          double dl[N];
           {
             double z[N], w[N];
 #pragma unroll
@@ -301,7 +301,7 @@ __global__ void __launch_bounds__(128, 1) commit_kernel(const __grid_constant__ 
               if (i > 0) {
 #pragma unroll
                 for (int q = 0; q < N; ++q)
-                  t += (kvp(LO::K1 + q * N + r) * inv_t + pvp(LO::F4 + q * N + r) * inv_b) * mprev[q];
+                  t += (kvp(LO::K1 + q * N + r) * inv_t + pvp(LO::F4 + q * N + r) * inv_b) * dprev[q];
               }
               z[r] = t;
             }
@@ -317,15 +317,12 @@ __global__ void __launch_bounds__(128, 1) commit_kernel(const __grid_constant__ 
               double t = 0.0;
 #pragma unroll
               for (int q = r; q < N; ++q) t += psi(tri_idx(q, r)) * w[q];
-              m[r] = t;
+              dl[r] = t;  // delta = cur.mean - nxt.mean
             }
           }
 #pragma unroll
-          for (int r = 0; r < N; ++r) *rg(st_, LO::E_MU + r) = m[r];
-          double dl[N];
-#pragma unroll
           for (int r = 0; r < N; ++r) {
-            dl[r] = pv(LO::F2 + r) - m[r];  // delta = cur.mean - nxt.mean
+            *rg(st_, LO::E_MU + r) = pv(LO::F2 + r) - dl[r];
             acc1 += dl[r] * dl[r];
           }
 #pragma unroll
@@ -342,10 +339,7 @@ __global__ void __launch_bounds__(128, 1) commit_kernel(const __grid_constant__ 
             acc0 += 2.0 * t;
           }
 #pragma unroll
-          for (int r = 0; r < N; ++r) {
-            mprev[r] = m[r];
-            dprev[r] = dl[r];
-          }
+          for (int r = 0; r < N; ++r) dprev[r] = dl[r];
         } else {
           // ---- covariance recursion (gbp.py:72-78)
 #pragma unroll
@@ -528,8 +522,8 @@ int launch_commit_split(const V2Launch& q, cudaStream_t s) {
   int r;
   if ((r = v3::make_map(&a.m_ld, q.ld, q.Bp, T, K, 32, T)) || (r = v3::make_map(&a.m_lo, q.lo, q.Bp, N2, K1, 32, N2)) ||
       (r = v3::make_map(&a.m_kd, q.kd, KW, T, K, Kb, T)) || (r = v3::make_map(&a.m_ko, q.ko, KW, N2, K1, Kb, N2)) ||
-      (r = v3::make_map(&a.m_gd, q.gd, q.Bp, T, K, 32, T)) || (r = v3::make_map(&a.m_g, q.g, q.Bp, n, K, 32, n)) ||
-      (r = v3::make_map(&a.m_eta, q.eta, q.Bp, n, K, 32, n)) || (r = v3::make_map(&a.m_v, q.v, q.Bp, n, K, 32, n)) ||
+      (r = v3::make_map(&a.m_gd, q.gd, q.Bp, T, K, 32, T)) ||
+      (r = v3::make_map(&a.m_e, q.scratch + probe_residual_offset(q.nplans, K, n), q.Bp, n, K, 32, n)) ||
       (r = v3::make_map(&a.m_mu, q.mu, q.Bp, n, K, 32, n)) || (r = v3::make_map(&a.m_pm, q.pmean, q.Bp, n, K, 32, n)) ||
       (r = v3::make_map(&a.m_phi, q.scratch, BLp, SE, K, 32, T)) ||
       (r = v3::make_map(&a.m_psiy, q.scratch, BLp, SE, K, 32, T + n)))

@@ -180,6 +180,15 @@ __global__ void pin_beta_kernel(int B, const double* __restrict__ pinned, const 
   }
 }
 
+// dst (rows, B) column plans[s] <- src (nsel, rows) row s
+__global__ void scatter_cols_kernel(int nsel, const int* __restrict__ plans, int64_t rows,
+                                    const double* __restrict__ src, double* __restrict__ dst, int64_t B) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (int64_t)nsel * rows) return;
+  const int64_t sidx = t / rows, row = t % rows;
+  dst[row * B + plans[sidx]] = src[t];
+}
+
 __global__ void count_active_kernel(int B, const int* active, int* out) {
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b < B && active[b]) atomicAdd(out, 1);
@@ -561,6 +570,63 @@ extern "C" int gvp_engine_step_beta(gvp_engine* e, const double* beta) {
   GVP_CUDA(cudaMemsetAsync(e->ps.fixkl, 0, sizeof(int) * e->B, s));
   ++e->iters_launched;
   GVP_CUDA(cudaStreamSynchronize(s));
+  return GVP_OK;
+}
+
+// Replace the current iterate (mean, precision) of selected plans, e.g. with
+// another implementation's state, and redo what an iteration leaves behind
+// for the next one: marginals, forward log det, Lambda mu and the factor
+// stage at the new state. Records, iteration counts and convergence state are
+// kept. Host arrays, batch-major over the nsel selected plans: mean
+// (nsel, K, n), diag (nsel, K, n, n), off (nsel, K-1, n, n).
+extern "C" int gvp_engine_set_state(gvp_engine* e, int32_t nsel, const int32_t* plans, const double* mean,
+                                    const double* diag, const double* off) {
+  if (!e || nsel < 1 || !plans || !mean || !diag || !off) return GVP_ERR_ARG;
+  const int64_t K = e->K, n = e->n, T = e->T, N2 = n * n, B = e->B;
+  for (int s = 0; s < nsel; ++s)
+    if (plans[s] < 0 || plans[s] >= e->nreal) {
+      set_error("set_state: plan index out of range");
+      return GVP_ERR_ARG;
+    }
+  cudaStream_t st = e->stream;
+  // packed lower diag blocks, host side
+  std::vector<double> dp((size_t)nsel * K * T);
+  for (int64_t s = 0; s < nsel; ++s)
+    for (int64_t i = 0; i < K; ++i)
+      for (int64_t r = 0; r < n; ++r)
+        for (int64_t c = 0; c <= r; ++c)
+          dp[(s * K + i) * T + r * (r + 1) / 2 + c] = diag[((s * K + i) * n + r) * n + c];
+  const int64_t rows_max = std::max({K * n, K * T, (K - 1) * N2});
+  double* stage = nullptr;
+  int* dplans = nullptr;
+  GVP_CUDA(cudaMalloc(&stage, sizeof(double) * nsel * rows_max));
+  GVP_CUDA(cudaMalloc(&dplans, sizeof(int) * nsel));
+  int r = GVP_OK;
+  auto put = [&](const double* src, int64_t rows, double* dst) -> int {
+    GVP_CUDA(cudaMemcpyAsync(stage, src, sizeof(double) * nsel * rows, cudaMemcpyHostToDevice, st));
+    scatter_cols_kernel<<<nblk(nsel * rows, 256), 256, 0, st>>>(nsel, dplans, rows, stage, dst, B);
+    GVP_CUDA(cudaGetLastError());
+    GVP_CUDA(cudaStreamSynchronize(st));  // the stage buffer is reused
+    return GVP_OK;
+  };
+  cudaError_t ce = cudaMemcpyAsync(dplans, plans, sizeof(int) * nsel, cudaMemcpyHostToDevice, st);
+  if (ce != cudaSuccess) r = cuda_fail(ce, "set_state upload");
+  if (!r) r = put(mean, K * n, e->mean);
+  if (!r) r = put(dp.data(), K * T, e->diag);
+  if (!r && K > 1) r = put(off, (K - 1) * N2, e->off);
+  cudaFree(stage);
+  cudaFree(dplans);
+  if (r) return r;
+  if ((r = launch_marginals_packed((int)B, K, e->n, B, e->diag, e->off, e->covs, e->crosses, e->ps.logdet,
+                                   e->ps.status, e->ps.where, e->scratch, e->ps.active, st)))
+    return r;
+  if ((r = launch_logdet_fwd_packed((int)B, K, e->n, B, e->diag, e->off, e->ps.logdet, nullptr, e->ps.status,
+                                    e->ps.where, st)))
+    return r;
+  if ((r = launch_lam_mu((int)B, K, e->n, B, e->diag, e->off, e->mean, e->v, st))) return r;
+  if ((r = e->factors())) return r;
+  e->launches += 4;
+  GVP_CUDA(cudaStreamSynchronize(st));
   return GVP_OK;
 }
 

@@ -450,6 +450,170 @@ __host__ __device__ constexpr bool sym_zero_tri(int t, int P) {
   return sym_zero2(r, t - r * (r + 1) / 2, P);
 }
 
+// gaussian_sqrt's last resort (quadrature.py:178-181): the symmetric
+// eigendecomposition root R = V diag(sqrt(max(lambda, 0))) of the covariance,
+// here by cyclic Jacobi rotations (eigenvalues to ~eps |lambda|_max). A
+// non-triangular root mixes every coordinate into the positions, so the
+// projection grouping does not apply: every sigma point of the rule is
+// evaluated. _moment_gradients (factors.py:95-104) then inverts R
+// (np.linalg.solve): a clipped (zero) eigenvalue makes R singular and the
+// reference raises numpy.linalg.LinAlgError -> GVP_ERR_SQRT here.
+template <int N>
+GVP_DEV void jacobi_eigh(double (&A)[N][N], double (&V)[N][N]) {
+#pragma unroll
+  for (int r = 0; r < N; ++r)
+#pragma unroll
+    for (int c = 0; c < N; ++c) V[r][c] = r == c ? 1.0 : 0.0;
+  for (int sweep = 0; sweep < 64; ++sweep) {
+    double off = 0.0, dia = 0.0;
+#pragma unroll
+    for (int p = 0; p < N; ++p) {
+      dia += A[p][p] * A[p][p];
+#pragma unroll
+      for (int q = p + 1; q < N; ++q) off += A[p][q] * A[p][q];
+    }
+    if (!(off > 1e-36 * dia)) break;
+#pragma unroll
+    for (int p = 0; p < N; ++p)
+#pragma unroll
+      for (int q = p + 1; q < N; ++q) {
+        const double apq = A[p][q];
+        if (apq == 0.0) continue;
+        const double th = (A[q][q] - A[p][p]) / (2.0 * apq);
+        const double t = (th >= 0.0 ? 1.0 : -1.0) / (fabs(th) + sqrt(th * th + 1.0));
+        const double c = 1.0 / sqrt(t * t + 1.0), sn = t * c;
+#pragma unroll
+        for (int k = 0; k < N; ++k) {
+          const double akp = A[k][p], akq = A[k][q];
+          A[k][p] = c * akp - sn * akq;
+          A[k][q] = sn * akp + c * akq;
+        }
+#pragma unroll
+        for (int k = 0; k < N; ++k) {
+          const double apk = A[p][k], aqk = A[q][k];
+          A[p][k] = c * apk - sn * aqk;
+          A[q][k] = sn * apk + c * aqk;
+        }
+#pragma unroll
+        for (int k = 0; k < N; ++k) {
+          const double vkp = V[k][p], vkq = V[k][q];
+          V[k][p] = c * vkp - sn * vkq;
+          V[k][q] = sn * vkp + c * vkq;
+        }
+      }
+  }
+}
+
+// The whole factor through the eigh root (see jacobi_eigh): moments over every
+// rule point, then the moment-form gradients with P^-1 = V diag(1/lambda) V'.
+// S: the covariance (lower triangle read, symmetrised like 0.5 (cov + cov')).
+template <int N, int P>
+__device__ __noinline__ void factor_eigh_path(const double (&S)[N][N], const double (&mu)[N], const RuleDev& R, const FieldDev& F,
+                              double radius_eps, double sigma_obs, const FactorOut& out, int64_t b, int64_t f,
+                              int64_t knot) {
+  constexpr int T = N * (N + 1) / 2;
+  double A[N][N], V[N][N];
+#pragma unroll
+  for (int r = 0; r < N; ++r)
+#pragma unroll
+    for (int c = 0; c <= r; ++c) A[r][c] = A[c][r] = S[r][c];
+  jacobi_eigh<N>(A, V);
+  double root[N][N], lam[N];
+  bool singular = false;
+#pragma unroll
+  for (int k = 0; k < N; ++k) {
+    lam[k] = A[k][k] > 0.0 ? A[k][k] : 0.0;  // np.clip(eigvals, 0.0, None)
+    singular = singular || !(lam[k] > 0.0);
+    const double sq = sqrt(lam[k]);
+#pragma unroll
+    for (int r = 0; r < N; ++r) root[r][k] = V[r][k] * sq;
+  }
+  double e0 = 0.0, E1[N], E2[T];
+#pragma unroll
+  for (int r = 0; r < N; ++r) E1[r] = 0.0;
+#pragma unroll
+  for (int k = 0; k < T; ++k) E2[k] = 0.0;
+  unsigned long long nout = 0;
+  for (int64_t l = 0; l < R.npts; ++l) {
+    double dx[N];
+#pragma unroll
+    for (int r = 0; r < N; ++r) {
+      double acc = 0.0;
+#pragma unroll
+      for (int k = 0; k < N; ++k) acc += root[r][k] * __ldg(R.points + l * N + k);
+      dx[r] = acc;
+    }
+    bool o;
+    const double d = (P == 2) ? interp2_clamped(F, mu[0] + dx[0], mu[1] + dx[1], o)
+                              : interp3<false>(F, mu[0] + dx[0], mu[1] + dx[1], mu[P - 1] + dx[P - 1], o);
+    nout += o ? 1ull : 0ull;
+    const double gap = radius_eps - d;
+    if (gap > 0.0) {
+      const double wc = __ldg(R.weights + l) * sigma_obs * gap * gap;
+      e0 += wc;
+#pragma unroll
+      for (int r = 0; r < N; ++r) {
+        E1[r] += wc * dx[r];
+#pragma unroll
+        for (int c = 0; c <= r; ++c) E2[tri_idx(r, c)] += wc * dx[r] * dx[c];
+      }
+    }
+  }
+  if (nout) atomicAdd(out.oob + b, nout);
+  bool finite = isfinite(e0);
+#pragma unroll
+  for (int r = 0; r < N; ++r) finite = finite && isfinite(E1[r]);
+#pragma unroll
+  for (int k = 0; k < T; ++k) finite = finite && isfinite(E2[k]);
+  if (singular || !finite) {
+    atomicMax(out.status + b, singular ? GVP_ERR_SQRT : GVP_ERR_NONFINITE);
+    atomicMin(out.where + b, (int)knot);
+    return;
+  }
+  double Pi[N][N];  // P^-1 = V diag(1/lambda) V'
+#pragma unroll
+  for (int r = 0; r < N; ++r)
+#pragma unroll
+    for (int c = 0; c < N; ++c) {
+      double acc = 0.0;
+#pragma unroll
+      for (int k = 0; k < N; ++k) acc += V[r][k] * (V[c][k] / lam[k]);
+      Pi[r][c] = acc;
+    }
+#pragma unroll
+  for (int r = 0; r < N; ++r) {
+    double acc = 0.0;
+#pragma unroll
+    for (int k = 0; k < N; ++k) acc += Pi[r][k] * E1[k];
+    out.g_mu.p[knot * out.g_mu.sk + b * out.g_mu.sp + r * out.g_mu.se] = acc;
+  }
+  double W[N][N];  // E2 P^-1
+#pragma unroll
+  for (int r = 0; r < N; ++r)
+#pragma unroll
+    for (int c = 0; c < N; ++c) {
+      double acc = 0.0;
+#pragma unroll
+      for (int k = 0; k < N; ++k) acc += E2[r >= k ? tri_idx(r, k) : tri_idx(k, r)] * Pi[k][c];
+      W[r][c] = acc;
+    }
+#pragma unroll
+  for (int r = 0; r < N; ++r)
+#pragma unroll
+    for (int c = 0; c <= r; ++c) {
+      double hrc = 0.0, hcr = 0.0;  // (P^-1 E2 P^-1)[r][c] and [c][r]
+#pragma unroll
+      for (int k = 0; k < N; ++k) {
+        hrc += Pi[r][k] * W[k][c];
+        hcr += Pi[c][k] * W[k][r];
+      }
+      // symmetrize(-0.5 P^-1 e0 + 0.5 P^-1 E2 P^-1)
+      const double grc = -0.5 * Pi[r][c] * e0 + 0.5 * hrc, gcr = -0.5 * Pi[c][r] * e0 + 0.5 * hcr;
+      out.g_diag.p[knot * out.g_diag.sk + b * out.g_diag.sp + tri_idx(r, c) * out.g_diag.se] = 0.5 * (grc + gcr);
+    }
+  out.e_psi(b, f, 0) = e0 > 0.0 ? e0 : 0.0;
+}
+
 template <int N, int P, bool GRID2D, int NP, bool SYM>
 __global__ void __launch_bounds__(128, GVP_FACTOR_MINBLOCKS)
 factor_grads_kernel(int nplans, int64_t nfac, View mean, View covs, RuleDev R, FieldDev F,
@@ -487,17 +651,24 @@ factor_grads_kernel(int nplans, int64_t nfac, View mean, View covs, RuleDev R, F
   // gaussian_sqrt (quadrature.py:164-177): Cholesky, then one 1e-10 jitter retry
   // np.linalg.cholesky has no 1e-300 pivot floor: FLOOR=false
   double dinv[N];
-  bool ok = chol_fast<N, false>(S, L, dinv);
-  if (!ok) {
+  // false: the factor went through the eigh root (factor_eigh_path) and is done
+  auto gsqrt = [&]() -> bool {
+    bool ok = chol_fast<N, false>(S, L, dinv);
+    if (!ok) {
+      double Sj[N][N];
 #pragma unroll
-    for (int r = 0; r < N; ++r) S[r][r] += 1e-10;
-    ok = chol_fast<N, false>(S, L, dinv);
-  }
-  if (!ok) {  // the eigh root branch is not taken on device: report it
-    atomicMax(out.status + b, GVP_ERR_SQRT);
-    atomicMin(out.where + b, (int)knot);
-    return;
-  }
+      for (int r = 0; r < N; ++r)
+#pragma unroll
+        for (int c = 0; c <= r; ++c) Sj[r][c] = S[r][c] + (r == c ? 1e-10 : 0.0);
+      ok = chol_fast<N, false>(Sj, L, dinv);
+    }
+    if (!ok) factor_eigh_path<N, P>(S, mu, R, F, radius_eps, sigma_obs, out, b, f, knot);
+    return ok;
+  };
+  // planar clouds: the clear-cloud test below needs only S[:2,:2], so the
+  // Cholesky is deferred until a lane needs its sigma points
+  constexpr bool LAZY = NP > 0 && P == 2;
+  if (!LAZY && !gsqrt()) return;
 
   // ---- quadrature over distinct position projections
   double e0 = 0.0, E1[N], E2[T];
@@ -519,8 +690,9 @@ factor_grads_kernel(int nplans, int64_t nfac, View mean, View covs, RuleDev R, F
       // spectral norm of L[:2,:2]: |L_pp xi| <= sqrt(lambda_max(L_pp L_pp')) |xi|, and
       // L_pp L_pp' = S[:2,:2] (the Cholesky's leading block), closed form; up to sqrt(2)
       // tighter than the Frobenius bound for a round cloud. (1 + 1e-12) covers rounding.
+      // (+1e-10: a jitter retry of the deferred Cholesky raises lambda_max by at most that)
       const double a = S[0][0], c = S[1][1], h = 0.5 * (a - c);
-      fr = (0.5 * (a + c) + sqrt(h * h + S[1][0] * S[1][0])) * (1.0 + 1e-12);
+      fr = (0.5 * (a + c) + sqrt(h * h + S[1][0] * S[1][0]) + (LAZY ? 1e-10 : 0.0)) * (1.0 + 1e-12);
     } else {
 #pragma unroll
       for (int r = 0; r < P; ++r)
@@ -543,6 +715,7 @@ factor_grads_kernel(int nplans, int64_t nfac, View mean, View covs, RuleDev R, F
                                  : interp3<false>(F, mu[0], mu[1], mu[P - 1], oc);
       if (dc - F.lip * Rad - radius_eps > 1e-9) {
         if (!inside) {  // bounds test of every projection, as the quadrature below does it
+          if (LAZY && !gsqrt()) return;
 #pragma unroll
           for (int j = 0; j < NP; ++j) {
             double pos[P];
@@ -566,6 +739,7 @@ factor_grads_kernel(int nplans, int64_t nfac, View mean, View covs, RuleDev R, F
         return;
       }
     }
+    if (LAZY && !gsqrt()) return;
     double psi[NP];
     bool any_hit = false;
     if (P == 2 && __all_sync(__activemask(), inside)) {

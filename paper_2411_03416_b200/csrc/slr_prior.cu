@@ -357,7 +357,8 @@ __global__ void prior_node_kernel(int nplans, int S, int n, int m, const double*
 
 // Grammian (node order), symmetrise, SPD check with 1e-10 retry, inverse
 __global__ void prior_step_kernel(int nplans, int S, int nodes, const double* __restrict__ terms,
-                                  double* __restrict__ grams, double* __restrict__ qinv, int* status, int* where) {
+                                  double* __restrict__ grams, double* __restrict__ qinv, int* status, int* where,
+                                  double reg) {
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= nplans * S) return;
   constexpr int M = NS;
@@ -371,6 +372,11 @@ __global__ void prior_step_kernel(int nplans, int S, int nodes, const double* __
       G[r * M + c] = v;
       G[c * M + r] = v;
     }
+  if (reg > 0.0) {  // robust-conditioning mode: Q + reg tr(Q)/n I (deviates from the reference)
+    double tr = 0.0;
+    for (int r = 0; r < M; ++r) tr += G[r * M + r];
+    for (int r = 0; r < M; ++r) G[r * M + r] += reg * tr / M;
+  }
   double L[M * M];
   if (!chol_full<M>(G, L, 0.0)) {
     for (int r = 0; r < M; ++r) G[r * M + r] += 1e-10;  // _GRAMMIAN_JITTER (prior.py:96-98)
@@ -543,11 +549,13 @@ extern "C" int gvp_slr_quadrotor(int32_t nplans, int32_t K, const double* means,
 // A (S, 6, 6), a (S, 6), B (S, 6, m); Gauss-Legendre nodes/weights on [-1, 1].
 // Out: phis (S,6,6), offsets (S,6), grammians (S,6,6), diag (S+1,6,6),
 // off (S,6,6), info (S+1,6). The anchored mean is a separate mean solve.
-extern "C" int gvp_prior_assemble(int32_t nplans, int32_t S, int32_t n, int32_t m, const double* A, const double* a,
-                                  const double* B, double dt, double q_c, double sigma_b, const double* x0,
-                                  const double* goal, const double* gl_nodes, const double* gl_weights,
-                                  int32_t nodes, double* phis, double* offs, double* grams, double* diag,
-                                  double* off, double* info, int32_t* status, int32_t* where) {
+extern "C" int gvp_prior_assemble_reg(int32_t nplans, int32_t S, int32_t n, int32_t m, const double* A,
+                                      const double* a, const double* B, double dt, double q_c, double sigma_b,
+                                      const double* x0, const double* goal, const double* gl_nodes,
+                                      const double* gl_weights, int32_t nodes, double grammian_reg, double* phis,
+                                      double* offs, double* grams, double* diag, double* off, double* info,
+                                      int32_t* status, int32_t* where) {
+  if (!(grammian_reg >= 0.0)) return GVP_ERR_ARG;
   if (nplans < 1 || S < 1 || nodes < 1 || !(dt > 0) || !(q_c > 0) || !(sigma_b > 0)) return GVP_ERR_ARG;
   if (n != slrp::NS || m < 1 || m > 6) {
     set_error("device prior assembly supports n = 6 (planar quadrotor)");
@@ -579,7 +587,7 @@ extern "C" int gvp_prior_assemble(int32_t nplans, int32_t S, int32_t n, int32_t 
   slrp::prior_node_kernel<<<nblk(BS * (nodes + 1), 64), 64>>>(nplans, S, n, m, dA, da, dB, dt, q_c, dgs, dgw, nodes,
                                                               dterms, dphi, doff, ds, dwh);
   GVP_CUDA(cudaGetLastError());
-  slrp::prior_step_kernel<<<nblk(BS, 64), 64>>>(nplans, S, nodes, dterms, dgram, dqi, ds, dwh);
+  slrp::prior_step_kernel<<<nblk(BS, 64), 64>>>(nplans, S, nodes, dterms, dgram, dqi, ds, dwh, grammian_reg);
   GVP_CUDA(cudaGetLastError());
   const double anchor = 1.0 / (sigma_b * sigma_b);
   slrp::prior_knot_kernel<<<nblk(BK, 64), 64>>>(nplans, S, dphi, doff, dqi, dx0, dgoal, anchor, ddiag, dof, dinfo);
@@ -593,4 +601,13 @@ extern "C" int gvp_prior_assemble(int32_t nplans, int32_t S, int32_t n, int32_t 
   GVP_CUDA(cudaMemcpy(status, ds, nplans * sizeof(int), cudaMemcpyDeviceToHost));
   GVP_CUDA(cudaMemcpy(where, dwh, nplans * sizeof(int), cudaMemcpyDeviceToHost));
   return GVP_OK;
+}
+
+extern "C" int gvp_prior_assemble(int32_t nplans, int32_t S, int32_t n, int32_t m, const double* A, const double* a,
+                                  const double* B, double dt, double q_c, double sigma_b, const double* x0,
+                                  const double* goal, const double* gl_nodes, const double* gl_weights,
+                                  int32_t nodes, double* phis, double* offs, double* grams, double* diag,
+                                  double* off, double* info, int32_t* status, int32_t* where) {
+  return gvp_prior_assemble_reg(nplans, S, n, m, A, a, B, dt, q_c, sigma_b, x0, goal, gl_nodes, gl_weights, nodes,
+                                0.0, phis, offs, grams, diag, off, info, status, where);
 }

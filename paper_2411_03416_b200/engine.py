@@ -118,6 +118,17 @@ class PlanBatch:
             raise ValueError(f"beta needs {self.B} entries")
         self._ok(self.lib.gvp_engine_step_beta(self.handle, N.ptr(b)), "gvp_engine_step_beta")
 
+    def set_state(self, plans, mean, diag, off):
+        """Replace the iterate of the given plans (batch-major over `plans`:
+        mean (s, K, n), diag (s, K, n, n), off (s, K-1, n, n)) and recompute
+        the marginals, log det and factor stage at it."""
+        pl = np.ascontiguousarray(np.asarray(plans, dtype=np.int32).reshape(-1))
+        s, K, n = len(pl), self.K, self.n
+        m, d, o = N.f64(np.reshape(mean, (s, K, n))), N.f64(np.reshape(diag, (s, K, n, n))), \
+            N.f64(np.reshape(off, (s, K - 1, n, n)))
+        self._ok(self.lib.gvp_engine_set_state(self.handle, s, N.ptr(pl), N.ptr(m), N.ptr(d), N.ptr(o)),
+                 "gvp_engine_set_state")
+
     def oob(self) -> np.ndarray:
         """Per-plan count of sigma points clamped at the SDF border so far."""
         out = np.zeros(self.B, dtype=np.int64)

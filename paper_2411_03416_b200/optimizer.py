@@ -256,8 +256,8 @@ def _raise_plan_status(status: int, where: int, cfg: OptimizerConfig):
     if status == N.GVP_ERR_NONFINITE:
         from .factors import FactorEvaluationError
         raise FactorEvaluationError(where, "non-finite expectation")
-    if status == N.GVP_ERR_SQRT:
-        raise NotImplementedError(f"factor {where}: covariance needs the eigh root of gaussian_sqrt")
+    if status == N.GVP_ERR_SQRT:  # singular eigh root: np.linalg.solve in _moment_gradients (factors.py:98)
+        raise np.linalg.LinAlgError(f"Singular matrix (factor {where}: eigh root of gaussian_sqrt)")
     if status != 0:
         raise RuntimeError(f"plan failed with status {status}")
 

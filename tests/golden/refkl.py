@@ -69,3 +69,81 @@ def kl_banded(nxt_mean, nxt_diag, nxt_off, cur_mean, cur_diag, cur_off) -> float
     ldn = 2.0 * float(np.sum(np.log(Ln[0])))
     ldc = 2.0 * float(np.sum(np.log(Lc[0])))
     return 0.5 * (tr + mah - dim + ldn - ldc)
+
+
+def _chol_band_ld(ab: np.ndarray) -> np.ndarray:
+    """Banded Cholesky (lower storage ab[i-j, j] = A[i, j]) in 80-bit long double."""
+    kd, dim = ab.shape[0] - 1, ab.shape[1]
+    A = ab.astype(np.longdouble)
+    L = np.zeros_like(A)
+    for j in range(dim):
+        k0 = max(0, j - kd)
+        row_j = np.array([L[j - k, k] for k in range(k0, j)], dtype=np.longdouble)  # L[j, k0:j]
+        s = A[0, j] - np.dot(row_j, row_j)
+        if not s > 0:
+            raise np.linalg.LinAlgError(f"long-double Cholesky: pivot {j}")
+        d = np.sqrt(s)
+        L[0, j] = d
+        for i in range(j + 1, min(dim, j + kd + 1)):
+            ki = max(0, i - kd)
+            acc = A[i - j, j]
+            for k in range(ki, j):
+                acc -= L[i - k, k] * L[j - k, k]
+            L[i - j, j] = acc / d
+    return L
+
+
+def kl_banded_ld(nxt_mean, nxt_diag, nxt_off, cur_mean, cur_diag, cur_off, block: int = 512) -> float:
+    """kl_banded in 80-bit long double on the same (double) matrices: the
+    arbiter's arbiter (64-bit significand, ~2000x finer than fp64)."""
+    Ln = _chol_band_ld(banded_lower(np.asarray(nxt_diag), np.asarray(nxt_off)))
+    Lc = _chol_band_ld(banded_lower(np.asarray(cur_diag), np.asarray(cur_off)))
+    kd, dim = Ln.shape[0] - 1, Ln.shape[1]
+    tr = np.longdouble(0.0)
+    for c0 in range(0, dim, block):
+        c1 = min(dim, c0 + block)
+        B = np.zeros((dim, c1 - c0), dtype=np.longdouble)  # columns c0..c1 of Lc
+        for k in range(kd + 1):
+            idx = np.arange(c0, c1)
+            ok = idx + k < dim
+            B[idx[ok] + k, idx[ok] - c0] = Lc[k, idx[ok]]
+        X = np.zeros_like(B)
+        for i in range(c0, dim):  # forward substitution, rows below c0 are zero
+            acc = B[i].copy()
+            for k in range(1, kd + 1):
+                if i - k >= c0:
+                    acc -= Ln[k, i - k] * X[i - k]
+            X[i] = acc / Ln[0, i]
+        tr += np.sum(X * X)
+    d = np.asarray(cur_mean, dtype=np.longdouble).reshape(-1) - np.asarray(nxt_mean, dtype=np.longdouble).reshape(-1)
+    y = np.zeros(dim, dtype=np.longdouble)
+    for k in range(kd + 1):
+        y[:dim - k] += Lc[k, :dim - k] * d[k:]
+    mah = np.sum(y * y)
+    ldn = 2 * np.sum(np.log(Ln[0]))
+    ldc = 2 * np.sum(np.log(Lc[0]))
+    return float(0.5 * (tr + mah - dim + ldn - ldc))
+
+
+def exact_bt_solve(diag, off, rhs, x0=None, sweeps: int = 4) -> np.ndarray:
+    """Solution of the block-tridiagonal SPD system (diag (K,n,n), off (K-1,n,n)
+    = block (i, i+1)) with right-hand side rhs, by iterative refinement: LAPACK
+    banded solves for the corrections, residuals in 80-bit long double. Accurate
+    to ~1e-12 relative for cond up to ~1e12: the arbiter for ill-conditioned
+    mean solves."""
+    import scipy.linalg as sl
+
+    diag, off = np.asarray(diag, dtype=np.float64), np.asarray(off, dtype=np.float64)
+    K, n = diag.shape[0], diag.shape[1]
+    ab = banded_lower(diag, off)
+    b = np.asarray(rhs, dtype=np.longdouble).reshape(K, n)
+    D, U = diag.astype(np.longdouble), off.astype(np.longdouble)
+    x = np.zeros((K, n), dtype=np.longdouble) if x0 is None else np.asarray(x0, dtype=np.longdouble).reshape(K, n)
+    for _ in range(sweeps):
+        y = np.einsum("kij,kj->ki", D, x)
+        y[:-1] += np.einsum("kij,kj->ki", U, x[1:])
+        y[1:] += np.einsum("kji,kj->ki", U, x[:-1])
+        r = np.asarray(b - y, dtype=np.float64).reshape(-1)
+        dx = sl.solveh_banded(ab, r, lower=True).reshape(K, n)
+        x = x + dx.astype(np.longdouble)
+    return np.asarray(x, dtype=np.float64).reshape(-1)
