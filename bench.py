@@ -62,27 +62,14 @@ def c5_cfg(P, max_iters):
 
 
 def build_problem(P, goals):
-    """Shared prior precision; per-plan info / prior mean / initial mean.
-    The anchored prior mean is affine in the goal, so plan b's mean is the
-    base mean plus n precomputed unit responses (setup only, not timed)."""
-    K, n = N_INTERVALS + 1, 4
+    """The C5 problem through the public batch API's builder
+    (optimizer.batch_problem, what run_pgvimp_batch loads): one prior (the
+    first plan's), per-plan info / anchored mean / initial mean from the
+    affine dependence on the goal (setup only, not timed)."""
     sys_ltv = P.point_robot_lti(2)(N_INTERVALS, T_TOTAL / N_INTERVALS)
-    base_goal = np.array([10.0, 10.0, 0.0, 0.0])
-    prior = P.assemble_prior(sys_ltv, np.zeros(4), base_goal, 1.0, 1e-3)
-    anchor = np.eye(n) / 1e-3 ** 2
-    resp = np.zeros((n, K, n))
-    for j in range(n):
-        eta = np.zeros((K, n))
-        eta[-1] = anchor[:, j]
-        resp[j] = P.gbp_mean_solve(prior.prec, eta.reshape(-1)).reshape(K, n)
-    dg = goals - base_goal
-    B = len(goals)
-    info = np.repeat(prior.info.reshape(1, K, n), B, axis=0)
-    info[:, -1, :] += dg @ anchor.T
-    pmean = prior.mean.reshape(1, K, n) + np.einsum("bj,jkn->bkn", dg, resp)
-    a = np.linspace(0.0, 1.0, K).reshape(1, K, 1)
-    init = a * goals[:, None, :]
-    return prior, info, pmean, init
+    from paper_2411_03416_b200.optimizer import batch_problem
+
+    return batch_problem(sys_ltv, np.zeros(4), goals, 1.0, 1e-3, c5_cfg(P, 10))
 
 
 class ClockSampler:

@@ -38,7 +38,8 @@ extern "C" {
 #define GVP_ERR_NOT_SPD 1          /* NotPositiveDefiniteError (blocktri.py:20); where = knot */
 #define GVP_ERR_NONFINITE 2        /* FactorEvaluationError (factors.py:34-37); where = factor index */
 #define GVP_ERR_NO_FEASIBLE_STEP 3 /* RuntimeError "no feasible step size" (optimizer.py:217-221) */
-#define GVP_ERR_SQRT 4             /* gaussian_sqrt needed its eigh root (quadrature.py:178-181) */
+#define GVP_ERR_SQRT 4             /* gaussian_sqrt's eigh root (quadrature.py:178-181) has a clipped
+                                      eigenvalue: singular, numpy.linalg.LinAlgError in _moment_gradients */
 #define GVP_ERR_ARG -1             /* bad argument (ValueError) */
 #define GVP_ERR_UNSUPPORTED -2     /* block size n outside the supported range, or grid ndim not 2/3 */
 #define GVP_ERR_CUDA -3            /* CUDA runtime failure; see gvp_last_error() */
@@ -278,6 +279,14 @@ int gvp_prior_assemble(int32_t nplans, int32_t S, int32_t n, int32_t m, const do
                        const double* B, double dt, double q_c, double sigma_b, const double* x0, const double* goal,
                        const double* gl_nodes, const double* gl_weights, int32_t nodes, double* phis, double* offs,
                        double* grams, double* diag, double* off, double* info, int32_t* status, int32_t* where);
+/* The same with the robust-conditioning mode (NOT the reference's arithmetic):
+ * every Grammian regularised to Q + grammian_reg tr(Q)/n I before its SPD
+ * check and inverse (grammian_reg = 0: gvp_prior_assemble). */
+int gvp_prior_assemble_reg(int32_t nplans, int32_t S, int32_t n, int32_t m, const double* A, const double* a,
+                           const double* B, double dt, double q_c, double sigma_b, const double* x0,
+                           const double* goal, const double* gl_nodes, const double* gl_weights, int32_t nodes,
+                           double grammian_reg, double* phis, double* offs, double* grams, double* diag,
+                           double* off, double* info, int32_t* status, int32_t* where);
 
 /* ------------------------------------------------ 7-DOF sphere arm */
 /* Factor moments (the factor_expectations contract, _kernels.pyx:132-177) for

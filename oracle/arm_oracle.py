@@ -10,9 +10,12 @@ angles (the first half of the 14-dimensional state), d the trilinear SDF of the
 reference (sdf.py:80-122). This module restates that definition directly — a
 standard-DH forward kinematics, every sigma point, sequential accumulation —
 and is the checker of the CUDA kernel (csrc/arm_factor.cu). There is no
-reference output to pin it against: it is checked for self-consistency
-(tests/test_arm_cpu.py: FK against closed-form poses, the expectation against
-a Monte-Carlo estimate, the Stein identity of the gradients).
+reference output to pin it against: it is checked for self-consistency —
+FK orthonormality / reach / base-rotation equivariance and the
+degenerate-covariance point cost (tests/test_arm.py), the Stein identity of the
+moment-form gradients and the factorised-vs-joint ("Eq. 20") gradients of a
+3-knot chain (tests/test_arm_cpu.py, the reference's test_factors.py:72-82 and
+:136-162 restated for the arm potential).
 """
 
 from __future__ import annotations

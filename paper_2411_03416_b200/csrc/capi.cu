@@ -232,6 +232,8 @@ extern "C" int gvp_evaluate_factors(const double* mean, const double* covs, int6
   GVP_TRY(C.arena.get(4, K * T, &d_gd));
   GVP_TRY(C.arena.get(5, 1, &d_oob));
   GVP_TRY(C.arena.get(6, 2, &d_st));
+  int* d_eigh;  // gaussian_sqrt's eigh fallback list (FactorOut::eigh_list)
+  GVP_TRY(C.arena.get(7, (size_t)std::max<int64_t>(F, 1) + 1, &d_eigh));
   // the kernel reads the lower triangle of each covariance block, like
   // np.linalg.cholesky does in gaussian_sqrt (quadrature.py:175)
   const std::vector<double> covs_p = pack_lower(covs, K, n);
@@ -241,7 +243,7 @@ extern "C" int gvp_evaluate_factors(const double* mean, const double* covs, int6
   const int init_st[2] = {0, INT_MAX};
   GVP_TRY(h2d(d_st, init_st, 2, s));
   FactorOut fo{pmview(d_epsi, 1, 1), pmview(d_gmu, n, 1), pmview(d_gd, T, 1), d_oob, d_st,
-               d_st + 1};
+               d_st + 1, d_eigh};
   GVP_TRY(launch_factor_grads(1, K, n, pview(d_mean, n, 1), pview(d_covs, T, 1), C.rule.dev,
                               C.field.dev, radius_eps, sigma_obs, fo, nullptr, s));
   int st[2];
@@ -257,7 +259,7 @@ extern "C" int gvp_evaluate_factors(const double* mean, const double* covs, int6
   *oob = (int64_t)h_oob;
   if (st[0] != GVP_OK) {
     *where = st[1];
-    set_error(st[0] == GVP_ERR_SQRT ? "covariance needs the eigendecomposition root"
+    set_error(st[0] == GVP_ERR_SQRT ? "Singular matrix (eigh root of gaussian_sqrt with a clipped eigenvalue)"
                                     : "non-finite expectation");
     return st[0];
   }

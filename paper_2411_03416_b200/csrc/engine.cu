@@ -225,6 +225,7 @@ struct gvp_engine {
   double* plog = nullptr;
   int* pcount = nullptr;
   double* pinned = nullptr;  // gvp_engine_step_beta: per-plan step sizes (NaN = searched)
+  int* eigh_list = nullptr;  // FactorOut::eigh_list (gaussian_sqrt's eigh fallback)
   int max_probes = 0;
   int iters_launched = 0;
   int64_t launches = 0;
@@ -248,8 +249,8 @@ struct gvp_engine {
   MutView mvw(double* p, int64_t E) const { return MutView{p, E * B, B, 1}; }
 
   int factors() {
-    FactorOut fo{mvw(epsi, 1), mvw(gmu, n), mvw(gdiag, T), ps.oob, ps.fstatus, ps.fwhere};
-    launches += (K > 2);
+    FactorOut fo{mvw(epsi, 1), mvw(gmu, n), mvw(gdiag, T), ps.oob, ps.fstatus, ps.fwhere, eigh_list};
+    launches += 2 * (K > 2);  // factor_grads_kernel + the eigh fix-up
     return launch_factor_grads(B, K, n, vw(mean, n), vw(covs, T), rule.dev, field.dev, radius_eps,
                                sigma_obs, fo, ps.active, stream);
   }
@@ -379,7 +380,8 @@ extern "C" int gvp_engine_create(gvp_engine** out, int32_t nplans, int64_t nknot
       (r = e->alloc(&e->kfull_d, K * N2 * kb)) || (r = e->alloc(&e->scratch, (size_t)scr)) ||
       (r = e->alloc(&e->records, (size_t)cfg->max_iters * B * GVP_NREC)) ||
       (r = e->alloc(&e->scal, 10 * B)) || (r = e->alloc(&e->ints, 10 * B + 1)) ||
-      (r = e->alloc(&e->oob, B)))
+      (r = e->alloc(&e->oob, B)) ||
+      (r = e->alloc(&e->eigh_list, (size_t)(1 + B * std::max<int64_t>(K - 2, 1)))))
     return fail(r);
   PlanState& ps = e->ps;
   double* s = e->scal;
@@ -506,7 +508,7 @@ extern "C" int gvp_engine_step(gvp_engine* e, int32_t iters, int32_t sync) {
       e->launches = before;  // counted per replay below
     }
     GVP_CUDA(cudaGraphLaunch(e->graph, s));
-    e->launches += 4 + (e->K > 2);  // residual, probes, commit, [factors], control
+    e->launches += 4 + 2 * (e->K > 2);  // residual, probes, commit, [factors + eigh fix-up], control
     ++e->iters_launched;
   }
   if (sync) GVP_CUDA(cudaStreamSynchronize(s));

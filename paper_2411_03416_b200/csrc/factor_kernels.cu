@@ -508,7 +508,7 @@ GVP_DEV void jacobi_eigh(double (&A)[N][N], double (&V)[N][N]) {
 // rule point, then the moment-form gradients with P^-1 = V diag(1/lambda) V'.
 // S: the covariance (lower triangle read, symmetrised like 0.5 (cov + cov')).
 template <int N, int P>
-__device__ __noinline__ void factor_eigh_path(const double (&S)[N][N], const double (&mu)[N], const RuleDev& R, const FieldDev& F,
+GVP_DEV void factor_eigh_path(const double (&S)[N][N], const double (&mu)[N], const RuleDev& R, const FieldDev& F,
                               double radius_eps, double sigma_obs, const FactorOut& out, int64_t b, int64_t f,
                               int64_t knot) {
   constexpr int T = N * (N + 1) / 2;
@@ -662,7 +662,14 @@ factor_grads_kernel(int nplans, int64_t nfac, View mean, View covs, RuleDev R, F
         for (int c = 0; c <= r; ++c) Sj[r][c] = S[r][c] + (r == c ? 1e-10 : 0.0);
       ok = chol_fast<N, false>(Sj, L, dinv);
     }
-    if (!ok) factor_eigh_path<N, P>(S, mu, R, F, radius_eps, sigma_obs, out, b, f, knot);
+    if (!ok) {  // the eigh root (a separate fix-up kernel keeps its registers off this one)
+      if (out.eigh_list) {
+        out.eigh_list[1 + atomicAdd(out.eigh_list, 1)] = (int)(b * nfac + f);
+      } else {
+        atomicMax(out.status + b, GVP_ERR_SQRT);
+        atomicMin(out.where + b, (int)knot);
+      }
+    }
     return ok;
   };
   // planar clouds: the clear-cloud test below needs only S[:2,:2], so the
@@ -885,6 +892,29 @@ factor_grads_kernel(int nplans, int64_t nfac, View mean, View covs, RuleDev R, F
   out.e_psi(b, f, 0) = e0 > 0.0 ? e0 : 0.0;  // e_psi = max(e0, 0) (factors.py:218-224)
 }
 
+// Factors whose covariance needed gaussian_sqrt's eigh root (listed by
+// factor_grads_kernel): the whole factor through factor_eigh_path.
+template <int N, int P>
+__global__ void factor_eigh_kernel(int64_t nfac, View mean, View covs, RuleDev R, FieldDev F, double radius_eps,
+                                   double sigma_obs, FactorOut out) {
+  const int cnt = out.eigh_list[0];
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < cnt; t += gridDim.x * blockDim.x) {
+    const int64_t code = out.eigh_list[1 + t], b = code / nfac, f = code % nfac, knot = f + 1;
+    FieldDev Fb = F;
+    if (Fb.plan_map) Fb.corners += (int64_t)Fb.plan_map[b] * Fb.map_stride;
+    double mu[N], S[N][N];
+    const double* mp = mean.p + knot * mean.sk + b * mean.sp;
+    const double* cp = covs.p + knot * covs.sk + b * covs.sp;
+#pragma unroll
+    for (int r = 0; r < N; ++r) mu[r] = mp[r * mean.se];
+#pragma unroll
+    for (int r = 0; r < N; ++r)
+#pragma unroll
+      for (int c = 0; c <= r; ++c) S[r][c] = cp[tri_idx(r, c) * covs.se];
+    factor_eigh_path<N, P>(S, mu, R, Fb, radius_eps, sigma_obs, out, b, f, knot);
+  }
+}
+
 template <int N, int P>
 static int grads_impl(int nplans, int64_t K, const View& mean, const View& covs, const RuleDev& R,
                       const FieldDev& F, double re, double so, const FactorOut& out,
@@ -936,6 +966,7 @@ static int grads_impl(int nplans, int64_t K, const View& mean, const View& covs,
     }
     launch(std::false_type{});
   };
+  if (out.eigh_list) GVP_CUDA(cudaMemsetAsync(out.eigh_list, 0, sizeof(int), s));
   // specialisations for the configurations of SURVEY §8d: 13 projections
   // (k_q = 3, P = 2) and 57 (k_q = 5, P = 2); anything else takes the loop
   if (host && R.nproj == 13 && (int64_t)host->h_proj.size() == 13 * P)
@@ -945,6 +976,10 @@ static int grads_impl(int nplans, int64_t K, const View& mean, const View& covs,
   else
     go(std::integral_constant<int, 0>{});
   GVP_CUDA(cudaGetLastError());
+  if (out.eigh_list) {  // one small grid; exits at once when no factor needed the eigh root
+    factor_eigh_kernel<N, P><<<148, 64, 0, s>>>(nfac, mean, covs, R, F, re, so, out);
+    GVP_CUDA(cudaGetLastError());
+  }
   return GVP_OK;
 }
 

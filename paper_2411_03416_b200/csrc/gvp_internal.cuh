@@ -110,6 +110,10 @@ struct FactorOut {
   unsigned long long* oob;  // per plan
   int* status;              // per plan (0 ok, GVP_ERR_*)
   int* where;               // per plan (atomicMin'd factor index)
+  // gaussian_sqrt's eigh fallback: [0] = count, then b * nfac + f of every factor
+  // whose Cholesky (and jitter retry) failed, finished by the eigh fix-up kernel.
+  // nullptr: report GVP_ERR_SQRT instead. Size 1 + nplans * nfac.
+  int* eigh_list = nullptr;
 };
 int launch_factor_grads(int nplans, int64_t nknots, int n, const View& mean, const View& covs,
                         const RuleDev& rule, const FieldDev& field, double radius_eps,

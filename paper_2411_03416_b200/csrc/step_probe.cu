@@ -43,6 +43,12 @@
 namespace gvp {
 namespace v4 {
 
+#ifdef GVP_PROBE_PROFILE
+// diagnostic build only (-DGVP_PROBE_PROFILE): per-role cycles spent working vs
+// waiting (TMA + CTA barrier) in probe_split_kernel, summed over lane-0 threads
+__device__ unsigned long long g_probe_prof[8];
+#endif
+
 using v3::PlanSt;
 using v3::Pick;
 using v3::T_;
@@ -107,9 +113,85 @@ struct Args {
   int rotate;  // split kernel: rotate the warp roles by the CTA's SM residency slot
 };
 
+// Branch-free pieces of the per-knot Cholesky: the library's double rsqrt and
+// frexp carry special-value slow paths (a CALL under a convergence barrier in
+// the hot loop); pivots here are positive normal numbers (anything else already
+// fails the SPD test, whose value is then irrelevant), so: the hardware
+// approximation + two Newton steps (~1 ulp), and exponent extraction from the bits.
+GVP_DEV double rsqrt_nb(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  const double h = 0.5 * x;
+  y = y * fma(-h * y, y, 1.5);
+  y = y * fma(-h * y, y, 1.5);
+  return y;
+}
+GVP_DEV double frexp_pos(double x, int* e) {  // x > 0 normal: x = m 2^e, m in [0.5, 1)
+  const long long bits = __double_as_longlong(x);
+  *e = (int)((bits >> 52) & 0x7ff) - 1022;
+  return __longlong_as_double((bits & ~(0x7ffLL << 52)) | (1022LL << 52));
+}
+template <int N>
+GVP_DEV bool chol_inv_nb(const double (&A)[T_<N>], double (&Li)[T_<N>], double& pivprod) {
+  double L[T_<N>], inv[N];
+  bool ok = true;
+  pivprod = 1.0;
+#pragma unroll
+  for (int j = 0; j < N; ++j) {
+    double s = A[tri_idx(j, j)];
+#pragma unroll
+    for (int k = 0; k < j; ++k) s -= L[tri_idx(j, k)] * L[tri_idx(j, k)];
+    ok = ok && (s > 0.0);
+    const double r = rsqrt_nb(s);
+    const double d = s * r;
+    ok = ok && (d > kPivotFloor);
+    L[tri_idx(j, j)] = d;
+    inv[j] = r;
+    pivprod *= d;
+#pragma unroll
+    for (int i = j + 1; i < N; ++i) {
+      double t = A[tri_idx(i, j)];
+#pragma unroll
+      for (int k = 0; k < j; ++k) t -= L[tri_idx(i, k)] * L[tri_idx(j, k)];
+      L[tri_idx(i, j)] = t * r;
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < N; ++c) {
+    Li[tri_idx(c, c)] = inv[c];
+#pragma unroll
+    for (int r = c + 1; r < N; ++r) {
+      double t = 0.0;
+#pragma unroll
+      for (int k = c; k < r; ++k) t += L[tri_idx(r, k)] * Li[tri_idx(k, c)];
+      Li[tri_idx(r, c)] = -t * inv[r];
+    }
+  }
+  return ok;
+}
+
 template <int N>
 GVP_DEV double symv(const double (&A)[T_<N>], int r, int c) {
   return r >= c ? A[tri_idx(r, c)] : A[tri_idx(c, r)];
+}
+
+// TMA issue of knot i's stage (s: ring step) for the split probe kernels
+template <int N, int L, bool KS>
+GVP_DEV void split_issue(const Args& a, double* smem, uint64_t* bars, int64_t b0, int64_t s, int64_t i) {
+  using LO = Lay<N, L, KS, true>;
+  constexpr int Pb = LO::Pb, Kb = LO::Kb;
+  double* st = smem + (s % LO::NS) * LO::STAGE;
+  uint64_t* bar = &bars[s % LO::NS];
+  v3::mbar_expect_tx(bar, LO::TX);
+  const int ck = KS ? 0 : (int)b0;
+  const int io = (int)(i > 0 ? i - 1 : 0);  // off-diagonal block (i-1, i)
+  double* pr = st + LO::OFF_PRIOR;
+  v3::tma3(pr + LO::R_KD * Kb, &a.m_kd, ck, 0, (int)i, bar);
+  v3::tma3(pr + LO::R_KO * Kb, &a.m_ko, ck, 0, io, bar);
+  v3::tma3(st + LO::R_LD * Pb, &a.m_ld, (int)b0, 0, (int)i, bar);
+  v3::tma3(st + LO::R_GD * Pb, &a.m_gd, (int)b0, 0, (int)i, bar);
+  v3::tma3(st + LO::R_E * Pb, &a.m_e, (int)b0, 0, (int)i, bar);
+  v3::tma3(st + LO::R_LO * Pb, &a.m_lo, (int)b0, 0, io, bar);
 }
 
 // Four warps per 32 lane slots, one chain stage each:
@@ -212,10 +294,22 @@ __global__ void __launch_bounds__(128, probe_minb<N>()) probe_split_kernel(const
 
     if (tid == 0)
       for (int s = 0; s < LO::AH && s < K; ++s) issue(sbase + s, s);
+#ifdef GVP_PROBE_PROFILE
+    long long prof_work = 0, prof_wait = 0, tprev = 0;
+#endif
     for (int64_t st_ = 0; st_ <= K; ++st_) {
       const int64_t s = sbase + st_;
+#ifdef GVP_PROBE_PROFILE
+      const long long tp0 = clock64();
+#endif
       if (st_ < K) wait_slot(s);
       __syncthreads();  // step st_-1 complete: ring / stage slots may be reused
+#ifdef GVP_PROBE_PROFILE
+      const long long tp1 = clock64();
+      if (st_ > 0) prof_work += tp0 - tprev;
+      prof_wait += tp1 - tp0;
+      tprev = tp1;
+#endif
       if (tid == 0 && st_ + LO::AH < K) issue(s + LO::AH, st_ + LO::AH);
       if (!tangent) {
         // ---------------------------- Schur producer, knot i = st_
@@ -264,14 +358,14 @@ __global__ void __launch_bounds__(128, probe_minb<N>()) probe_split_kernel(const
           }
         }
         double pp;
-        if (!v3::chol_inv<N>(M, Li, pp)) {
+        if (!chol_inv_nb<N>(M, Li, pp)) {
           ffail[chain * 32 + lcol] = (int)i;
           alive = false;
           continue;
         }
         if (chain == 0) {  // log det = 2 log prod(pivots), product kept normalised
           int ex;
-          pm = frexp(pm * pp, &ex);
+          pm = frexp_pos(pm * pp, &ex);
           acc_e += ex;
         } else {
 #pragma unroll
@@ -397,6 +491,12 @@ __global__ void __launch_bounds__(128, probe_minb<N>()) probe_split_kernel(const
       }
     }
     sbase += K;
+#ifdef GVP_PROBE_PROFILE
+    if (lcol == 0) {
+      atomicAdd(&g_probe_prof[role * 2], (unsigned long long)prof_work);
+      atomicAdd(&g_probe_prof[role * 2 + 1], (unsigned long long)prof_wait);
+    }
+#endif
 
     // ---------------- combine the chains: the mean chain fails first
     // (proximal_update raises before gbp_marginals, optimizer.py:203-207)
@@ -581,13 +681,13 @@ __global__ void __launch_bounds__(64) probe_fused_kernel(const __grid_constant__
           }
       }
       double pp;
-      if (!v3::chol_inv<N>(M, Li, pp)) {
+      if (!chol_inv_nb<N>(M, Li, pp)) {
         fail_knot = (int)i;
         continue;
       }
       if (role == 0) {
         int ex;
-        pm = frexp(pm * pp, &ex);
+        pm = frexp_pos(pm * pp, &ex);
         acc_e += ex;
       }
       double X[N2];
@@ -748,7 +848,7 @@ __global__ void logdet_fwd_packed_kernel(int B, int64_t K, int64_t Bp, const dou
       }
     }
     double pp;
-    if (!v3::chol_inv<N>(M, Li, pp)) {
+    if (!chol_inv_nb<N>(M, Li, pp)) {
       out[b] = NAN;
       if (status) {
         status[b] = GVP_ERR_NOT_SPD;
@@ -757,7 +857,7 @@ __global__ void logdet_fwd_packed_kernel(int B, int64_t K, int64_t Bp, const dou
       return;
     }
     int ex;
-    pm = frexp(pm * pp, &ex);
+    pm = frexp_pos(pm * pp, &ex);
     acc_e += ex;
   }
   out[b] = 2.0 * (log(pm) + (double)acc_e * 0.6931471805599453);
@@ -848,7 +948,7 @@ int launch_probe(const V2Launch& q, const int L, cudaStream_t s) {
   // q.fill (auto lanes): the split CTA's time is its step latency times its
   // rounds, nearly independent of how many CTAs share the SM, so spread the
   // plans over every resident CTA slot; each plan then gets 32 / ppc lanes
-  auto fill_ppc = [&](const void* fn, size_t bytes) {
+  auto fill_ppc = [&](const void* fn, size_t bytes, int threads) {
     if (!q.fill) return;
     static int nsm = 0;
     if (!nsm) {
@@ -857,7 +957,7 @@ int launch_probe(const V2Launch& q, const int L, cudaStream_t s) {
       cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     }
     int occ = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, 128, bytes) != cudaSuccess || occ < 1) occ = 1;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, threads, bytes) != cudaSuccess || occ < 1) occ = 1;
     const int64_t slots = (int64_t)occ * std::max(nsm, 1);
     // even: a TMA box must start on a 16-byte boundary of the plan-minor rows
     const int64_t want = (q.nplans + slots - 1) / slots;
@@ -865,11 +965,11 @@ int launch_probe(const V2Launch& q, const int L, cudaStream_t s) {
   };
 #define GVP_V4_KS(NN, LL, KK)                                                                          \
   {                                                                                                    \
-    if (split) {                                                                                       \
+    if (split) {                                                                                \
       using LOH = v4::Lay<NN, LL, KK, true>;                                                           \
       GVP_CUDA(cudaFuncSetAttribute(v4::probe_split_kernel<NN, LL, KK>,                                \
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)LOH::BYTES));    \
-      fill_ppc((const void*)v4::probe_split_kernel<NN, LL, KK>, LOH::BYTES);                           \
+      fill_ppc((const void*)v4::probe_split_kernel<NN, LL, KK>, LOH::BYTES, 128);                      \
       v4::probe_split_kernel<NN, LL, KK><<<(unsigned)((q.nplans + a.ppc - 1) / a.ppc), 128, LOH::BYTES, s>>>(a); \
     } else {                                                                                           \
       using LOH = v4::Lay<NN, LL, KK, false>;                                                          \
@@ -904,3 +1004,15 @@ int launch_probe(const V2Launch& q, const int L, cudaStream_t s) {
 }
 
 }  // namespace gvp
+
+#ifdef GVP_PROBE_PROFILE
+// (diagnostic build) out[2 role + {0,1}] = cycles working / waiting since the last call
+extern "C" int gvp_probe_profile(double* out) {
+  unsigned long long h[8];
+  GVP_CUDA(cudaMemcpyFromSymbol(h, gvp::v4::g_probe_prof, sizeof(h)));
+  const unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  GVP_CUDA(cudaMemcpyToSymbol(gvp::v4::g_probe_prof, z, sizeof(z)));
+  for (int i = 0; i < 8; ++i) out[i] = (double)h[i];
+  return GVP_OK;
+}
+#endif

@@ -14,7 +14,7 @@
 from __future__ import annotations
 
 import time
-from dataclasses import dataclass, field
+from dataclasses import dataclass, replace, field
 
 import numpy as np
 
@@ -386,6 +386,56 @@ class BatchResult:
     wall_time_ms: float
 
 
+def batch_problem(sys_ltv: LTVSystem, x0s, goals, q_c: float, sigma_b: float, cfg: OptimizerConfig):
+    """The priors of B plans that share the system, q_c and sigma_b (SURVEY §8e
+    batch axis) without B prior assemblies: the anchored precision does not
+    depend on the boundary states, the information vector only at the two
+    anchor knots (prior.py:140-150), and the anchored mean / flow are affine in
+    them — so one prior (plan 0's) plus 2n unit responses of the mean solve
+    (on the device) give every plan's. Returns (prior of plan 0, info (B,K,n),
+    prior mean (B,K,n), initial mean (B,K,n))."""
+    x0s = np.atleast_2d(np.asarray(x0s, dtype=np.float64))
+    goals = np.atleast_2d(np.asarray(goals, dtype=np.float64))
+    B = max(len(x0s), len(goals))
+    x0s = np.broadcast_to(x0s, (B, x0s.shape[1]))
+    goals = np.broadcast_to(goals, (B, goals.shape[1]))
+    base = assemble_prior(sys_ltv, x0s[0], goals[0], q_c, sigma_b)
+    K, n = base.nsteps + 1, base.n
+    anchor = np.eye(n) / sigma_b ** 2
+    d0, dg = x0s - x0s[0], goals - goals[0]
+    info = np.repeat(base.info.reshape(1, K, n), B, axis=0)
+    info[:, 0, :] += d0 @ anchor.T
+    info[:, -1, :] += dg @ anchor.T
+    # anchored-mean responses to a unit change of each start / goal coordinate
+    from .prior import anchored_mean
+
+    resp0, respg = np.zeros((n, K, n)), np.zeros((n, K, n))
+    for j in range(n):
+        e = np.zeros((K, n))
+        e[0] = anchor[:, j]
+        resp0[j] = anchored_mean(base.prec, e.reshape(-1)).reshape(K, n)
+        e[0], e[-1] = 0.0, anchor[:, j]
+        respg[j] = anchored_mean(base.prec, e.reshape(-1)).reshape(K, n)
+    pmean = (base.mean.reshape(1, K, n) + np.einsum("bj,jkn->bkn", d0, resp0)
+             + np.einsum("bj,jkn->bkn", dg, respg))
+    if cfg.init_mean is not None:
+        init = np.repeat(initial_mean(base, cfg).reshape(1, K, n), B, axis=0)
+    elif cfg.init not in ("flow", "prior"):  # initial_mean's straight line, every plan at once
+        a = np.linspace(0.0, 1.0, K).reshape(1, K, 1)
+        init = (1.0 - a) * x0s[:, None, :] + a * goals[:, None, :]
+    elif cfg.init == "prior":
+        init = pmean.copy()
+    else:  # the flow is affine in x0: propagate the start offsets through the transitions
+        flow = np.repeat(base.flow_mean.reshape(1, K, n), B, axis=0)
+        dflow = d0.copy()
+        for i in range(K - 1):
+            dflow = dflow @ np.asarray(base.phis[i]).T
+            flow[:, i + 1] += dflow
+        flow[:, 0] += d0
+        init = flow
+    return base, info, pmean, init
+
+
 def run_pgvimp_batch(sys_ltv: LTVSystem, env: Environment | None, cfg: OptimizerConfig, x0s, goals,
                      q_c: float, sigma_b: float, spec_lanes: int = 0) -> BatchResult:
     """Many independent plans on one GPU: same system, map and settings, per
@@ -393,22 +443,14 @@ def run_pgvimp_batch(sys_ltv: LTVSystem, env: Environment | None, cfg: Optimizer
     out with their status; the batch never aborts."""
     cfg.validate()
     t0 = time.perf_counter()
-    x0s = np.atleast_2d(np.asarray(x0s, dtype=np.float64))
-    goals = np.atleast_2d(np.asarray(goals, dtype=np.float64))
-    B = max(len(x0s), len(goals))
-    x0s = np.broadcast_to(x0s, (B, x0s.shape[1]))
-    goals = np.broadcast_to(goals, (B, goals.shape[1]))
-    priors = [assemble_prior(sys_ltv, x0s[b], goals[b], q_c, sigma_b) for b in range(B)]
-    K, n = priors[0].nsteps + 1, priors[0].n
+    base, info, pmean, init = batch_problem(sys_ltv, x0s, goals, q_c, sigma_b, cfg)
+    B, K, n = info.shape
     rule = smolyak_rule(cfg.k_q, n)
     sdf = env.sdf if env is not None else far_field()
     model = env.model if env is not None else CollisionModel(0.0, 1.0)
     eng = PlanBatch(B, K, n, sdf, model, rule, cfg, shared_prior=True, spec_lanes=spec_lanes)
     try:
-        eng.load(priors[0].prec.diag_stack, priors[0].prec.off_stack,
-                 np.stack([p.info.reshape(K, n) for p in priors]),
-                 np.stack([p.mean.reshape(K, n) for p in priors]),
-                 np.stack([initial_mean(p, cfg).reshape(K, n) for p in priors]))
+        eng.load(base.prec.diag_stack, base.prec.off_stack, info, pmean, init)
         eng.run()
         st = eng.state()
         sm = eng.summary()

@@ -84,8 +84,18 @@ def test_batch_equals_single_runs(P):
     goals[:, :2] += rng.uniform(-0.3, 0.3, size=(6, 2))
     batch = P.run_pgvimp_batch(sys_ltv, env, cfg, np.zeros(4), goals, 1.0, 1e-3)
     assert np.all(batch.status == 0)
+    # the batch's own per-plan priors (optimizer.batch_problem); each plan alone
+    from dataclasses import replace
+
+    from paper_2411_03416_b200.optimizer import batch_problem
+
+    base, info, pmean, _ = batch_problem(sys_ltv, np.zeros(4), goals, 1.0, 1e-3, cfg)
+    own = P.assemble_prior(sys_ltv, np.zeros(4), goals[3], 1.0, 1e-3)  # vs a separate assembly
+    assert np.abs(info[3].reshape(-1) - own.info).max() <= 1e-15 * np.abs(own.info).max()
+    assert np.abs(pmean[3].reshape(-1) - own.mean).max() <= 1e-6 * np.abs(own.mean).max()
     for b in range(6):
-        single = P.run_pgvimp(sys_ltv, env, cfg, np.zeros(4), goals[b], 1.0, 1e-3)
+        prior_b = replace(base, info=info[b].reshape(-1), mean=pmean[b].reshape(-1), goal=goals[b])
+        single = P.run_pgvimp(sys_ltv, env, cfg, np.zeros(4), goals[b], 1.0, 1e-3, prior=prior_b)
         assert batch.iterations[b] == single.iterations
         assert np.array_equal(batch.mean[b].reshape(-1), single.final.mean)
         assert np.array_equal(batch.covs[b], np.stack(single.marginals.covs))
