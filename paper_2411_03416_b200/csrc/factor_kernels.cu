@@ -654,13 +654,10 @@ factor_grads_kernel(int nplans, int64_t nfac, View mean, View covs, RuleDev R, F
   // false: the factor went through the eigh root (factor_eigh_path) and is done
   auto gsqrt = [&]() -> bool {
     bool ok = chol_fast<N, false>(S, L, dinv);
-    if (!ok) {
-      double Sj[N][N];
+    if (!ok) {  // (in place: the clear-cloud bound below then covers the jittered cloud)
 #pragma unroll
-      for (int r = 0; r < N; ++r)
-#pragma unroll
-        for (int c = 0; c <= r; ++c) Sj[r][c] = S[r][c] + (r == c ? 1e-10 : 0.0);
-      ok = chol_fast<N, false>(Sj, L, dinv);
+      for (int r = 0; r < N; ++r) S[r][r] += 1e-10;
+      ok = chol_fast<N, false>(S, L, dinv);
     }
     if (!ok) {  // the eigh root (a separate fix-up kernel keeps its registers off this one)
       if (out.eigh_list) {
@@ -672,10 +669,7 @@ factor_grads_kernel(int nplans, int64_t nfac, View mean, View covs, RuleDev R, F
     }
     return ok;
   };
-  // planar clouds: the clear-cloud test below needs only S[:2,:2], so the
-  // Cholesky is deferred until a lane needs its sigma points
-  constexpr bool LAZY = NP > 0 && P == 2;
-  if (!LAZY && !gsqrt()) return;
+  if (!gsqrt()) return;
 
   // ---- quadrature over distinct position projections
   double e0 = 0.0, E1[N], E2[T];
@@ -697,9 +691,8 @@ factor_grads_kernel(int nplans, int64_t nfac, View mean, View covs, RuleDev R, F
       // spectral norm of L[:2,:2]: |L_pp xi| <= sqrt(lambda_max(L_pp L_pp')) |xi|, and
       // L_pp L_pp' = S[:2,:2] (the Cholesky's leading block), closed form; up to sqrt(2)
       // tighter than the Frobenius bound for a round cloud. (1 + 1e-12) covers rounding.
-      // (+1e-10: a jitter retry of the deferred Cholesky raises lambda_max by at most that)
       const double a = S[0][0], c = S[1][1], h = 0.5 * (a - c);
-      fr = (0.5 * (a + c) + sqrt(h * h + S[1][0] * S[1][0]) + (LAZY ? 1e-10 : 0.0)) * (1.0 + 1e-12);
+      fr = (0.5 * (a + c) + sqrt(h * h + S[1][0] * S[1][0])) * (1.0 + 1e-12);
     } else {
 #pragma unroll
       for (int r = 0; r < P; ++r)
@@ -722,7 +715,6 @@ factor_grads_kernel(int nplans, int64_t nfac, View mean, View covs, RuleDev R, F
                                  : interp3<false>(F, mu[0], mu[1], mu[P - 1], oc);
       if (dc - F.lip * Rad - radius_eps > 1e-9) {
         if (!inside) {  // bounds test of every projection, as the quadrature below does it
-          if (LAZY && !gsqrt()) return;
 #pragma unroll
           for (int j = 0; j < NP; ++j) {
             double pos[P];
@@ -746,7 +738,6 @@ factor_grads_kernel(int nplans, int64_t nfac, View mean, View covs, RuleDev R, F
         return;
       }
     }
-    if (LAZY && !gsqrt()) return;
     double psi[NP];
     bool any_hit = false;
     if (P == 2 && __all_sync(__activemask(), inside)) {

@@ -21,6 +21,9 @@ for st in $STAGES; do
     ncuprobe)
       timeout 900 ncu --set full --import-source on --clock-control none --kernel-name regex:probe_split \
         --launch-skip 3 --launch-count 1 -o $O/${TAG}_probe -f python bench.py $SHORT > $O/${TAG}_ncuprobe.log 2>&1 ;;
+    ncucommit)
+      timeout 900 ncu --set full --import-source on --clock-control none --kernel-name regex:commit_kernel \
+        --launch-skip 3 --launch-count 1 -o $O/${TAG}_commit -f python bench.py $SHORT > $O/${TAG}_ncucommit.log 2>&1 ;;
     ncufactor)
       timeout 900 ncu --set full --import-source on --clock-control none --kernel-name regex:factor_grads \
         --launch-skip 5 --launch-count 1 -o $O/${TAG}_factor -f python bench.py $SHORT > $O/${TAG}_ncufactor.log 2>&1 ;;
