@@ -140,6 +140,20 @@ int gvp_select_step_size(const double* mean, const double* diag, const double* o
                          double* crosses, double* probe_log, int32_t max_probes,
                          int32_t* nprobes, int64_t* where);
 
+/* The same, given the log det of the current precision (ld_cur; NaN: computed
+ * here, as gvp_select_step_size does) and returning the accepted state's log
+ * det (*ld_next; NaN where the path does not produce it): a host loop carries
+ * one iteration's into the next (kl_joint's logdet_cur, entropy_of) instead of
+ * two extra log det sweeps per iteration. */
+int gvp_select_step_size_ld(const double* mean, const double* diag, const double* off,
+                            const double* kdiag, const double* koff, const double* info,
+                            const double* g_mu, const double* gdiag, const double* goff,
+                            int64_t nblocks, int32_t n, double temp, double kl_bound,
+                            double beta_min, double beta_max, double* beta, double* kl,
+                            double* out_mean, double* out_diag, double* out_off, double* covs,
+                            double* crosses, double* probe_log, int32_t max_probes,
+                            int32_t* nprobes, int64_t* where, double ld_cur, double* ld_next);
+
 /* Candidate lanes (1, 2, 4, 8, 16) gvp_select_step_size probes concurrently;
  * the beta sequence is the reference's for any value (default 16). */
 int gvp_set_step_lanes(int32_t lanes);

@@ -68,6 +68,10 @@ _SIGS = {
                                        C.c_int32, C.c_double, C.c_double, C.c_double, C.c_double,
                                        _dp, _dp, _dp, _dp, _dp, _dp, _dp, _dp, C.c_int32, _i32p,
                                        _i64p]),
+    "gvp_select_step_size_ld": (C.c_int, [_dp, _dp, _dp, _dp, _dp, _dp, _dp, _dp, _dp, C.c_int64,
+                                          C.c_int32, C.c_double, C.c_double, C.c_double, C.c_double,
+                                          _dp, _dp, _dp, _dp, _dp, _dp, _dp, _dp, C.c_int32, _i32p,
+                                          _i64p, C.c_double, _dp]),
     "gvp_engine_create": (C.c_int, [C.POINTER(C.c_void_p), C.c_int32, C.c_int64, C.c_int32,
                                     C.c_int32, _dp, C.c_int32, _i64p, _dp, C.c_double, C.c_double,
                                     C.c_double, _dp, _dp, C.c_int64, C.POINTER(PlanConfig)]),

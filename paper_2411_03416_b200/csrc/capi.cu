@@ -61,6 +61,9 @@ struct Context {
   Arena arena;
   Field field;
   Rule rule;
+  // gvp_select_step_size_ld: a known log det of the current precision (NaN:
+  // compute it) and the accepted state's log det, for the call in progress
+  double ld_in = NAN, ld_out = NAN;
   int init() {
     if (stream) return GVP_OK;
     int ndev = 0;
@@ -529,9 +532,9 @@ int wide_step_call(Context& C, const double* mean, const double* diag, const dou
   double* wscr;
   GVP_TRY(C.arena.get(60, (size_t)wide_scratch_doubles(1, K, n), &wscr));
   // scal: 0 beta (in: previous / fixed, out: accepted), 1 kl, 2 ld_next, 4 temp, 5 ld_cur
-  const double init[6] = {fixed ? beta_fixed : NAN, 0.0, 0.0, 0.0, temp, 0.0};
+  const double init[6] = {fixed ? beta_fixed : NAN, 0.0, 0.0, 0.0, temp, std::isfinite(C.ld_in) ? C.ld_in : 0.0};
   GVP_TRY(h2d(b.scal, init, 6, s));
-  if (!fixed) {  // log det of the current precision (kl_joint's logdet_cur, forward Schur)
+  if (!fixed && !std::isfinite(C.ld_in)) {  // log det of the current precision (kl_joint's logdet_cur)
     GVP_TRY(launch_wide_logdet(1, K, n, pb.diag, pb.off, b.scal + 5, nullptr, b.st, b.st + 1, s));
     int64_t w0 = -1;
     if (fetch_status(C, b.st, &w0) != GVP_OK) {
@@ -571,8 +574,8 @@ int wide_step_call(Context& C, const double* mean, const double* diag, const dou
     }
     return stw[0];
   }
-  double sc[2];
-  GVP_TRY(d2h(sc, b.scal, 2, s));
+  double sc[3];
+  GVP_TRY(d2h(sc, b.scal, 3, s));
   GVP_TRY(d2h(out_mean, b.omean, K * n, s));
   GVP_TRY(d2h(out_diag, b.odiag, K * B2, s));
   GVP_TRY(d2h(out_off, b.ooff, (K - 1) * B2, s));
@@ -581,6 +584,7 @@ int wide_step_call(Context& C, const double* mean, const double* diag, const dou
   GVP_CUDA(cudaStreamSynchronize(s));
   if (beta) *beta = sc[0];
   if (kl) *kl = sc[1];
+  if (!fixed) C.ld_out = sc[2];
   if (where) *where = -1;
   return GVP_OK;
 }
@@ -691,8 +695,8 @@ static int select_step_size_v1(const double* mean, const double* diag, const dou
     }
     return stw[0];
   }
-  double sc[2];
-  GVP_TRY(d2h(sc, b.scal, 2, s));
+  double sc[3];
+  GVP_TRY(d2h(sc, b.scal, 3, s));
   GVP_TRY(d2h(out_mean, b.omean, K * n, s));
   GVP_TRY(d2h(out_diag, b.odiag, K * B2, s));
   GVP_TRY(d2h(out_off, b.ooff, (K - 1) * B2, s));
@@ -714,6 +718,15 @@ extern "C" int gvp_set_step_lanes(int32_t lanes) {
   return GVP_OK;
 }
 
+static int select_step_impl(Context& C, const double* mean, const double* diag, const double* off,
+                            const double* kdiag, const double* koff, const double* info,
+                            const double* g_mu, const double* gdiag, const double* goff,
+                            int64_t nblocks, int32_t n, double temp, double kl_bound,
+                            double beta_min, double beta_max, double* beta, double* kl,
+                            double* out_mean, double* out_diag, double* out_off,
+                            double* covs, double* crosses, double* probe_log,
+                            int32_t max_probes, int32_t* nprobes, int64_t* where);
+
 extern "C" int gvp_select_step_size(const double* mean, const double* diag, const double* off,
                                     const double* kdiag, const double* koff, const double* info,
                                     const double* g_mu, const double* gdiag, const double* goff,
@@ -724,6 +737,41 @@ extern "C" int gvp_select_step_size(const double* mean, const double* diag, cons
                                     int32_t max_probes, int32_t* nprobes, int64_t* where) {
   Context& C = ctx();
   std::lock_guard<std::mutex> lock(C.mu);
+  C.ld_in = NAN;
+  return select_step_impl(C, mean, diag, off, kdiag, koff, info, g_mu, gdiag, goff, nblocks, n, temp, kl_bound,
+                          beta_min, beta_max, beta, kl, out_mean, out_diag, out_off, covs, crosses, probe_log,
+                          max_probes, nprobes, where);
+}
+
+extern "C" int gvp_select_step_size_ld(const double* mean, const double* diag, const double* off,
+                                       const double* kdiag, const double* koff, const double* info,
+                                       const double* g_mu, const double* gdiag, const double* goff,
+                                       int64_t nblocks, int32_t n, double temp, double kl_bound,
+                                       double beta_min, double beta_max, double* beta, double* kl,
+                                       double* out_mean, double* out_diag, double* out_off,
+                                       double* covs, double* crosses, double* probe_log,
+                                       int32_t max_probes, int32_t* nprobes, int64_t* where, double ld_cur,
+                                       double* ld_next) {
+  Context& C = ctx();
+  std::lock_guard<std::mutex> lock(C.mu);
+  C.ld_in = ld_cur;
+  C.ld_out = NAN;
+  const int r = select_step_impl(C, mean, diag, off, kdiag, koff, info, g_mu, gdiag, goff, nblocks, n, temp,
+                                 kl_bound, beta_min, beta_max, beta, kl, out_mean, out_diag, out_off, covs, crosses,
+                                 probe_log, max_probes, nprobes, where);
+  C.ld_in = NAN;
+  if (ld_next) *ld_next = C.ld_out;
+  return r;
+}
+
+static int select_step_impl(Context& C, const double* mean, const double* diag, const double* off,
+                            const double* kdiag, const double* koff, const double* info,
+                            const double* g_mu, const double* gdiag, const double* goff,
+                            int64_t nblocks, int32_t n, double temp, double kl_bound,
+                            double beta_min, double beta_max, double* beta, double* kl,
+                            double* out_mean, double* out_diag, double* out_off,
+                            double* covs, double* crosses, double* probe_log,
+                            int32_t max_probes, int32_t* nprobes, int64_t* where) {
   GVP_TRY(C.init());
   GVP_TRY(check_chain_n(n));
   if (n >= kWideMin)
@@ -800,7 +848,11 @@ extern "C" int gvp_select_step_size(const double* mean, const double* diag, cons
   GVP_TRY(launch_lam_mu(2, K, n, 2, ld, lo, mu, v, s));
   GVP_TRY(launch_marginals_packed(1, K, n, 2, ld, lo, ocov, ocr, scal + 10, st, st + 1, scr,
                                   nullptr, s));
-  GVP_TRY(launch_logdet_fwd_packed(1, K, n, 2, ld, lo, scal + 10, nullptr, st, st + 1, s));
+  if (std::isfinite(C.ld_in)) {
+    GVP_TRY(h2d(scal + 10, &C.ld_in, 1, s));
+  } else {
+    GVP_TRY(launch_logdet_fwd_packed(1, K, n, 2, ld, lo, scal + 10, nullptr, st, st + 1, s));
+  }
   int64_t w0 = -1;
   if (fetch_status(C, st, &w0) != GVP_OK) {
     if (where) *where = w0;
@@ -842,14 +894,14 @@ extern "C" int gvp_select_step_size(const double* mean, const double* diag, cons
     }
     return stw[0];
   }
-  double sc[4];
+  double sc[5];
   std::vector<double> ldo((size_t)(K * T)), covo((size_t)(K * T));
   auto narrow = [&](double* dst, const double* src, int64_t rows) -> int {
     if (rows > 0)
       GVP_CUDA(cudaMemcpy2DAsync(dst, 8, src, 16, 8, rows, cudaMemcpyDeviceToHost, s));
     return GVP_OK;
   };
-  GVP_TRY(d2h(sc, scal, 4, s));
+  GVP_TRY(d2h(sc, scal, 5, s));
   GVP_TRY(narrow(out_mean, omu, K * n));
   GVP_TRY(narrow(ldo.data(), old_, K * T));
   GVP_TRY(narrow(out_off, olo, K1 * N2));
@@ -860,6 +912,7 @@ extern "C" int gvp_select_step_size(const double* mean, const double* diag, cons
   unpack_sym(covo.data(), K, n, covs);
   *beta = sc[0];
   *kl = sc[2];
+  C.ld_out = sc[4];
   if (where) *where = -1;
   return GVP_OK;
 }

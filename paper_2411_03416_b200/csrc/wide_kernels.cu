@@ -36,6 +36,8 @@
 #include "step_common.cuh"
 #include "wide_block.cuh"
 
+#include <cooperative_groups.h>
+
 namespace gvp {
 namespace wide {
 
@@ -522,25 +524,36 @@ struct CurTr {  // the current precision Lambda and mean (trace / Mahalanobis te
   GVP_DEV double mean(int64_t i, int r) const { return a->mean(b, i, r); }
 };
 
-template <int NM, int W>
+// G > 1: one plan's search spread over a thread-block cluster of G CTAs (G x W
+// probe slots on G SMs); each CTA runs the same search state machine on the
+// whole round's results, which every CTA scatters into all the others' shared
+// memory (DSMEM) before a cluster barrier. A single wide plan (C3) otherwise
+// runs on one SM with W slots per round.
+template <int NM, int W, int G>
 __global__ void __launch_bounds__(64 * W) step_kernel(const __grid_constant__ StepArgs a) {
+  namespace cg = cooperative_groups;
   extern __shared__ __align__(16) double sm[];
+  constexpr int WG = W * G;
   const int tid = threadIdx.x, warp = tid >> 5, slot = warp >> 1, role = warp & 1;
-  const int64_t b = blockIdx.x;
+  const int g = G > 1 ? (int)cg::this_cluster().block_rank() : 0;
+  const int64_t b = blockIdx.x / G;
   const int n = exact_n<NM>(a.n);
   const int64_t K = a.K;
   WarpWs<NM> w(sm + warp * WarpWs<NM>::DOUBLES);
   double* tail = sm + 2 * W * WarpWs<NM>::DOUBLES;
   v3::PlanSt* pst = reinterpret_cast<v3::PlanSt*>(tail);  // 10 doubles
   double* r_beta = tail + 16;
-  double* r_kl = r_beta + W;
-  int* r_res = reinterpret_cast<int*>(r_kl + W);
-  int* r_fail = r_res + W;
-  int* r_on = r_fail + W;
-  double* xv = reinterpret_cast<double*>(r_on + W + (W & 1));  // per slot: trace, logdet, mahal
-  int* xf = reinterpret_cast<int*>(xv + 3 * W);                 // per slot: fail A, fail B
+  double* r_kl = r_beta + WG;
+  int* r_res = reinterpret_cast<int*>(r_kl + WG);
+  int* r_fail = r_res + WG;
+  int* r_on = r_fail + WG;
+  double* xv = reinterpret_cast<double*>(r_on + WG + (WG & 1));  // per local slot: trace, logdet, mahal
+  int* xf = reinterpret_cast<int*>(xv + 3 * W);                   // per local slot: fail A, fail B
   const int64_t per_slot = K * n * n * 2 + K * n;
-  double* scr = a.scratch + (b * W + slot) * per_slot;
+  double* scr = a.scratch + ((b * G + g) * W + slot) * per_slot;
+  auto cluster_sync = [&]() {
+    if constexpr (G > 1) cg::this_cluster().sync(); else __syncthreads();
+  };
 
   auto run = [&](double beta, bool write) {
     const double temp = a.temp[b];
@@ -581,10 +594,10 @@ __global__ void __launch_bounds__(64 * W) step_kernel(const __grid_constant__ St
     }
   };
 
-  if (a.fixed) {  // proximal_update: slot 0 only
-    if (slot == 0) run(a.beta[b], true);
+  if (a.fixed) {  // proximal_update: slot 0 of the cluster's first CTA only
+    if (slot == 0 && g == 0) run(a.beta[b], true);
     __syncthreads();
-    if (tid == 0) {
+    if (tid == 0 && g == 0) {
       const int fB = xf[1];
       a.status[b] = fB < 0 ? GVP_OK : GVP_ERR_NOT_SPD;
       a.where[b] = fB;
@@ -595,14 +608,14 @@ __global__ void __launch_bounds__(64 * W) step_kernel(const __grid_constant__ St
   v3::search_init(a, pst, 1, b, false, tid);
   __syncthreads();
   for (;;) {
-    const v3::Pick pk = v3::search_pick(a, pst, 1, W, slot, tid, false);
+    const v3::Pick pk = v3::search_pick(a, pst, 1, WG, g * W + slot, tid, false);
     if (pk.kl == 0) break;
     __syncthreads();
     if (pk.on) run(pk.beta, false);
     __syncthreads();
     if (tid < W) {
-      const int s = tid;
-      const v3::Pick ps = v3::search_pick(a, pst, 1, W, s, -1, false);
+      const int s = tid, gs = g * W + s;
+      const v3::Pick ps = v3::search_pick(a, pst, 1, WG, gs, -1, false);
       const int fA = xf[s * 2], fB = xf[s * 2 + 1];
       const int rr = fB >= 0 ? 2 : (fA >= 0 ? 1 : 0);
       double klv = 0.0;
@@ -610,19 +623,31 @@ __global__ void __launch_bounds__(64 * W) step_kernel(const __grid_constant__ St
         const double x = 0.5 * ((((xv[s * 3] + xv[s * 3 + 2]) - (double)(K * n)) + xv[s * 3 + 1]) - a.ld_cur[b]);
         klv = (0.0 > x) ? 0.0 : x;  // python max(x, 0.0): NaN stays NaN
       }
-      r_beta[s] = ps.beta;
-      r_kl[s] = klv;
-      r_res[s] = rr;
-      r_fail[s] = fB >= 0 ? fB : fA;
-      r_on[s] = ps.on ? 1 : 0;
+      for (int dst = 0; dst < G; ++dst) {  // every CTA of the cluster gets the whole round
+        double *rb = r_beta, *rk = r_kl;
+        int *rs = r_res, *rf = r_fail, *ro = r_on;
+        if constexpr (G > 1) {
+          cg::cluster_group cl = cg::this_cluster();
+          rb = cl.map_shared_rank(r_beta, dst);
+          rk = cl.map_shared_rank(r_kl, dst);
+          rs = cl.map_shared_rank(r_res, dst);
+          rf = cl.map_shared_rank(r_fail, dst);
+          ro = cl.map_shared_rank(r_on, dst);
+        }
+        rb[gs] = ps.beta;
+        rk[gs] = klv;
+        rs[gs] = rr;
+        rf[gs] = fB >= 0 ? fB : fA;
+        ro[gs] = ps.on ? 1 : 0;
+      }
     }
-    __syncthreads();
+    cluster_sync();
     if (tid == 0) v3::search_decide(a, pst, 0, pk.dbase, pk.dkl, b, false, r_beta, r_kl, r_res, r_fail, r_on);
-    __syncthreads();
+    cluster_sync();  // nobody scatters the next round into a CTA still deciding this one
   }
-  // commit: the accepted beta re-probed in write mode (deterministic: the same
-  // numbers as its probe), KL and log det of the accepted state
-  const bool ok = (b < a.B) && (!a.active || a.active[b]) && a.status[b] == GVP_OK;
+  // commit (the cluster's first CTA): the accepted beta re-probed in write mode
+  // (deterministic: the same numbers as its probe), KL and log det of the accepted state
+  const bool ok = (b < a.B) && (!a.active || a.active[b]) && a.status[b] == GVP_OK && g == 0;
   if (ok && slot == 0) run(a.beta[b], true);
   __syncthreads();
   if (ok && tid == 0) {
@@ -646,9 +671,14 @@ constexpr int slots() {
 }  // namespace wide
 
 // ---------------------------------------------------------------------- host
+// probe slots of one plan spread over a cluster of kWideCluster CTAs while the
+// batch is small (n <= 16); a large batch fills the GPU with one CTA per plan
+constexpr int kWideCluster = 4;
+static int wide_cluster(int nplans, int n) { return (n <= 16 && nplans <= 148 / kWideCluster) ? kWideCluster : 1; }
+
 int64_t wide_scratch_doubles(int nplans, int64_t K, int n) {
   const int W = n <= 16 ? wide::slots<16>() : wide::slots<32>();
-  return (int64_t)nplans * W * (K * n * n * 2 + K * n);
+  return (int64_t)nplans * W * wide_cluster(nplans, n) * (K * n * n * 2 + K * n);
 }
 
 template <class F>
@@ -708,14 +738,39 @@ int launch_wide_step(const WideStep& q, cudaStream_t s) {
   a.beta = q.beta; a.kl = q.kl; a.ld_next = q.ld_next; a.temp = q.temp; a.ld_cur = q.ld_cur;
   a.kl_bound = q.kl_bound; a.beta_min = q.beta_min; a.beta_max = q.beta_max;
   a.probe_log = q.probe_log; a.max_probes = q.max_probes; a.scratch = q.scratch; a.fixed = q.fixed ? 1 : 0;
+  const int G = wide_cluster(q.nplans, q.n);
   return wide_dispatch(q.n, [&](auto tag) -> int {
     constexpr int NM = decltype(tag)::value;
     constexpr int W = wide::slots<NM>();
-    const size_t bytes = (2 * W * wide::WarpWs<NM>::DOUBLES + 16 + 8 * W + 8) * 8;
-    GVP_CUDA(cudaFuncSetAttribute(wide::step_kernel<NM, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
-    wide::step_kernel<NM, W><<<q.nplans, 64 * W, bytes, s>>>(a);
-    GVP_CUDA(cudaGetLastError());
-    return GVP_OK;
+    auto go = [&](auto gtag) -> int {
+      constexpr int GG = decltype(gtag)::value;
+      const size_t bytes = (2 * W * wide::WarpWs<NM>::DOUBLES + 16 + 4 * W * GG + 4 * W + 8) * 8;
+      GVP_CUDA(cudaFuncSetAttribute(wide::step_kernel<NM, W, GG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)bytes));
+      if constexpr (GG == 1) {
+        wide::step_kernel<NM, W, 1><<<q.nplans, 64 * W, bytes, s>>>(a);
+      } else {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3((unsigned)(q.nplans * GG));
+        cfg.blockDim = dim3(64 * W);
+        cfg.dynamicSmemBytes = bytes;
+        cfg.stream = s;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = GG;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        GVP_CUDA(cudaLaunchKernelEx(&cfg, wide::step_kernel<NM, W, GG>, a));
+      }
+      GVP_CUDA(cudaGetLastError());
+      return GVP_OK;
+    };
+    if constexpr (NM <= 16) {
+      if (G == kWideCluster) return go(std::integral_constant<int, kWideCluster>{});
+    }
+    return go(std::integral_constant<int, 1>{});
   });
 }
 

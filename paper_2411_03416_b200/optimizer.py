@@ -123,6 +123,7 @@ class StepSelection:
     kl: float
     marginals: ChainMarginals
     probes: np.ndarray | None = None  # (nprobes, 3): beta, spd_ok, kl
+    logdet: float | None = None       # log det of next_state.prec (None: not produced)
 
 
 def _step_arrays(cur, prior, g_mu, g_sigma):
@@ -163,22 +164,26 @@ def kl_joint(nxt: JointGaussian, cur: JointGaussian, nxt_marginals: ChainMargina
 
 def select_step_size(cur: JointGaussian, prior: DiscretePrior, g_mu: np.ndarray,
                      g_sigma: BlockTridiagonalMatrix, cfg: OptimizerConfig, temp: float,
-                     max_probes: int = 64) -> StepSelection:
+                     max_probes: int = 64, logdet_cur: float | None = None) -> StepSelection:
     """Largest feasible beta in [beta_min, beta_max] by bisection to 1e-3
-    relative width (optimizer.py:188-231); the whole search runs on device."""
+    relative width (optimizer.py:188-231); the whole search runs on device.
+    logdet_cur (optional): log det of cur.prec when the caller already has it
+    (the previous step's `logdet`), saving a sweep; the result carries the
+    accepted state's log det where the device path produces it."""
     lib = N.load()
     K, n = cur.nblocks, cur.block_size
     arrs = _step_arrays(cur, prior, g_mu, g_sigma)
-    beta, kl = np.zeros(1), np.zeros(1)
+    beta, kl, ld_next = np.zeros(1), np.zeros(1), np.full(1, np.nan)
     om, od, oo = np.empty((K, n)), np.empty((K, n, n)), np.empty((max(K - 1, 0), n, n))
     cv, cr = np.empty((K, n, n)), np.empty((max(K - 1, 0), n, n))
     plog = np.zeros((max_probes, 3))
     nprobes = np.zeros(1, dtype=np.int32)
     where = np.zeros(1, dtype=np.int64)
-    code = N.check(lib.gvp_select_step_size(
+    code = N.check(lib.gvp_select_step_size_ld(
         *[N.ptr(a) for a in arrs], K, n, float(temp), float(cfg.kl_bound), float(cfg.beta_min),
         float(cfg.beta_max), N.ptr(beta), N.ptr(kl), N.ptr(om), N.ptr(od), N.ptr(oo), N.ptr(cv),
-        N.ptr(cr), N.ptr(plog), max_probes, N.ptr(nprobes), N.ptr(where)), "select_step_size")
+        N.ptr(cr), N.ptr(plog), max_probes, N.ptr(nprobes), N.ptr(where),
+        float("nan") if logdet_cur is None else float(logdet_cur), N.ptr(ld_next)), "select_step_size")
     if code == N.GVP_ERR_NO_FEASIBLE_STEP:
         raise RuntimeError(f"no feasible step size at beta_min={cfg.beta_min} (KL bound {cfg.kl_bound})")
     if code == N.GVP_ERR_NOT_SPD:
@@ -187,7 +192,8 @@ def select_step_size(cur: JointGaussian, prior: DiscretePrior, g_mu: np.ndarray,
     return StepSelection(beta=float(beta[0]),
                          next_state=JointGaussian(mean=om.reshape(-1), prec=BlockTridiagonalMatrix(od, oo)),
                          kl=float(kl[0]), marginals=ChainMarginals.from_stacks(cv, cr),
-                         probes=plog[:min(int(nprobes[0]), max_probes)].copy())
+                         probes=plog[:min(int(nprobes[0]), max_probes)].copy(),
+                         logdet=float(ld_next[0]) if np.isfinite(ld_next[0]) else None)
 
 
 def entropy_of(prec: BlockTridiagonalMatrix) -> float:
@@ -197,8 +203,10 @@ def entropy_of(prec: BlockTridiagonalMatrix) -> float:
 def cost_breakdown(cur: JointGaussian, prior: DiscretePrior, temp: float,
                    marginals: ChainMarginals | None = None,
                    factor_values: list | None = None, env: Environment | None = None,
-                   rule: QuadratureRule | None = None, threads: int = 1) -> CostBreakdown:
-    """(prior, collision, -T H) costs of an iterate (optimizer.py:238-277)."""
+                   rule: QuadratureRule | None = None, threads: int = 1,
+                   logdet: float | None = None) -> CostBreakdown:
+    """(prior, collision, -T H) costs of an iterate (optimizer.py:238-277);
+    logdet (optional): log det of cur.prec if the caller has it."""
     if marginals is None:
         marginals = gbp_marginals(cur.prec)
     delta = cur.mean - prior.mean
@@ -213,7 +221,8 @@ def cost_breakdown(cur: JointGaussian, prior: DiscretePrior, temp: float,
                                                  threads=threads, marginals=marginals)
     collision = float(sum(f.e_psi for f in factor_values))
     return CostBreakdown(prior_cost=prior_cost, collision_cost=collision,
-                         entropy_cost=-temp * entropy_of(cur.prec))
+                         entropy_cost=-temp * (entropy_of(cur.prec) if logdet is None else
+                                               0.5 * (cur.prec.dim * (_LOG_2PI + 1.0) - logdet)))
 
 
 def initial_mean(prior: DiscretePrior, cfg: OptimizerConfig) -> np.ndarray:
@@ -289,6 +298,7 @@ def _run_pgvimp_host(prior: DiscretePrior, env, cfg: OptimizerConfig, t0: float)
     prev_total = prev_temp = None
     switched = False
     cached = None
+    ld_cur = None
     for it in range(1, cfg.max_iters + 1):
         t_iter = time.perf_counter()
         if env is not None:
@@ -296,11 +306,12 @@ def _run_pgvimp_host(prior: DiscretePrior, env, cfg: OptimizerConfig, t0: float)
             g_mu, g_sigma = assemble_joint_gradients(fv, maps, K, n)
         else:
             g_mu, g_sigma = np.zeros(K * n), BlockTridiagonalMatrix.zeros(K, n)
-        step = select_step_size(cur, prior, g_mu, g_sigma, cfg, temp)
+        step = select_step_size(cur, prior, g_mu, g_sigma, cfg, temp, logdet_cur=ld_cur)
+        ld_cur = step.logdet  # the next search's logdet_cur and this record's entropy
         nxt = step.next_state
         nxt_f = factors(nxt, step.marginals) if env is not None else []
         cached = nxt_f if env is not None else None
-        costs = cost_breakdown(nxt, prior, temp, marginals=step.marginals, factor_values=nxt_f)
+        costs = cost_breakdown(nxt, prior, temp, marginals=step.marginals, factor_values=nxt_f, logdet=ld_cur)
         mean_shift = float(np.linalg.norm(nxt.mean - cur.mean))
         result.records.append({"type": "iter", "iter": it, "beta": step.beta, "temperature": temp,
                                "prior_cost": costs.prior_cost, "collision_cost": costs.collision_cost,

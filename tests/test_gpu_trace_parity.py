@@ -246,7 +246,7 @@ def test_c5_one_step_from_reference_states(P):
     iteration starts from the REFERENCE's state (gvp_engine_set_state), so the
     comparison isolates one iteration of the engine. The reference is re-run on
     this host (oracle/ref_bench.trace_states: its own loop body, records bitwise
-    those of tests/golden c5_sample) for 16 of the traced plans, 10 iterations,
+    those of tests/golden c5_sample) for the 32 traced plans, 10 iterations,
     and also gives the EXACT solution of its own mean system at the accepted
     beta (iterative refinement with long-double residuals). Checked per
     plan-iteration, in the bench's engine layout:
@@ -270,7 +270,7 @@ def test_c5_one_step_from_reference_states(P):
         pytest.skip("oracle/_ref not built")
     g = golden("c5_sample")
     sample = g["plans"].astype(np.int64)
-    sel = np.arange(0, len(sample), 2)          # 16 of the 32 traced plans
+    sel = np.arange(len(sample))                # all 32 traced plans
     cols = sample[sel]
     iters = g["records"].shape[1]
     traces = R.trace_states_many(cols, iters)
