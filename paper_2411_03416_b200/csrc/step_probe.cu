@@ -175,25 +175,6 @@ GVP_DEV double symv(const double (&A)[T_<N>], int r, int c) {
   return r >= c ? A[tri_idx(r, c)] : A[tri_idx(c, r)];
 }
 
-// TMA issue of knot i's stage (s: ring step) for the split probe kernels
-template <int N, int L, bool KS>
-GVP_DEV void split_issue(const Args& a, double* smem, uint64_t* bars, int64_t b0, int64_t s, int64_t i) {
-  using LO = Lay<N, L, KS, true>;
-  constexpr int Pb = LO::Pb, Kb = LO::Kb;
-  double* st = smem + (s % LO::NS) * LO::STAGE;
-  uint64_t* bar = &bars[s % LO::NS];
-  v3::mbar_expect_tx(bar, LO::TX);
-  const int ck = KS ? 0 : (int)b0;
-  const int io = (int)(i > 0 ? i - 1 : 0);  // off-diagonal block (i-1, i)
-  double* pr = st + LO::OFF_PRIOR;
-  v3::tma3(pr + LO::R_KD * Kb, &a.m_kd, ck, 0, (int)i, bar);
-  v3::tma3(pr + LO::R_KO * Kb, &a.m_ko, ck, 0, io, bar);
-  v3::tma3(st + LO::R_LD * Pb, &a.m_ld, (int)b0, 0, (int)i, bar);
-  v3::tma3(st + LO::R_GD * Pb, &a.m_gd, (int)b0, 0, (int)i, bar);
-  v3::tma3(st + LO::R_E * Pb, &a.m_e, (int)b0, 0, (int)i, bar);
-  v3::tma3(st + LO::R_LO * Pb, &a.m_lo, (int)b0, 0, io, bar);
-}
-
 // Four warps per 32 lane slots, one chain stage each:
 //   warp 0  Lambda' Schur:   W = Li_{i-1} Lambda'_{i-1,i}, Phi_i, chol -> Li_i, log det
 //   warp 1  Lambda' tangent: Phi'_i, Psi_i, trace                 (one knot behind warp 0)
@@ -231,7 +212,7 @@ __global__ void __launch_bounds__(128, probe_minb<N>()) probe_split_kernel(const
   const int lcol = tid & 31;            // lane slot
   constexpr int P = LO::P, Pb = LO::Pb, Kb = LO::Kb, LP = P * L;
   const int64_t b0 = (int64_t)blockIdx.x * a.ppc;
-  const int64_t K = a.K;
+  const int K = (int)a.K;  // 32-bit step arithmetic: every loop-control op is a single integer op
   double* ring = smem + LO::RING;
   double* xch = smem + LO::XCH;
   int* ffail = reinterpret_cast<int*>(xch + 4 * 32);  // [chain][slot] first failing knot
@@ -249,29 +230,29 @@ __global__ void __launch_bounds__(128, probe_minb<N>()) probe_split_kernel(const
   v3::search_init(a, pst, a.ppc, b0, false, tid);
   __syncthreads();
 
-  auto slot = [&](int64_t s) { return smem + (s % LO::NS) * LO::STAGE; };
-  auto issue = [&](int64_t s, int64_t i) {
+  auto slot = [&](int s) { return smem + ((unsigned)s % LO::NS) * LO::STAGE; };
+  auto issue = [&](int s, int i) {
     double* st = slot(s);
-    uint64_t* bar = &bars[s % LO::NS];
+    uint64_t* bar = &bars[(unsigned)s % LO::NS];
     v3::mbar_expect_tx(bar, LO::TX);
     const int ck = KS ? 0 : (int)b0;
-    const int io = (int)(i > 0 ? i - 1 : 0);  // off-diagonal block (i-1, i)
+    const int io = i > 0 ? i - 1 : 0;  // off-diagonal block (i-1, i)
     double* pr = st + LO::OFF_PRIOR;
-    v3::tma3(pr + LO::R_KD * Kb, &a.m_kd, ck, 0, (int)i, bar);
+    v3::tma3(pr + LO::R_KD * Kb, &a.m_kd, ck, 0, i, bar);
     v3::tma3(pr + LO::R_KO * Kb, &a.m_ko, ck, 0, io, bar);
-    v3::tma3(st + LO::R_LD * Pb, &a.m_ld, (int)b0, 0, (int)i, bar);
-    v3::tma3(st + LO::R_GD * Pb, &a.m_gd, (int)b0, 0, (int)i, bar);
-    v3::tma3(st + LO::R_E * Pb, &a.m_e, (int)b0, 0, (int)i, bar);
+    v3::tma3(st + LO::R_LD * Pb, &a.m_ld, (int)b0, 0, i, bar);
+    v3::tma3(st + LO::R_GD * Pb, &a.m_gd, (int)b0, 0, i, bar);
+    v3::tma3(st + LO::R_E * Pb, &a.m_e, (int)b0, 0, i, bar);
     v3::tma3(st + LO::R_LO * Pb, &a.m_lo, (int)b0, 0, io, bar);
   };
-  auto wait_slot = [&](int64_t s) {
-    v3::mbar_wait(&bars[s % LO::NS], (uint32_t)((s / LO::NS) & 1));
+  auto wait_slot = [&](int s) {
+    v3::mbar_wait(&bars[(unsigned)s % LO::NS], ((unsigned)s / LO::NS) & 1u);
   };
-  auto rg = [&](int64_t s, int ch, int e) -> double* {
-    return ring + (((int)(s & 1) * 2 + ch) * LO::ENT + e) * 32 + lcol;
+  auto rg = [&](int s, int ch, int e) -> double* {
+    return ring + (((s & 1) * 2 + ch) * LO::ENT + e) * 32 + lcol;
   };
 
-  int64_t sbase = 0;
+  int sbase = 0;
   for (;;) {
     const Pick pk = v3::search_pick(a, pst, a.ppc, LP, lcol, tid, false);
     if (pk.kl == 0) break;  // uniform: every thread read the same shared state
@@ -297,8 +278,8 @@ __global__ void __launch_bounds__(128, probe_minb<N>()) probe_split_kernel(const
 #ifdef GVP_PROBE_PROFILE
     long long prof_work = 0, prof_wait = 0, tprev = 0;
 #endif
-    for (int64_t st_ = 0; st_ <= K; ++st_) {
-      const int64_t s = sbase + st_;
+    for (int st_ = 0; st_ <= K; ++st_) {
+      const int s = sbase + st_;
 #ifdef GVP_PROBE_PROFILE
       const long long tp0 = clock64();
 #endif
@@ -315,8 +296,9 @@ __global__ void __launch_bounds__(128, probe_minb<N>()) probe_split_kernel(const
         // ---------------------------- Schur producer, knot i = st_
         // W is formed one row at a time; each row is a rank-1 update of the
         // pivot (and of the eliminated rhs) and goes straight to the ring.
-        const int64_t i = st_;
-        if (i >= K || !alive) continue;
+        const int i = st_;
+        if (i >= K) continue;  // (a failed or idle lane keeps computing on garbage the
+                               // combine discards: no lane-divergent branch in the step)
         const double* sg = slot(s);
         const double* pr = sg + LO::OFF_PRIOR;
         auto pv = [&](int row) { return sg[row * Pb + p]; };
@@ -358,10 +340,9 @@ __global__ void __launch_bounds__(128, probe_minb<N>()) probe_split_kernel(const
           }
         }
         double pp;
-        if (!chol_inv_nb<N>(M, Li, pp)) {
+        if (!chol_inv_nb<N>(M, Li, pp) && alive) {
           ffail[chain * 32 + lcol] = (int)i;
           alive = false;
-          continue;
         }
         if (chain == 0) {  // log det = 2 log prod(pivots), product kept normalised
           int ex;
@@ -383,13 +364,8 @@ __global__ void __launch_bounds__(128, probe_minb<N>()) probe_split_kernel(const
         // ---------------------------- tangent consumer, knot i = st_ - 1
         // Phi'_i = Lambda_ii - (G'W + W'G) + W'(Psi_{i-1} W), accumulated over
         // the rows of W (ring) and G = Li_{i-1} Lambda_{i-1,i} (formed here).
-        const int64_t i = st_ - 1;
-        if (i < 0 || !alive) continue;
-        const int ff = ffail[chain * 32 + lcol];
-        if (ff >= 0 && ff <= i) {
-          alive = false;
-          continue;
-        }
+        const int i = st_ - 1;
+        if (i < 0) continue;
         const double* sg = slot(s - 1);
         auto pv = [&](int row) { return sg[row * Pb + p]; };
         double Pd[T], wp[N];
