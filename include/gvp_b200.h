@@ -202,8 +202,12 @@ int gvp_engine_load_dev(gvp_engine* e, const double* kdiag, const double* koff,
 int gvp_engine_step(gvp_engine* e, int32_t iters, int32_t sync);
 /* Same as gvp_engine_step but kernel by kernel with CUDA events on the
  * engine stream; the device time of each stage summed over the iterations
- * goes to ms[0..3] = {bisection, commit, factor_grads, control} (synchronous). */
+ * goes to ms[0..3] = {bisection (residual + probes), commit, factor kernel,
+ * eigh fix-up + control} (synchronous). */
 int gvp_engine_step_profiled(gvp_engine* e, int32_t iters, double* ms);
+/* Same with one bucket per kernel: ms[0..nms) of {residual, probes, commit,
+ * factor kernel, eigh fix-up, control}. */
+int gvp_engine_step_profiled_ex(gvp_engine* e, int32_t iters, double* ms, int32_t nms);
 /* The engine's cudaStream_t (as void*), for events/interop. */
 void* gvp_engine_stream(gvp_engine* e);
 /* Block until the engine stream is idle. */

@@ -82,6 +82,7 @@ _SIGS = {
     "gvp_engine_step": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32]),
     "gvp_engine_sync": (C.c_int, [C.c_void_p]),
     "gvp_engine_step_profiled": (C.c_int, [C.c_void_p, C.c_int32, _dp]),
+    "gvp_engine_step_profiled_ex": (C.c_int, [C.c_void_p, C.c_int32, _dp, C.c_int32]),
     "gvp_engine_stream": (C.c_void_p, [C.c_void_p]),
     "gvp_engine_active": (C.c_int, [C.c_void_p, _i32p]),
     "gvp_engine_get_state": (C.c_int, [C.c_void_p, _dp, _dp, _dp, _dp, _dp]),

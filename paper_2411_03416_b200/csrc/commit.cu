@@ -103,7 +103,7 @@ __global__ void __launch_bounds__(128, 1) commit_kernel(const __grid_constant__ 
   const int64_t b0 = (int64_t)blockIdx.x * 32;
   const int64_t b = b0 + p;
   const int kcol = KS ? 0 : p;
-  const int64_t K = a.K;
+  const int K = (int)a.K;  // 32-bit step arithmetic (every loop-control op one integer op)
   double* ring = smem + LO::RING;
   double* xch = smem + LO::XCH;
 
@@ -119,10 +119,10 @@ __global__ void __launch_bounds__(128, 1) commit_kernel(const __grid_constant__ 
   const double inv_b = ok ? 1.0 / beta : 0.0, c = ok ? beta / (beta + 1.0) : 0.0;
   double* scr = a.scratch + b;
 
-  auto slot = [&](int64_t s) { return smem + (s % LO::NS) * LO::STAGE; };
-  auto issue = [&](int64_t s, int64_t i, bool passB) {
+  auto slot = [&](int s) { return smem + ((unsigned)s % LO::NS) * LO::STAGE; };
+  auto issue = [&](int s, int i, bool passB) {
     double* st = slot(s);
-    uint64_t* bar = &bars[s % LO::NS];
+    uint64_t* bar = &bars[(unsigned)s % LO::NS];
     v3::mbar_expect_tx(bar, passB ? LO::TX_B : LO::TX_F);
     const int ck = KS ? 0 : (int)b0;
     double* pr = st + LO::OFF_PRIOR;
@@ -143,8 +143,8 @@ __global__ void __launch_bounds__(128, 1) commit_kernel(const __grid_constant__ 
       v3::tma3(st + LO::OFF_PSIY, &a.m_psiy, (int)b0, LO::S_LIPSI, (int)i, bar);  // LIPSI | Y of knot i
     }
   };
-  auto wait = [&](int64_t s) { v3::mbar_wait(&bars[s % LO::NS], (uint32_t)((s / LO::NS) & 1)); };
-  auto rg = [&](int64_t st, int e) -> double* { return ring + ((int)(st & 1) * LO::ENT + e) * 32 + p; };
+  auto wait = [&](int s) { v3::mbar_wait(&bars[(unsigned)s % LO::NS], ((unsigned)s / LO::NS) & 1u); };
+  auto rg = [&](int st, int e) -> double* { return ring + ((int)(st & 1) * LO::ENT + e) * 32 + p; };
 
   // =============================== pass B: knots K-1 .. 0 (warps 0, 1)
   int res = 0, fail_knot = -1;
@@ -154,11 +154,11 @@ __global__ void __launch_bounds__(128, 1) commit_kernel(const __grid_constant__ 
     double LiN[T], yN[N];
     if (tid == 0)
       for (int s = 0; s < LO::AH + 1 && s < K; ++s) issue(s, K - 1 - s, true);
-    for (int64_t s = 0; s < K; ++s) {
+    for (int s = 0; s < K; ++s) {
       wait(s);
       __syncthreads();
       if (tid == 0 && s + LO::AH + 1 < K) issue(s + LO::AH + 1, K - 1 - (s + LO::AH + 1), true);
-      const int64_t i = K - 1 - s;
+      const int i = K - 1 - s;
       if (side || !ok || res != 0) continue;
       const double* st = slot(s);
       const double* pr = st + LO::OFF_PRIOR;
@@ -219,7 +219,7 @@ __global__ void __launch_bounds__(128, 1) commit_kernel(const __grid_constant__ 
       double* sc = scr + (i * SE) * a.BLp;
       if (role == 0) {
         int ex;
-        pm = frexp(pm * pp, &ex);
+        pm = v3::frexp_pos(pm * pp, &ex);
         pe += ex;
 #pragma unroll
         for (int r = 0; r < N; ++r)
@@ -269,17 +269,17 @@ __global__ void __launch_bounds__(128, 1) commit_kernel(const __grid_constant__ 
 #pragma unroll
       for (int q = 0; q < T; ++q) Sig[q] = scr[(LO::S_PHI + q) * a.BLp];  // Sigma_00 = Phi_0^-1
     }
-    const int64_t sbase = K;
+    const int sbase = K;
     if (tid == 0)
       for (int s = 0; s < LO::AH && s < K; ++s) issue(sbase + s, s, false);
-    for (int64_t st_ = 0; st_ <= K; ++st_) {
-      const int64_t s = sbase + st_;
+    for (int st_ = 0; st_ <= K; ++st_) {
+      const int s = sbase + st_;
       if (st_ < K) wait(s);
       __syncthreads();
       if (tid == 0 && st_ + LO::AH < K) issue(s + LO::AH, st_ + LO::AH, false);
       if (!passF) continue;
       if (!side) {
-        const int64_t i = st_;
+        const int i = st_;
         if (i >= K) continue;
         const double* sg = slot(s);
         const double* pr = sg + LO::OFF_PRIOR;
@@ -382,7 +382,7 @@ __global__ void __launch_bounds__(128, 1) commit_kernel(const __grid_constant__ 
         }
       } else {
         // ---------------------------- side warps, knot i = st_ - 1
-        const int64_t i = st_ - 1;
+        const int i = st_ - 1;
         if (i < 0) continue;
         const double* sg = slot(s - 1);
         const double* pr = sg + LO::OFF_PRIOR;

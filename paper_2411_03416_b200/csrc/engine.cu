@@ -248,11 +248,18 @@ struct gvp_engine {
   View vw(const double* p, int64_t E) const { return View{p, E * B, B, 1}; }
   MutView mvw(double* p, int64_t E) const { return MutView{p, E * B, B, 1}; }
 
-  int factors() {
+  // phases: bit 0 the factor kernel, bit 1 the eigh fix-up, which then
+  // re-arms the list (zeroed once at creation) for the next factor kernel
+  int factors(int phases = 3) {
     FactorOut fo{mvw(epsi, 1), mvw(gmu, n), mvw(gdiag, T), ps.oob, ps.fstatus, ps.fwhere, eigh_list};
-    launches += 2 * (K > 2);  // factor_grads_kernel + the eigh fix-up
-    return launch_factor_grads(B, K, n, vw(mean, n), vw(covs, T), rule.dev, field.dev, radius_eps,
-                               sigma_obs, fo, ps.active, stream);
+    fo.phases = phases;
+    fo.reset_eigh = false;
+    launches += ((phases & 1) + ((phases >> 1) & 1)) * (K > 2);  // factor_grads_kernel, eigh fix-up
+    int r = launch_factor_grads(B, K, n, vw(mean, n), vw(covs, T), rule.dev, field.dev, radius_eps,
+                                sigma_obs, fo, ps.active, stream);
+    if (r) return r;
+    if (phases & 2) GVP_CUDA(cudaMemsetAsync(eigh_list, 0, sizeof(int), stream));
+    return GVP_OK;
   }
 
   V2Launch step_args() const {
@@ -383,6 +390,7 @@ extern "C" int gvp_engine_create(gvp_engine** out, int32_t nplans, int64_t nknot
       (r = e->alloc(&e->oob, B)) ||
       (r = e->alloc(&e->eigh_list, (size_t)(1 + B * std::max<int64_t>(K - 2, 1)))))
     return fail(r);
+  if (cudaMemset(e->eigh_list, 0, sizeof(int)) != cudaSuccess) return fail(GVP_ERR_CUDA);
   PlanState& ps = e->ps;
   double* s = e->scal;
   ps.temp = s; ps.logdet = s + B; ps.beta = s + 2 * B; ps.kl = s + 3 * B; ps.shift = s + 4 * B;
@@ -515,25 +523,34 @@ extern "C" int gvp_engine_step(gvp_engine* e, int32_t iters, int32_t sync) {
   return GVP_OK;
 }
 
-extern "C" int gvp_engine_step_profiled(gvp_engine* e, int32_t iters, double* ms) {
+// Per-kernel device times of `iters` iterations (ungraphed, events between the
+// kernels), summed into ms[0..nms): residual, probe (bisection), commit, factor
+// kernel, eigh fix-up, control.
+extern "C" int gvp_engine_step_profiled_ex(gvp_engine* e, int32_t iters, double* ms, int32_t nms) {
+  if (!e || !ms || nms < 1) return GVP_ERR_ARG;
+  constexpr int NB = 6;
   cudaStream_t s = e->stream;
-  cudaEvent_t ev[5];
+  cudaEvent_t ev[NB + 1];
   for (auto& x : ev) GVP_CUDA(cudaEventCreate(&x));
-  double acc[4] = {0, 0, 0, 0};
+  double acc[NB] = {0, 0, 0, 0, 0, 0};
+  int r = GVP_OK;
   for (int k = 0; k < iters && e->iters_launched < e->cfg.max_iters; ++k) {
     GVP_CUDA(cudaEventRecord(ev[0], s));
-    int r = launch_select_bisect(e->step_args(), s);
-    if (r) return r;
-    GVP_CUDA(cudaEventRecord(ev[1], s));
-    if ((r = launch_select_commit(e->step_args(), s))) return r;
-    e->launches += 3;  // residual + bisection probes + commit
+    V2Launch q = e->step_args();
+    q.ev_residual_done = ev[1];
+    if ((r = launch_select_bisect(q, s))) break;
     GVP_CUDA(cudaEventRecord(ev[2], s));
-    if ((r = e->factors())) return r;
+    if ((r = launch_select_commit(e->step_args(), s))) break;
+    e->launches += 3;  // residual + bisection probes + commit
     GVP_CUDA(cudaEventRecord(ev[3], s));
-    if ((r = e->control())) return r;
+    if ((r = e->factors(1))) break;
     GVP_CUDA(cudaEventRecord(ev[4], s));
-    GVP_CUDA(cudaEventSynchronize(ev[4]));
-    for (int j = 0; j < 4; ++j) {
+    if ((r = e->factors(2))) break;
+    GVP_CUDA(cudaEventRecord(ev[5], s));
+    if ((r = e->control())) break;
+    GVP_CUDA(cudaEventRecord(ev[6], s));
+    GVP_CUDA(cudaEventSynchronize(ev[6]));
+    for (int j = 0; j < NB; ++j) {
       float t = 0.f;
       GVP_CUDA(cudaEventElapsedTime(&t, ev[j], ev[j + 1]));
       acc[j] += t;
@@ -541,7 +558,19 @@ extern "C" int gvp_engine_step_profiled(gvp_engine* e, int32_t iters, double* ms
     ++e->iters_launched;
   }
   for (auto& x : ev) cudaEventDestroy(x);
-  for (int j = 0; j < 4; ++j) ms[j] = acc[j];
+  for (int j = 0; j < NB && j < nms; ++j) ms[j] = acc[j];
+  return r;
+}
+
+// ms[0..4): bisection (residual + probes), commit, factor kernel, eigh fix-up + control
+extern "C" int gvp_engine_step_profiled(gvp_engine* e, int32_t iters, double* ms) {
+  double m[6];
+  const int r = gvp_engine_step_profiled_ex(e, iters, m, 6);
+  if (r) return r;
+  ms[0] = m[0] + m[1];
+  ms[1] = m[2];
+  ms[2] = m[3];
+  ms[3] = m[4] + m[5];
   return GVP_OK;
 }
 

@@ -957,17 +957,20 @@ static int grads_impl(int nplans, int64_t K, const View& mean, const View& covs,
     }
     launch(std::false_type{});
   };
-  if (out.eigh_list) GVP_CUDA(cudaMemsetAsync(out.eigh_list, 0, sizeof(int), s));
+  if (out.eigh_list && out.reset_eigh && (out.phases & 1))
+    GVP_CUDA(cudaMemsetAsync(out.eigh_list, 0, sizeof(int), s));
   // specialisations for the configurations of SURVEY §8d: 13 projections
   // (k_q = 3, P = 2) and 57 (k_q = 5, P = 2); anything else takes the loop
-  if (host && R.nproj == 13 && (int64_t)host->h_proj.size() == 13 * P)
-    go(std::integral_constant<int, 13>{});
-  else if (host && R.nproj == 57 && (int64_t)host->h_proj.size() == 57 * P)
-    go(std::integral_constant<int, 57>{});
-  else
-    go(std::integral_constant<int, 0>{});
-  GVP_CUDA(cudaGetLastError());
-  if (out.eigh_list) {  // one small grid; exits at once when no factor needed the eigh root
+  if (out.phases & 1) {
+    if (host && R.nproj == 13 && (int64_t)host->h_proj.size() == 13 * P)
+      go(std::integral_constant<int, 13>{});
+    else if (host && R.nproj == 57 && (int64_t)host->h_proj.size() == 57 * P)
+      go(std::integral_constant<int, 57>{});
+    else
+      go(std::integral_constant<int, 0>{});
+    GVP_CUDA(cudaGetLastError());
+  }
+  if (out.eigh_list && (out.phases & 2)) {  // one small grid; exits at once when no factor needed the eigh root
     factor_eigh_kernel<N, P><<<148, 64, 0, s>>>(nfac, mean, covs, R, F, re, so, out);
     GVP_CUDA(cudaGetLastError());
   }

@@ -114,6 +114,12 @@ struct FactorOut {
   // whose Cholesky (and jitter retry) failed, finished by the eigh fix-up kernel.
   // nullptr: report GVP_ERR_SQRT instead. Size 1 + nplans * nfac.
   int* eigh_list = nullptr;
+  // bit 0: the factor kernel, bit 1: the eigh fix-up (callers that time the
+  // factor kernel alone launch the two separately)
+  int phases = 3;
+  // zero eigh_list[0] before the factor kernel; the engine instead re-arms the
+  // list itself once the fix-up has consumed it (outside the timed factor stage)
+  bool reset_eigh = true;
 };
 int launch_factor_grads(int nplans, int64_t nknots, int n, const View& mean, const View& covs,
                         const RuleDev& rule, const FieldDev& field, double radius_eps,
@@ -194,6 +200,9 @@ struct V2Launch {
   // forward-Schur log det); the commit overwrites them only where fixkl[b]
   bool search_kl;
   const int* fixkl;
+  // recorded between the residual kernel and the probe kernel when set
+  // (per-kernel timing, gvp_engine_step_profiled_ex); never inside a capture
+  cudaEvent_t ev_residual_done;
 };
 // forward-Schur log det of packed precisions (plan-minor, stride Bp), the
 // probes' own recursion: a bit-identical ld_cur for the next search. mask

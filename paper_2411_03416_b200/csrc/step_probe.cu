@@ -113,62 +113,7 @@ struct Args {
   int rotate;  // split kernel: rotate the warp roles by the CTA's SM residency slot
 };
 
-// Branch-free pieces of the per-knot Cholesky: the library's double rsqrt and
-// frexp carry special-value slow paths (a CALL under a convergence barrier in
-// the hot loop); pivots here are positive normal numbers (anything else already
-// fails the SPD test, whose value is then irrelevant), so: the hardware
-// approximation + two Newton steps (~1 ulp), and exponent extraction from the bits.
-GVP_DEV double rsqrt_nb(double x) {
-  double y;
-  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
-  const double h = 0.5 * x;
-  y = y * fma(-h * y, y, 1.5);
-  y = y * fma(-h * y, y, 1.5);
-  return y;
-}
-GVP_DEV double frexp_pos(double x, int* e) {  // x > 0 normal: x = m 2^e, m in [0.5, 1)
-  const long long bits = __double_as_longlong(x);
-  *e = (int)((bits >> 52) & 0x7ff) - 1022;
-  return __longlong_as_double((bits & ~(0x7ffLL << 52)) | (1022LL << 52));
-}
-template <int N>
-GVP_DEV bool chol_inv_nb(const double (&A)[T_<N>], double (&Li)[T_<N>], double& pivprod) {
-  double L[T_<N>], inv[N];
-  bool ok = true;
-  pivprod = 1.0;
-#pragma unroll
-  for (int j = 0; j < N; ++j) {
-    double s = A[tri_idx(j, j)];
-#pragma unroll
-    for (int k = 0; k < j; ++k) s -= L[tri_idx(j, k)] * L[tri_idx(j, k)];
-    ok = ok && (s > 0.0);
-    const double r = rsqrt_nb(s);
-    const double d = s * r;
-    ok = ok && (d > kPivotFloor);
-    L[tri_idx(j, j)] = d;
-    inv[j] = r;
-    pivprod *= d;
-#pragma unroll
-    for (int i = j + 1; i < N; ++i) {
-      double t = A[tri_idx(i, j)];
-#pragma unroll
-      for (int k = 0; k < j; ++k) t -= L[tri_idx(i, k)] * L[tri_idx(j, k)];
-      L[tri_idx(i, j)] = t * r;
-    }
-  }
-#pragma unroll
-  for (int c = 0; c < N; ++c) {
-    Li[tri_idx(c, c)] = inv[c];
-#pragma unroll
-    for (int r = c + 1; r < N; ++r) {
-      double t = 0.0;
-#pragma unroll
-      for (int k = c; k < r; ++k) t += L[tri_idx(r, k)] * Li[tri_idx(k, c)];
-      Li[tri_idx(r, c)] = -t * inv[r];
-    }
-  }
-  return ok;
-}
+using v3::frexp_pos;
 
 template <int N>
 GVP_DEV double symv(const double (&A)[T_<N>], int r, int c) {
@@ -340,7 +285,7 @@ __global__ void __launch_bounds__(128, probe_minb<N>()) probe_split_kernel(const
           }
         }
         double pp;
-        if (!chol_inv_nb<N>(M, Li, pp) && alive) {
+        if (!v3::chol_inv<N>(M, Li, pp) && alive) {
           ffail[chain * 32 + lcol] = (int)i;
           alive = false;
         }
@@ -657,7 +602,7 @@ __global__ void __launch_bounds__(64) probe_fused_kernel(const __grid_constant__
           }
       }
       double pp;
-      if (!chol_inv_nb<N>(M, Li, pp)) {
+      if (!v3::chol_inv<N>(M, Li, pp)) {
         fail_knot = (int)i;
         continue;
       }
@@ -824,7 +769,7 @@ __global__ void logdet_fwd_packed_kernel(int B, int64_t K, int64_t Bp, const dou
       }
     }
     double pp;
-    if (!chol_inv_nb<N>(M, Li, pp)) {
+    if (!v3::chol_inv<N>(M, Li, pp)) {
       out[b] = NAN;
       if (status) {
         status[b] = GVP_ERR_NOT_SPD;
@@ -882,6 +827,7 @@ int launch_probe(const V2Launch& q, const int L, cudaStream_t s) {
         return GVP_ERR_UNSUPPORTED;
     }
   }
+  if (q.ev_residual_done) GVP_CUDA(cudaEventRecord(q.ev_residual_done, s));
   v4::Args a;
   std::memset(&a, 0, sizeof(a));
   a.B = q.nplans;

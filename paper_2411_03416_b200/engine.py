@@ -137,10 +137,20 @@ class PlanBatch:
 
     def step_profiled(self, iters: int = 1) -> np.ndarray:
         """Kernel-by-kernel iterations with CUDA events; returns summed device
-        ms of (bisection, commit, factor_grads, control)."""
+        ms of (bisection incl. the residual kernel, commit, factor kernel,
+        eigh fix-up + control)."""
         ms = np.zeros(4)
         self._ok(self.lib.gvp_engine_step_profiled(self.handle, int(iters), N.ptr(ms)),
                  "gvp_engine_step_profiled")
+        return ms
+
+    PROFILE_BUCKETS = ("residual", "probes", "commit", "factor_grads", "eigh_fixup", "control")
+
+    def step_profiled_ex(self, iters: int = 1) -> np.ndarray:
+        """Same, one bucket per kernel (PROFILE_BUCKETS)."""
+        ms = np.zeros(len(self.PROFILE_BUCKETS))
+        self._ok(self.lib.gvp_engine_step_profiled_ex(self.handle, int(iters), N.ptr(ms), len(ms)),
+                 "gvp_engine_step_profiled_ex")
         return ms
 
     def stream_ptr(self) -> int:
