@@ -219,7 +219,7 @@ __global__ void __launch_bounds__(128, 1) commit_kernel(const __grid_constant__ 
       double* sc = scr + (i * SE) * a.BLp;
       if (role == 0) {
         int ex;
-        pm = v3::frexp_pos(pm * pp, &ex);
+        pm = frexp_pos(pm * pp, &ex);
         pe += ex;
 #pragma unroll
         for (int r = 0; r < N; ++r)

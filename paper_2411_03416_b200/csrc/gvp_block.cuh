@@ -16,6 +16,25 @@ namespace gvp {
 
 constexpr double kPivotFloor = 1e-300;  // blocktri.py:17
 
+// Branch-free pieces of the per-knot Cholesky: the library's double rsqrt and
+// frexp carry special-value slow paths (a CALL under a convergence barrier in
+// the hot loop); pivots here are positive normal numbers (anything else already
+// fails the SPD test, whose value is then irrelevant), so: the hardware
+// approximation + two Newton steps (~1 ulp), and exponent extraction from the bits.
+GVP_DEV double rsqrt_nb(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  const double h = 0.5 * x;
+  y = y * fma(-h * y, y, 1.5);
+  y = y * fma(-h * y, y, 1.5);
+  return y;
+}
+GVP_DEV double frexp_pos(double x, int* e) {  // x > 0 normal: x = m 2^e, m in [0.5, 1)
+  const long long bits = __double_as_longlong(x);
+  *e = (int)((bits >> 52) & 0x7ff) - 1022;
+  return __longlong_as_double((bits & ~(0x7ffLL << 52)) | (1022LL << 52));
+}
+
 // ---------------------------------------------------------------- strided views
 // element (plan b, knot i, entry e) lives at p[i*sk + e*se + b*sp].
 // Plan-minor ("interleaved") batches use sp=1, se=B, sk=E*B; a view shared by

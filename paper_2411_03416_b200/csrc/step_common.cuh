@@ -58,24 +58,6 @@ constexpr int cx_round(int x, int m) { return (x + m - 1) / m * m; }
 constexpr int cx_gran(int w) { return w % 16 == 0 ? 1 : w % 8 == 0 ? 2 : w % 4 == 0 ? 4 : w % 2 == 0 ? 8 : 16; }
 
 // ------------------------------------------------------------ packed algebra
-// Branch-free pieces of the per-knot Cholesky: the library's double rsqrt and
-// frexp carry special-value slow paths (a CALL under a convergence barrier in
-// the hot loop); pivots here are positive normal numbers (anything else already
-// fails the SPD test, whose value is then irrelevant), so: the hardware
-// approximation + two Newton steps (~1 ulp), and exponent extraction from the bits.
-GVP_DEV double rsqrt_nb(double x) {
-  double y;
-  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
-  const double h = 0.5 * x;
-  y = y * fma(-h * y, y, 1.5);
-  y = y * fma(-h * y, y, 1.5);
-  return y;
-}
-GVP_DEV double frexp_pos(double x, int* e) {  // x > 0 normal: x = m 2^e, m in [0.5, 1)
-  const long long bits = __double_as_longlong(x);
-  *e = (int)((bits >> 52) & 0x7ff) - 1022;
-  return __longlong_as_double((bits & ~(0x7ffLL << 52)) | (1022LL << 52));
-}
 template <int N>
 GVP_DEV bool chol_inv(const double (&A)[T_<N>], double (&Li)[T_<N>], double& pivprod) {
   double L[T_<N>], inv[N];

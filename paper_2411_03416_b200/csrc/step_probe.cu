@@ -113,7 +113,6 @@ struct Args {
   int rotate;  // split kernel: rotate the warp roles by the CTA's SM residency slot
 };
 
-using v3::frexp_pos;
 
 template <int N>
 GVP_DEV double symv(const double (&A)[T_<N>], int r, int c) {

@@ -83,12 +83,26 @@ GVP_DEV bool chol(const double* A, double* L, int n, double& pm, int& pe) {
 #pragma unroll
       for (int k = 0; k < j; ++k) s -= l[k] * L[j * LD + k];
       const double d = __shfl_sync(FULL, s, j);
-      const double piv = sqrt(d);
+      // sqrt and the column scale through one reciprocal square root (no IEEE
+      // sqrt / division subroutines on the chain); d is warp-uniform, so is the
+      // exact fallback for pivots near the subnormal range
+      double piv, rp;
+      if (d > 1e-280) {
+        rp = rsqrt_nb(d);
+        piv = d * rp;
+      } else {
+        piv = sqrt(d);
+        rp = 1.0 / piv;
+      }
       ok = ok && (d > 0.0) && (!FLOOR || piv > kPivotFloor);
-      l[j] = (r == j) ? piv : (r > j ? s / piv : 0.0);
+      l[j] = (r == j) ? piv : (r > j ? s * rp : 0.0);
       if (r < n && r >= j) L[r * LD + j] = l[j];
       int e;
-      pm = frexp(pm * piv, &e);
+      if (d > 1e-280) {
+        pm = frexp_pos(pm * piv, &e);  // pm in [0.5, 1), piv > 1e-140: a positive normal product
+      } else {
+        pm = frexp(pm * piv, &e);
+      }
       pe += e;
       __syncwarp();
     }
@@ -96,11 +110,14 @@ GVP_DEV bool chol(const double* A, double* L, int n, double& pm, int& pe) {
   return ok;
 }
 
-// Li = L^-1 (lower), lane c computes column c by forward substitution
+// Li = L^-1 (lower), lane c computes column c by forward substitution; the
+// n diagonal reciprocals are formed once, one per lane, and broadcast by
+// shuffle (no division on the substitution chain)
 template <int NM>
 GVP_DEV void trinv(const double* L, double* Li, int n) {
   constexpr int LD = Tile<NM>::LD;
   const int c = lane();
+  const double dinv = c < n ? 1.0 / L[c * LD + c] : 0.0;
   double x[NM];
 #pragma unroll
   for (int r = 0; r < NM; ++r) {
@@ -109,7 +126,8 @@ GVP_DEV void trinv(const double* L, double* Li, int n) {
       double t = (r == c) ? 1.0 : 0.0;
 #pragma unroll
       for (int k = 0; k < r; ++k) t -= L[r * LD + k] * x[k];
-      x[r] = (r >= c) ? t / L[r * LD + r] : 0.0;
+      const double dr = __shfl_sync(FULL, dinv, r);  // every lane (not under the select)
+      x[r] = (r >= c) ? t * dr : 0.0;
       if (c < n) Li[r * LD + c] = x[r];
     }
   }
