@@ -41,6 +41,19 @@
 namespace gvp {
 namespace wide {
 
+// One plan's knot-major dense array (every wide caller passes one plan with
+// contiguous n x n blocks / n-vectors): entry e of knot i at p[i * E + e].
+// 32-bit index arithmetic and no per-entry stride multiplies; the plan index
+// of the strided views is dropped (launchers check the layout).
+template <class Ptr>
+struct DenseT {
+  Ptr p;
+  int E;
+  GVP_DEV auto& operator()(int64_t, int64_t i, int64_t e) const { return p[(int)i * E + (int)e]; }
+};
+using DView = DenseT<const double*>;
+using DMut = DenseT<double*>;
+
 // ------------------------------------------------------------------ chain A
 // gbp_marginals of the chain whose blocks the source gives (diag(i, r, c),
 // off(i, r, c) = block (i, i+1)): backward Schur pivots Phi_i -> Phi_i^-1 in
@@ -309,7 +322,7 @@ GVP_DEV constexpr int exact_n(int n) {
 
 // ------------------------------------------------------------------ sources
 struct BtSrc {  // a stored block-tridiagonal matrix (+ rhs)
-  View D, U, E;
+  DView D, U, E;
   int64_t b;
   int n;
   GVP_DEV double diag(int64_t i, int r, int c) const { return D(b, i, r * n + c); }
@@ -322,7 +335,7 @@ struct NoOut {
   GVP_DEV void mean(int64_t, int, double) const {}
 };
 struct BtOut {
-  MutView C, X, M;
+  DMut C, X, M;
   int64_t b;
   int n;
   GVP_DEV void cov(int64_t i, int r, int c, double v) const {
@@ -343,14 +356,14 @@ struct NoTr {
 
 // ------------------------------------------------------------------ drop-in kernels (one warp per plan)
 template <int NM>
-__global__ void __launch_bounds__(32) marginals_kernel(int64_t K, int n_in, View D, View U, MutView cov, MutView cross,
+__global__ void __launch_bounds__(32) marginals_kernel(int64_t K, int n_in, DView D, DView U, DMut cov, DMut cross,
                                                        double* logdet, double* scratch, int* status, int* where) {
   extern __shared__ __align__(16) double sm[];
   const int n = exact_n<NM>(n_in);
   WarpWs<NM> w(sm);
   const int64_t b = blockIdx.x;
-  BtSrc src{D, U, View{nullptr, 0, 0, 0}, b, n};
-  BtOut out{cov, cross, MutView{nullptr, 0, 0, 0}, b, n};
+  BtSrc src{D, U, DView{nullptr, 0}, b, n};
+  BtOut out{cov, cross, DMut{nullptr, 0}, b, n};
   double tr, ld;
   const int f = chain_marginals<NM>(src, K, n, scratch + b * K * n * n, w, out, NoTr{}, tr, ld);
   if (lane() == 0) {
@@ -361,14 +374,14 @@ __global__ void __launch_bounds__(32) marginals_kernel(int64_t K, int n_in, View
 }
 
 template <int NM>
-__global__ void __launch_bounds__(32) mean_solve_kernel(int64_t K, int n_in, View D, View U, View E, MutView x,
+__global__ void __launch_bounds__(32) mean_solve_kernel(int64_t K, int n_in, DView D, DView U, DView E, DMut x,
                                                         double* scratch, int* status, int* where) {
   extern __shared__ __align__(16) double sm[];
   const int n = exact_n<NM>(n_in);
   WarpWs<NM> w(sm);
   const int64_t b = blockIdx.x;
   BtSrc src{D, U, E, b, n};
-  BtOut out{MutView{nullptr, 0, 0, 0}, MutView{nullptr, 0, 0, 0}, x, b, n};
+  BtOut out{DMut{nullptr, 0}, DMut{nullptr, 0}, x, b, n};
   double mh;
   double* lg = scratch + b * K * (n * n + n);
   const int f = chain_mean<NM>(src, K, n, lg, lg + K * n * n, w, out, NoTr{}, mh);
@@ -382,7 +395,7 @@ __global__ void __launch_bounds__(32) mean_solve_kernel(int64_t K, int n_in, Vie
 // W = L_{i-1}^-1 U_{i-1}; chol_spd without symmetrising (LAPACK reads the
 // lower triangle); log det = 2 sum log diag L
 template <int NM>
-__global__ void __launch_bounds__(32) logdet_kernel(int64_t K, int n_in, View D, View U, double* logdet, double* chols,
+__global__ void __launch_bounds__(32) logdet_kernel(int64_t K, int n_in, DView D, DView U, double* logdet, double* chols,
                                                     int* status, int* where) {
   constexpr int LD = Tile<NM>::LD;
   extern __shared__ __align__(16) double sm[];
@@ -448,12 +461,12 @@ __global__ void __launch_bounds__(32) logdet_kernel(int64_t K, int n_in, View D,
 // ------------------------------------------------------------------ step (bisection) kernel
 struct StepArgs {
   // problem (one plan per CTA; plan-minor views)
-  View mean, diag, off, kdiag, koff, info, gmu, gdiag, goff;
+  DView mean, diag, off, kdiag, koff, info, gmu, gdiag, goff;
   bool has_goff;
   int n;
   int64_t K;
   // outputs (write mode)
-  MutView o_mean, o_diag, o_off, o_cov, o_cross;
+  DMut o_mean, o_diag, o_off, o_cov, o_cross;
   // search state / records (the field names step_common's search expects)
   int B;
   const int* active;
@@ -563,8 +576,7 @@ __global__ void __launch_bounds__(64 * W) step_kernel(const __grid_constant__ St
     if (role == 0) {
       if (!a.fixed) {
         ProbeSrcA src{&a, b, two_t, inv_t, inv_b, c};
-        BtOut out{write ? a.o_cov : MutView{nullptr, 0, 0, 0}, write ? a.o_cross : MutView{nullptr, 0, 0, 0},
-                  MutView{nullptr, 0, 0, 0}, b, n};
+        BtOut out{write ? a.o_cov : DMut{nullptr, 0}, write ? a.o_cross : DMut{nullptr, 0}, DMut{nullptr, 0}, b, n};
         f = chain_marginals<NM>(src, K, n, scr, w, out, CurTr{&a, b}, tr, ld);
       }
       if (write) {  // Lambda' blocks (symmetrised diagonal, optimizer.py:151-153)
@@ -578,7 +590,7 @@ __global__ void __launch_bounds__(64 * W) step_kernel(const __grid_constant__ St
       }
     } else {
       ProbeSrcB src{&a, b, temp, inv_t, inv_b};
-      BtOut out{MutView{nullptr, 0, 0, 0}, MutView{nullptr, 0, 0, 0}, write ? a.o_mean : MutView{nullptr, 0, 0, 0},
+      BtOut out{DMut{nullptr, 0}, DMut{nullptr, 0}, write ? a.o_mean : DMut{nullptr, 0},
                 b, n};
       f = chain_mean<NM>(src, K, n, scr + K * n * n, scr + 2 * K * n * n, w, out, CurTr{&a, b}, mh);
     }
@@ -690,6 +702,19 @@ static int wide_dispatch(int n, F f) {
   return GVP_ERR_UNSUPPORTED;
 }
 
+// the wide kernels read one plan's dense blocks (wide::DenseT): strided views
+// must be that layout (one plan, entry stride 1, knot stride = entries)
+static bool dense_ok(int nplans, const double* p, int64_t sk, int64_t se, int64_t E) {
+  return nplans == 1 && (p == nullptr || (se == 1 && sk == E));
+}
+static wide::DView dv(const View& v, int64_t E) { return wide::DView{v.p, (int)E}; }
+static wide::DMut dm(const MutView& v, int64_t E) { return wide::DMut{v.p, (int)E}; }
+#define GVP_WIDE_DENSE(nplans, v, E)                                                  \
+  if (!dense_ok(nplans, (v).p, (v).sk, (v).se, (E))) {                                \
+    set_error("wide block kernels take one plan's contiguous blocks (" #v ")");      \
+    return GVP_ERR_ARG;                                                               \
+  }
+
 int launch_wide_marginals(int nplans, int64_t K, int n, const View& D, const View& U, const MutView& cov,
                           const MutView& cross, double* logdet, double* scratch, int* status, int* where,
                           cudaStream_t s) {
@@ -697,7 +722,11 @@ int launch_wide_marginals(int nplans, int64_t K, int n, const View& D, const Vie
     constexpr int NM = decltype(tag)::value;
     const size_t bytes = wide::WarpWs<NM>::DOUBLES * 8;
     GVP_CUDA(cudaFuncSetAttribute(wide::marginals_kernel<NM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
-    wide::marginals_kernel<NM><<<nplans, 32, bytes, s>>>(K, n, D, U, cov, cross, logdet, scratch, status, where);
+    const int64_t N2 = (int64_t)n * n;
+    GVP_WIDE_DENSE(nplans, D, N2) GVP_WIDE_DENSE(nplans, U, N2) GVP_WIDE_DENSE(nplans, cov, N2)
+    GVP_WIDE_DENSE(nplans, cross, N2)
+    wide::marginals_kernel<NM><<<nplans, 32, bytes, s>>>(K, n, dv(D, N2), dv(U, N2), dm(cov, N2), dm(cross, N2),
+                                                         logdet, scratch, status, where);
     GVP_CUDA(cudaGetLastError());
     return GVP_OK;
   });
@@ -709,7 +738,11 @@ int launch_wide_mean_solve(int nplans, int64_t K, int n, const View& D, const Vi
     constexpr int NM = decltype(tag)::value;
     const size_t bytes = wide::WarpWs<NM>::DOUBLES * 8;
     GVP_CUDA(cudaFuncSetAttribute(wide::mean_solve_kernel<NM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
-    wide::mean_solve_kernel<NM><<<nplans, 32, bytes, s>>>(K, n, D, U, E, x, scratch, status, where);
+    const int64_t N2 = (int64_t)n * n;
+    GVP_WIDE_DENSE(nplans, D, N2) GVP_WIDE_DENSE(nplans, U, N2) GVP_WIDE_DENSE(nplans, E, n)
+    GVP_WIDE_DENSE(nplans, x, n)
+    wide::mean_solve_kernel<NM><<<nplans, 32, bytes, s>>>(K, n, dv(D, N2), dv(U, N2), dv(E, n), dm(x, n), scratch,
+                                                          status, where);
     GVP_CUDA(cudaGetLastError());
     return GVP_OK;
   });
@@ -721,7 +754,9 @@ int launch_wide_logdet(int nplans, int64_t K, int n, const View& D, const View& 
     constexpr int NM = decltype(tag)::value;
     const size_t bytes = wide::WarpWs<NM>::DOUBLES * 8;
     GVP_CUDA(cudaFuncSetAttribute(wide::logdet_kernel<NM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
-    wide::logdet_kernel<NM><<<nplans, 32, bytes, s>>>(K, n, D, U, logdet, chols, status, where);
+    const int64_t N2 = (int64_t)n * n;
+    GVP_WIDE_DENSE(nplans, D, N2) GVP_WIDE_DENSE(nplans, U, N2)
+    wide::logdet_kernel<NM><<<nplans, 32, bytes, s>>>(K, n, dv(D, N2), dv(U, N2), logdet, chols, status, where);
     GVP_CUDA(cudaGetLastError());
     return GVP_OK;
   });
@@ -730,10 +765,19 @@ int launch_wide_logdet(int nplans, int64_t K, int n, const View& D, const View& 
 int launch_wide_step(const WideStep& q, cudaStream_t s) {
   wide::StepArgs a;
   std::memset(&a, 0, sizeof(a));
-  a.mean = q.mean; a.diag = q.diag; a.off = q.off; a.kdiag = q.kdiag; a.koff = q.koff; a.info = q.info;
-  a.gmu = q.gmu; a.gdiag = q.gdiag; a.goff = q.goff; a.has_goff = q.has_goff;
+  const int64_t N2 = (int64_t)q.n * q.n, nv = q.n;
+  GVP_WIDE_DENSE(q.nplans, q.mean, nv) GVP_WIDE_DENSE(q.nplans, q.diag, N2) GVP_WIDE_DENSE(q.nplans, q.off, N2)
+  GVP_WIDE_DENSE(q.nplans, q.kdiag, N2) GVP_WIDE_DENSE(q.nplans, q.koff, N2) GVP_WIDE_DENSE(q.nplans, q.info, nv)
+  GVP_WIDE_DENSE(q.nplans, q.gmu, nv) GVP_WIDE_DENSE(q.nplans, q.gdiag, N2)
+  if (q.has_goff) { GVP_WIDE_DENSE(q.nplans, q.goff, N2) }
+  GVP_WIDE_DENSE(q.nplans, q.o_mean, nv) GVP_WIDE_DENSE(q.nplans, q.o_diag, N2) GVP_WIDE_DENSE(q.nplans, q.o_off, N2)
+  GVP_WIDE_DENSE(q.nplans, q.o_cov, N2) GVP_WIDE_DENSE(q.nplans, q.o_cross, N2)
+  a.mean = dv(q.mean, nv); a.diag = dv(q.diag, N2); a.off = dv(q.off, N2); a.kdiag = dv(q.kdiag, N2);
+  a.koff = dv(q.koff, N2); a.info = dv(q.info, nv);
+  a.gmu = dv(q.gmu, nv); a.gdiag = dv(q.gdiag, N2); a.goff = dv(q.goff, N2); a.has_goff = q.has_goff;
   a.n = q.n; a.K = q.K;
-  a.o_mean = q.o_mean; a.o_diag = q.o_diag; a.o_off = q.o_off; a.o_cov = q.o_cov; a.o_cross = q.o_cross;
+  a.o_mean = dm(q.o_mean, nv); a.o_diag = dm(q.o_diag, N2); a.o_off = dm(q.o_off, N2); a.o_cov = dm(q.o_cov, N2);
+  a.o_cross = dm(q.o_cross, N2);
   a.B = q.nplans; a.active = q.active; a.status = q.status; a.where = q.where; a.nprobes = q.nprobes;
   a.beta = q.beta; a.kl = q.kl; a.ld_next = q.ld_next; a.temp = q.temp; a.ld_cur = q.ld_cur;
   a.kl_bound = q.kl_bound; a.beta_min = q.beta_min; a.beta_max = q.beta_max;
