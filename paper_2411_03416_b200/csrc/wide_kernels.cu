@@ -55,54 +55,15 @@ using DView = DenseT<const double*>;
 using DMut = DenseT<double*>;
 
 // ------------------------------------------------------------------ chain A
-// gbp_marginals of the chain whose blocks the source gives (diag(i, r, c),
-// off(i, r, c) = block (i, i+1)): backward Schur pivots Phi_i -> Phi_i^-1 in
-// the global scratch pg (K x n x n), then the forward covariance recursion.
-// Optional: covs/crosses out, tr(Lambda Sigma) against a second chain (tr),
-// log det from the backward pivots. Returns the failing knot or -1.
+// Forward covariance recursion of gbp_marginals (gbp.py:72-78) from the
+// backward sweep's Phi_i^-1 in the global scratch pg: Sigma_ii / Sigma_i,i+1
+// out, and tr(Lambda Sigma) against a second chain (trc) when asked.
 template <int NM, class Src, class Out, class Tr>
-GVP_DEV int chain_marginals(const Src& src, int64_t K, int n, double* pg, WarpWs<NM>& w, const Out& out,
-                            const Tr& trc, double& trace, double& logdet) {
+GVP_DEV void chain_cov_forward(const Src& src, int64_t K, int n, const double* pg, WarpWs<NM>& w, const Out& out,
+                               const Tr& trc, double& trace) {
   constexpr int LD = Tile<NM>::LD;
   const int r = lane();
-  double pm = 1.0;
-  int pe = 0;
-  // ---- backward sweep: X holds Phi_{i+1}^-1
-  for (int64_t i = K - 1; i >= 0; --i) {
-    stage<NM>(w.T, n, [&](int a, int b) { return src.diag(i, a, b); });
-    if (i < K - 1) {
-      stage<NM>(w.U, n, [&](int a, int b) { return src.off(i, a, b); });
-      // trailing = D - U Phi^-1 U'
-      double y[NM];
-#pragma unroll
-      for (int c = 0; c < NM; ++c) {
-        double t = 0.0;
-        if (c < n && r < n) {
-#pragma unroll
-          for (int k = 0; k < NM; ++k)
-            if (k < n) t += w.U[r * LD + k] * w.X[k * LD + c];
-        }
-        y[c] = t;
-      }
-#pragma unroll
-      for (int c = 0; c < NM; ++c) {
-        if (c < n && r < n) {
-          double t = 0.0;
-#pragma unroll
-          for (int k = 0; k < NM; ++k)
-            if (k < n) t += y[k] * w.U[c * LD + k];
-          w.T[r * LD + c] -= t;
-        }
-      }
-      __syncwarp();
-    }
-    if (!chol<NM, true>(w.T, w.L, n, pm, pe)) return (int)i;
-    trinv<NM>(w.L, w.Li, n);
-    ltl<NM>(w.Li, w.X, n);
-    store_g<NM>(pg + i * (int64_t)n * n, w.X, n);
-  }
-  logdet = 2.0 * (log(pm) + (double)pe * 0.6931471805599453);
-  // ---- forward sweep: T holds Sigma_ii
+  // T holds Sigma_ii
   __syncwarp();
   load_g<NM>(w.T, pg, n);  // Sigma_00 = Phi_0^-1 (exactly symmetric)
   double tr = 0.0;
@@ -187,7 +148,186 @@ GVP_DEV int chain_marginals(const Src& src, int64_t K, int n, double* pg, WarpWs
     }
   }
   trace = warp_sum(tr);
+}
+
+// gbp_marginals of the chain whose blocks the source gives (diag(i, r, c),
+// off(i, r, c) = block (i, i+1)): backward Schur pivots Phi_i -> Phi_i^-1 in
+// the global scratch pg (K x n x n), then the forward covariance recursion.
+// Optional: covs/crosses out, tr(Lambda Sigma) against a second chain (tr),
+// log det from the backward pivots. Returns the failing knot or -1.
+template <int NM, class Src, class Out, class Tr>
+GVP_DEV int chain_marginals(const Src& src, int64_t K, int n, double* pg, WarpWs<NM>& w, const Out& out,
+                            const Tr& trc, double& trace, double& logdet) {
+  constexpr int LD = Tile<NM>::LD;
+  const int r = lane();
+  double pm = 1.0;
+  int pe = 0;
+  // ---- backward sweep: X holds Phi_{i+1}^-1
+  for (int64_t i = K - 1; i >= 0; --i) {
+    stage<NM>(w.T, n, [&](int a, int b) { return src.diag(i, a, b); });
+    if (i < K - 1) {
+      stage<NM>(w.U, n, [&](int a, int b) { return src.off(i, a, b); });
+      // trailing = D - U Phi^-1 U'
+      double y[NM];
+#pragma unroll
+      for (int c = 0; c < NM; ++c) {
+        double t = 0.0;
+        if (c < n && r < n) {
+#pragma unroll
+          for (int k = 0; k < NM; ++k)
+            if (k < n) t += w.U[r * LD + k] * w.X[k * LD + c];
+        }
+        y[c] = t;
+      }
+#pragma unroll
+      for (int c = 0; c < NM; ++c) {
+        if (c < n && r < n) {
+          double t = 0.0;
+#pragma unroll
+          for (int k = 0; k < NM; ++k)
+            if (k < n) t += y[k] * w.U[c * LD + k];
+          w.T[r * LD + c] -= t;
+        }
+      }
+      __syncwarp();
+    }
+    if (!chol<NM, true>(w.T, w.L, n, pm, pe)) return (int)i;
+    trinv<NM>(w.L, w.Li, n);
+    ltl<NM>(w.Li, w.X, n);
+    store_g<NM>(pg + i * (int64_t)n * n, w.X, n);
+  }
+  logdet = 2.0 * (log(pm) + (double)pe * 0.6931471805599453);
+  chain_cov_forward<NM>(src, K, n, pg, w, out, trc, trace);
   return -1;
+}
+
+// pair barrier of the two chain-A warps of one probe slot (named barrier id)
+GVP_DEV void pair_sync(int id) { asm volatile("bar.sync %0, 64;" ::"r"(id) : "memory"); }
+
+// Chain A of a probe in one backward pass on two warps. The Schur warp runs
+// the backward GBP Schur of Lambda' (gbp.py:58-70: y = U_i Phi_{i+1}^-1,
+// Phi_i = sym(D_i - y U_i'), its Cholesky -> log det, Phi_i^-1 = Li' Li); the
+// tangent warp, one knot behind, carries the same recursion's derivative along
+// the current precision Lambda (D -> D + t Lambda_ii, U -> U + t Lambda_i,i+1):
+//   Phi'_i = Lambda_ii - (Lo_i y' + y Lo_i') + y Phi'_{i+1} y'   (symmetrised)
+// and sums tr(Phi_i^-1 Phi'_i) = d/dt log det(Lambda' + t Lambda) = tr(Lambda
+// Sigma'), kl_joint's trace term (optimizer.py:164-177), with no forward
+// covariance sweep. y_i and Phi_i^-1 pass through a two-slot ring (4 tiles);
+// one pair barrier per step. pg (optional): Phi_i^-1 to the global scratch for
+// a following chain_cov_forward (write mode). fail: the failing knot or -1.
+template <int NM, class Src, class Tr>
+GVP_DEV void chain_trace_split(const Src& src, const Tr& trc, int64_t K, int n, bool tangent, WarpWs<NM>& w,
+                               double* ring, int bar_id, volatile int* s_fail, double* pg, double& trace,
+                               double& logdet, int& fail) {
+  constexpr int LD = Tile<NM>::LD, MAT = Tile<NM>::MAT;
+  const int r = lane();
+  auto ringY = [&](int64_t s) { return ring + ((s & 1) * 2) * MAT; };
+  auto ringX = [&](int64_t s) { return ring + ((s & 1) * 2 + 1) * MAT; };
+  double pm = 1.0, tr = 0.0;
+  int pe = 0;
+  if (!tangent && r == 0) *s_fail = -1;
+  for (int64_t s = 0; s <= K; ++s) {
+    pair_sync(bar_id);  // step s-1 of both warps complete: ring slot s & 1 is free, s_fail current
+    if (*s_fail >= 0) break;
+    if (!tangent) {
+      if (s == K) break;
+      const int64_t i = K - 1 - s;
+      stage<NM>(w.T, n, [&](int a, int b) { return src.diag(i, a, b); });
+      if (i < K - 1) {
+        stage<NM>(w.U, n, [&](int a, int b) { return src.off(i, a, b); });
+        const double* Xn = ringX(s - 1);  // Phi_{i+1}^-1
+        double* Y = ringY(s);
+        double y[NM];
+#pragma unroll
+        for (int c = 0; c < NM; ++c) {
+          double t = 0.0;
+          if (c < n && r < n) {
+#pragma unroll
+            for (int k = 0; k < NM; ++k)
+              if (k < n) t += w.U[r * LD + k] * Xn[k * LD + c];
+          }
+          y[c] = t;
+        }
+#pragma unroll
+        for (int c = 0; c < NM; ++c) {
+          if (c < n && r < n) {
+            Y[r * LD + c] = y[c];
+            double t = 0.0;
+#pragma unroll
+            for (int k = 0; k < NM; ++k)
+              if (k < n) t += y[k] * w.U[c * LD + k];
+            w.T[r * LD + c] -= t;
+          }
+        }
+        __syncwarp();
+      }
+      if (!chol<NM, true>(w.T, w.L, n, pm, pe)) {
+        if (r == 0) *s_fail = (int)i;
+        __syncwarp();
+        continue;  // the next pair barrier publishes the failure
+      }
+      trinv<NM>(w.L, w.Li, n);
+      ltl<NM>(w.Li, ringX(s), n);
+      if (pg) store_g<NM>(pg + i * (int64_t)n * n, ringX(s), n);
+    } else {
+      if (s == 0) continue;
+      const int64_t j = K - s;  // the knot the Schur warp finished in step s - 1
+      const double* Xj = ringX(s - 1);
+      const double* Yj = ringY(s - 1);
+      stage<NM>(w.T, n, [&](int a, int b) { return trc.diag(j, a, b); });  // Lambda_jj
+      double ph[NM];
+      if (j < K - 1) {
+        stage<NM>(w.U, n, [&](int a, int b) { return trc.off(j, a, b); });  // Lambda_j,j+1
+        // M = Lo Y' -> L tile;  Z = Y Phi'_{j+1} (X tile) -> registers
+        double z[NM];
+#pragma unroll
+        for (int c = 0; c < NM; ++c) {
+          double t = 0.0, u = 0.0;
+          if (c < n && r < n) {
+#pragma unroll
+            for (int k = 0; k < NM; ++k)
+              if (k < n) {
+                t += w.U[r * LD + k] * Yj[c * LD + k];
+                u += Yj[r * LD + k] * w.X[k * LD + c];
+              }
+          }
+          if (c < n && r < n) w.L[r * LD + c] = t;
+          z[c] = u;
+        }
+        __syncwarp();
+#pragma unroll
+        for (int c = 0; c < NM; ++c) {
+          double t = 0.0;
+          if (c < n && r < n) {
+#pragma unroll
+            for (int k = 0; k < NM; ++k)
+              if (k < n) t += z[k] * Yj[c * LD + k];
+            t = (w.T[r * LD + c] - (w.L[r * LD + c] + w.L[c * LD + r])) + t;
+          }
+          ph[c] = t;
+        }
+      } else {
+#pragma unroll
+        for (int c = 0; c < NM; ++c) ph[c] = (c < n && r < n) ? w.T[r * LD + c] : 0.0;
+      }
+      // Phi'_j symmetrised into the X tile (read above as Phi'_{j+1}: Li tile first)
+#pragma unroll
+      for (int c = 0; c < NM; ++c)
+        if (c < n && r < n) w.Li[r * LD + c] = ph[c];
+      __syncwarp();
+#pragma unroll
+      for (int c = 0; c < NM; ++c)
+        if (c < n && r < n) {
+          const double v = 0.5 * (w.Li[r * LD + c] + w.Li[c * LD + r]);
+          w.X[r * LD + c] = v;
+          tr += Xj[r * LD + c] * v;
+        }
+      __syncwarp();
+    }
+  }
+  fail = *s_fail;
+  trace = warp_sum(tr);
+  logdet = 2.0 * (log(pm) + (double)pe * 0.6931471805599453);
 }
 
 // ------------------------------------------------------------------ chain B
@@ -543,17 +683,19 @@ struct CurTr {  // the current precision Lambda and mean (trace / Mahalanobis te
 // memory (DSMEM) before a cluster barrier. A single wide plan (C3) otherwise
 // runs on one SM with W slots per round.
 template <int NM, int W, int G>
-__global__ void __launch_bounds__(64 * W) step_kernel(const __grid_constant__ StepArgs a) {
+__global__ void __launch_bounds__(96 * W) step_kernel(const __grid_constant__ StepArgs a) {
   namespace cg = cooperative_groups;
   extern __shared__ __align__(16) double sm[];
-  constexpr int WG = W * G;
-  const int tid = threadIdx.x, warp = tid >> 5, slot = warp >> 1, role = warp & 1;
+  constexpr int WG = W * G, MAT = Tile<NM>::MAT;
+  // three warps per probe slot: 0 chain A Schur, 1 chain B (mean system), 2 chain A tangent
+  const int tid = threadIdx.x, warp = tid >> 5, slot = warp / 3, role = warp - 3 * slot;
   const int g = G > 1 ? (int)cg::this_cluster().block_rank() : 0;
   const int64_t b = blockIdx.x / G;
   const int n = exact_n<NM>(a.n);
   const int64_t K = a.K;
   WarpWs<NM> w(sm + warp * WarpWs<NM>::DOUBLES);
-  double* tail = sm + 2 * W * WarpWs<NM>::DOUBLES;
+  double* ring = sm + 3 * W * WarpWs<NM>::DOUBLES + slot * 4 * MAT;  // chain A Schur -> tangent
+  double* tail = sm + 3 * W * WarpWs<NM>::DOUBLES + W * 4 * MAT;
   v3::PlanSt* pst = reinterpret_cast<v3::PlanSt*>(tail);  // 10 doubles
   double* r_beta = tail + 16;
   double* r_kl = r_beta + WG;
@@ -562,6 +704,7 @@ __global__ void __launch_bounds__(64 * W) step_kernel(const __grid_constant__ St
   int* r_on = r_fail + WG;
   double* xv = reinterpret_cast<double*>(r_on + WG + (WG & 1));  // per local slot: trace, logdet, mahal
   int* xf = reinterpret_cast<int*>(xv + 3 * W);                   // per local slot: fail A, fail B
+  int* s_fail = xf + 2 * W;                                       // per local slot: chain A failure (pair)
   const int64_t per_slot = K * n * n * 2 + K * n;
   double* scr = a.scratch + ((b * G + g) * W + slot) * per_slot;
   auto cluster_sync = [&]() {
@@ -573,13 +716,21 @@ __global__ void __launch_bounds__(64 * W) step_kernel(const __grid_constant__ St
     const double inv_t = 1.0 / temp, two_t = 2.0 / temp, inv_b = 1.0 / beta, c = beta / (beta + 1.0);
     double tr = 0.0, ld = 0.0, mh = 0.0;
     int f = -1;
-    if (role == 0) {
+    if (role != 1) {
       if (!a.fixed) {
         ProbeSrcA src{&a, b, two_t, inv_t, inv_b, c};
-        BtOut out{write ? a.o_cov : DMut{nullptr, 0}, write ? a.o_cross : DMut{nullptr, 0}, DMut{nullptr, 0}, b, n};
-        f = chain_marginals<NM>(src, K, n, scr, w, out, CurTr{&a, b}, tr, ld);
+        // one backward pass: log det (Schur warp) and tr(Lambda Sigma') (tangent warp);
+        // write mode keeps Phi^-1 for the forward covariance sweep (Schur warp)
+        chain_trace_split<NM>(src, CurTr{&a, b}, K, n, role == 2, w, ring, 1 + slot, s_fail + slot,
+                              write ? scr : nullptr, tr, ld, f);
+        if (write && role == 0 && f < 0) {
+          __syncwarp();
+          BtOut out{a.o_cov, a.o_cross, DMut{nullptr, 0}, b, n};
+          double unused;
+          chain_cov_forward<NM>(src, K, n, scr, w, out, NoTr{}, unused);
+        }
       }
-      if (write) {  // Lambda' blocks (symmetrised diagonal, optimizer.py:151-153)
+      if (write && role == 0) {  // Lambda' blocks (symmetrised diagonal, optimizer.py:151-153)
         ProbeSrcA src{&a, b, two_t, inv_t, inv_b, c};
         for (int64_t idx = lane(); idx < K * n * n; idx += 32) {
           const int64_t i = idx / (n * n);
@@ -596,9 +747,10 @@ __global__ void __launch_bounds__(64 * W) step_kernel(const __grid_constant__ St
     }
     if (lane() == 0) {
       if (role == 0) {
-        xv[slot * 3 + 0] = tr;
         xv[slot * 3 + 1] = ld;
         xf[slot * 2 + 0] = f;
+      } else if (role == 2) {
+        xv[slot * 3 + 0] = tr;
       } else {
         xv[slot * 3 + 2] = mh;
         xf[slot * 2 + 1] = f;
@@ -675,9 +827,10 @@ __global__ void __launch_bounds__(64 * W) step_kernel(const __grid_constant__ St
   }
 }
 
+// probe slots per CTA (3 warps each), bounded by the shared workspace
 template <int NM>
 constexpr int slots() {
-  return NM <= 16 ? 8 : 2;
+  return NM <= 16 ? 5 : 1;
 }
 
 }  // namespace wide
@@ -788,15 +941,16 @@ int launch_wide_step(const WideStep& q, cudaStream_t s) {
     constexpr int W = wide::slots<NM>();
     auto go = [&](auto gtag) -> int {
       constexpr int GG = decltype(gtag)::value;
-      const size_t bytes = (2 * W * wide::WarpWs<NM>::DOUBLES + 16 + 4 * W * GG + 4 * W + 8) * 8;
+      const size_t bytes =
+          (3 * W * wide::WarpWs<NM>::DOUBLES + 4 * W * wide::Tile<NM>::MAT + 16 + 4 * W * GG + 6 * W + 8) * 8;
       GVP_CUDA(cudaFuncSetAttribute(wide::step_kernel<NM, W, GG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)bytes));
       if constexpr (GG == 1) {
-        wide::step_kernel<NM, W, 1><<<q.nplans, 64 * W, bytes, s>>>(a);
+        wide::step_kernel<NM, W, 1><<<q.nplans, 96 * W, bytes, s>>>(a);
       } else {
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3((unsigned)(q.nplans * GG));
-        cfg.blockDim = dim3(64 * W);
+        cfg.blockDim = dim3(96 * W);
         cfg.dynamicSmemBytes = bytes;
         cfg.stream = s;
         cudaLaunchAttribute attr[1];
