@@ -54,6 +54,26 @@ struct DenseT {
 using DView = DenseT<const double*>;
 using DMut = DenseT<double*>;
 
+// Two lanes per block row for the n x n products of the chain steps (NM <= 16:
+// lane r + 16 h owns row r, columns [h H, h H + H)): every product takes half
+// the issue slots of the lane-per-row form on the warp's otherwise idle lanes.
+template <int NM>
+struct Half {
+  static constexpr bool ON = NM <= 16;
+  static constexpr int H = (NM + 1) / 2;
+};
+// the full row (NM entries) of a value held as halves by lanes r and r + 16
+template <int H>
+GVP_DEV void halves(const double (&mine)[H], double (&lo)[H], double (&hi)[H]) {
+  const bool up = (lane() >> 4) != 0;
+#pragma unroll
+  for (int cc = 0; cc < H; ++cc) {
+    const double o = __shfl_xor_sync(FULL, mine[cc], 16);
+    lo[cc] = up ? o : mine[cc];
+    hi[cc] = up ? mine[cc] : o;
+  }
+}
+
 // ------------------------------------------------------------------ chain A
 // Forward covariance recursion of gbp_marginals (gbp.py:72-78) from the
 // backward sweep's Phi_i^-1 in the global scratch pg: Sigma_ii / Sigma_i,i+1
@@ -237,6 +257,36 @@ GVP_DEV void chain_trace_split(const Src& src, const Tr& trc, int64_t K, int n, 
         stage<NM>(w.U, n, [&](int a, int b) { return src.off(i, a, b); });
         const double* Xn = ringX(s - 1);  // Phi_{i+1}^-1
         double* Y = ringY(s);
+        if constexpr (Half<NM>::ON) {
+          constexpr int H = Half<NM>::H;
+          const int r2 = lane() & 15, c0 = (lane() >> 4) * H;
+          double yh[H], ylo[H], yhi[H];
+#pragma unroll
+          for (int cc = 0; cc < H; ++cc) {
+            const int c = c0 + cc;
+            double t = 0.0;
+            if (c < n && r2 < n) {
+#pragma unroll
+              for (int k = 0; k < NM; ++k)
+                if (k < n) t += w.U[r2 * LD + k] * Xn[k * LD + c];
+              Y[r2 * LD + c] = t;
+            }
+            yh[cc] = t;
+          }
+          halves<H>(yh, ylo, yhi);
+#pragma unroll
+          for (int cc = 0; cc < H; ++cc) {
+            const int c = c0 + cc;
+            if (c < n && r2 < n) {
+              double t = 0.0;
+#pragma unroll
+              for (int k = 0; k < NM; ++k)
+                if (k < n) t += (k < H ? ylo[k] : yhi[k - H]) * w.U[c * LD + k];
+              w.T[r2 * LD + c] -= t;
+            }
+          }
+          __syncwarp();
+        } else {
         double y[NM];
 #pragma unroll
         for (int c = 0; c < NM; ++c) {
@@ -260,6 +310,7 @@ GVP_DEV void chain_trace_split(const Src& src, const Tr& trc, int64_t K, int n, 
           }
         }
         __syncwarp();
+        }
       }
       if (!chol<NM, true>(w.T, w.L, n, pm, pe)) {
         if (r == 0) *s_fail = (int)i;
@@ -275,6 +326,62 @@ GVP_DEV void chain_trace_split(const Src& src, const Tr& trc, int64_t K, int n, 
       const double* Xj = ringX(s - 1);
       const double* Yj = ringY(s - 1);
       stage<NM>(w.T, n, [&](int a, int b) { return trc.diag(j, a, b); });  // Lambda_jj
+      if constexpr (Half<NM>::ON) {
+        constexpr int H = Half<NM>::H;
+        const int r2 = lane() & 15, c0 = (lane() >> 4) * H;
+        double ph[H];
+        if (j < K - 1) {
+          stage<NM>(w.U, n, [&](int a, int b) { return trc.off(j, a, b); });  // Lambda_j,j+1
+          double zh[H], zlo[H], zhi[H];
+#pragma unroll
+          for (int cc = 0; cc < H; ++cc) {
+            const int c = c0 + cc;
+            double t = 0.0, u = 0.0;
+            if (c < n && r2 < n) {
+#pragma unroll
+              for (int k = 0; k < NM; ++k)
+                if (k < n) {
+                  t += w.U[r2 * LD + k] * Yj[c * LD + k];
+                  u += Yj[r2 * LD + k] * w.X[k * LD + c];
+                }
+              w.L[r2 * LD + c] = t;
+            }
+            zh[cc] = u;
+          }
+          halves<H>(zh, zlo, zhi);
+          __syncwarp();
+#pragma unroll
+          for (int cc = 0; cc < H; ++cc) {
+            const int c = c0 + cc;
+            double t = 0.0;
+            if (c < n && r2 < n) {
+#pragma unroll
+              for (int k = 0; k < NM; ++k)
+                if (k < n) t += (k < H ? zlo[k] : zhi[k - H]) * Yj[c * LD + k];
+              t = (w.T[r2 * LD + c] - (w.L[r2 * LD + c] + w.L[c * LD + r2])) + t;
+            }
+            ph[cc] = t;
+          }
+        } else {
+#pragma unroll
+          for (int cc = 0; cc < H; ++cc) ph[cc] = (c0 + cc < n && r2 < n) ? w.T[r2 * LD + c0 + cc] : 0.0;
+        }
+#pragma unroll
+        for (int cc = 0; cc < H; ++cc)
+          if (c0 + cc < n && r2 < n) w.Li[r2 * LD + c0 + cc] = ph[cc];
+        __syncwarp();
+#pragma unroll
+        for (int cc = 0; cc < H; ++cc) {
+          const int c = c0 + cc;
+          if (c < n && r2 < n) {
+            const double v = 0.5 * (w.Li[r2 * LD + c] + w.Li[c * LD + r2]);
+            w.X[r2 * LD + c] = v;
+            tr += Xj[r2 * LD + c] * v;
+          }
+        }
+        __syncwarp();
+        continue;
+      }
       double ph[NM];
       if (j < K - 1) {
         stage<NM>(w.U, n, [&](int a, int b) { return trc.off(j, a, b); });  // Lambda_j,j+1
@@ -349,36 +456,71 @@ GVP_DEV int chain_mean(const Src& src, int64_t K, int n, double* lg, double* zg,
     if (i > 0) {
       stage<NM>(w.U, n, [&](int a, int b) { return src.off(i - 1, a, b); });
       // Z = Li_{i-1} U_{i-1} -> X tile;  trailing -= Z'Z;  r -= Z' z_{i-1}
-      double z[NM];
+      if constexpr (Half<NM>::ON) {  // two lanes per row, half the columns each
+        constexpr int H = Half<NM>::H;
+        const int r2 = lane() & 15, c0 = (lane() >> 4) * H;
 #pragma unroll
-      for (int c = 0; c < NM; ++c) {
-        double t = 0.0;
-        if (c < n && r < n) {
+        for (int cc = 0; cc < H; ++cc) {
+          const int c = c0 + cc;
+          double t = 0.0;
+          if (c < n && r2 < n) {
 #pragma unroll
-          for (int k = 0; k < NM; ++k)
-            if (k < n && k <= r) t += w.Li[r * LD + k] * w.U[k * LD + c];
+            for (int k = 0; k < NM; ++k)
+              if (k < n && k <= r2) t += w.Li[r2 * LD + k] * w.U[k * LD + c];
+            w.X[r2 * LD + c] = t;
+          }
         }
-        z[c] = t;
-      }
+        __syncwarp();
 #pragma unroll
-      for (int c = 0; c < NM; ++c)
-        if (c < n && r < n) w.X[r * LD + c] = z[c];
-      __syncwarp();
-      if (r < n) {
-        double t2 = 0.0;
-#pragma unroll
-        for (int c = 0; c < NM; ++c)
-          if (c < n) {
+        for (int cc = 0; cc < H; ++cc) {
+          const int c = c0 + cc;
+          if (c < n && r2 < n) {
             double t = 0.0;
 #pragma unroll
             for (int k = 0; k < NM; ++k)
-              if (k < n) t += w.X[k * LD + r] * w.X[k * LD + c];
-            w.T[r * LD + c] -= t;
+              if (k < n) t += w.X[k * LD + r2] * w.X[k * LD + c];
+            w.T[r2 * LD + c] -= t;
           }
+        }
+        if (r < n) {
+          double t2 = 0.0;
 #pragma unroll
-        for (int k = 0; k < NM; ++k)
-          if (k < n) t2 += w.X[k * LD + r] * w.v0[k];
-        rv -= t2;
+          for (int k = 0; k < NM; ++k)
+            if (k < n) t2 += w.X[k * LD + r] * w.v0[k];
+          rv -= t2;
+        }
+      } else {
+        double z[NM];
+#pragma unroll
+        for (int c = 0; c < NM; ++c) {
+          double t = 0.0;
+          if (c < n && r < n) {
+#pragma unroll
+            for (int k = 0; k < NM; ++k)
+              if (k < n && k <= r) t += w.Li[r * LD + k] * w.U[k * LD + c];
+          }
+          z[c] = t;
+        }
+#pragma unroll
+        for (int c = 0; c < NM; ++c)
+          if (c < n && r < n) w.X[r * LD + c] = z[c];
+        __syncwarp();
+        if (r < n) {
+          double t2 = 0.0;
+#pragma unroll
+          for (int c = 0; c < NM; ++c)
+            if (c < n) {
+              double t = 0.0;
+#pragma unroll
+              for (int k = 0; k < NM; ++k)
+                if (k < n) t += w.X[k * LD + r] * w.X[k * LD + c];
+              w.T[r * LD + c] -= t;
+            }
+#pragma unroll
+          for (int k = 0; k < NM; ++k)
+            if (k < n) t2 += w.X[k * LD + r] * w.v0[k];
+          rv -= t2;
+        }
       }
       __syncwarp();
     }
