@@ -682,6 +682,8 @@ def main():
         result["c3"] = {"config": "C3: 7-DOF sphere arm (panda_like, 14 spheres), n=14, N=200, k_q=3 (421 points, "
                                   "113 joint projections), 128^3 map, kl_bound=10, beta_max=0.5",
                         "iterations": r3.iterations, "ms": w3, "ms_per_iteration": w3 / max(r3.iterations, 1),
+                        "ms_per_iteration_median": float(np.median([r["wall_time_ms"] for r in r3.records
+                                                                    if r.get("type") == "iter"])),
                         "path": "run_pgvimp host loop over the wide-block chain kernels + device arm factor stage"}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         result["cpu_baseline"] = cpu_baseline_leg()
