@@ -158,6 +158,30 @@ GVP_DEV void ltl(const double* Li, double* P, int n) {
   __syncwarp();
 }
 
+// ltl with two lanes per row (lane r + 16 h: columns [h H, h H + H)), NM <= 16
+template <int NM>
+GVP_DEV void ltl2(const double* Li, double* P, int n) {
+  constexpr int LD = Tile<NM>::LD, H = (NM + 1) / 2;
+  const int r = lane() & 15, c0 = (lane() >> 4) * H;
+  double p[H];
+#pragma unroll
+  for (int cc = 0; cc < H; ++cc) {
+    const int c = c0 + cc;
+    double t = 0.0;
+    if (c < n && r < n) {
+#pragma unroll
+      for (int k = 0; k < NM; ++k)
+        if (k < n && k >= r && k >= c) t += Li[k * LD + r] * Li[k * LD + c];
+    }
+    p[cc] = t;
+  }
+  __syncwarp();
+#pragma unroll
+  for (int cc = 0; cc < H; ++cc)
+    if (c0 + cc < n && r < n) P[r * LD + c0 + cc] = p[cc];
+  __syncwarp();
+}
+
 // tile -> global rows (n x n, row-major, stride n)
 template <int NM>
 GVP_DEV void store_g(double* g, const double* S, int n) {

@@ -318,7 +318,7 @@ GVP_DEV void chain_trace_split(const Src& src, const Tr& trc, int64_t K, int n, 
         continue;  // the next pair barrier publishes the failure
       }
       trinv<NM>(w.L, w.Li, n);
-      ltl<NM>(w.Li, ringX(s), n);
+      if constexpr (Half<NM>::ON) ltl2<NM>(w.Li, ringX(s), n); else ltl<NM>(w.Li, ringX(s), n);
       if (pg) store_g<NM>(pg + i * (int64_t)n * n, ringX(s), n);
     } else {
       if (s == 0) continue;
@@ -972,7 +972,7 @@ __global__ void __launch_bounds__(96 * W) step_kernel(const __grid_constant__ St
 // probe slots per CTA (3 warps each), bounded by the shared workspace
 template <int NM>
 constexpr int slots() {
-  return NM <= 16 ? 5 : 1;
+  return NM <= 16 ? 4 : 1;
 }
 
 }  // namespace wide
