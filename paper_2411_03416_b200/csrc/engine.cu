@@ -103,17 +103,34 @@ __global__ void control_kernel(int B, int64_t F, int n64dim, const double* __res
   ps.logdet[b] = ld_new;  // the accepted state becomes the current one
   double coll = 0.0;  // sum(f.e_psi), ascending factor order (optimizer.py:274)
   {
-    // the loads of a chunk are all in flight before its (sequential, in order) adds
-    constexpr int C = 32;
-    int64_t f = 0;
-    for (; f + C <= F; f += C) {
-      double buf[C];
-#pragma unroll
-      for (int k = 0; k < C; ++k) buf[k] = epsi[(f + k) * B + b];
-#pragma unroll
-      for (int k = 0; k < C; ++k) coll += buf[k];
+    // The adds are one dependent chain (the reference's order), so the loads
+    // must be far ahead of them: each thread streams its own plan's column
+    // through a two-chunk shared-memory buffer with asynchronous copies
+    // (per-thread completion, no barrier), C loads in flight per chunk.
+    constexpr int C = 64;
+    __shared__ double sbuf[2][C][32];
+    const int l = threadIdx.x;  // one warp per CTA
+    auto issue = [&](int buf, int64_t f0) {
+      const int64_t m = F - f0 < C ? F - f0 : C;
+      for (int k = 0; k < m; ++k) {
+        const unsigned dst = (unsigned)__cvta_generic_to_shared(&sbuf[buf][k][l]);
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(epsi + (f0 + k) * B + b)
+                     : "memory");
+      }
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    if (F > 0) issue(0, 0);
+    for (int64_t f0 = 0, c = 0; f0 < F; f0 += C, ++c) {
+      const int buf = (int)(c & 1);
+      if (f0 + C < F) {
+        issue(buf ^ 1, f0 + C);
+        asm volatile("cp.async.wait_group 1;" ::: "memory");
+      } else {
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
+      }
+      const int64_t m = F - f0 < C ? F - f0 : C;
+      for (int k = 0; k < m; ++k) coll += sbuf[buf][k][l];
     }
-    for (; f < F; ++f) coll += epsi[f * B + b];
   }
   const double temp = ps.temp[b];
   const double dim = (double)n64dim;
@@ -288,7 +305,9 @@ struct gvp_engine {
 
   int control() {
     const double ctol = cfg.collision_tol >= 0 ? cfg.collision_tol : 1e-4 * (double)(K - 1);
-    control_kernel<<<nblk(B, 128), 128, 0, stream>>>(B, std::max<int64_t>(K - 2, 0), (int)(K * n),
+    // one warp per CTA: the per-plan collision sum is a chain of dependent
+    // loads (reference order), so spread the plans over as many SMs as possible
+    control_kernel<<<nblk(B, 32), 32, 0, stream>>>(B, std::max<int64_t>(K - 2, 0), (int)(K * n),
                                                      epsi, ps, records, cfg.max_iters,
                                                      cfg.temp_high, cfg.tol_mean, cfg.tol_cost, ctol);
     ++launches;
