@@ -292,6 +292,13 @@ def time_to_converge(P, args, B, goals, prior, info, pmean, init, dev):
                        cell_size=0.05)
     env4 = P.Environment(sdf4, P.CollisionModel(radius_eps=1.5, sigma_obs=6.0))
     cfg4 = P.OptimizerConfig(k_q=3, kl_bound=10.0, temp_low=1.0, temp_high=5.0, max_iters=100)
+    try:  # warm (module loads, rules, device buffers), like the other legs
+        P.run_ipgvimp(P.planar_quadrotor(), env4, P.OptimizerConfig(k_q=3, kl_bound=10.0, temp_low=1.0,
+                                                                   temp_high=5.0, max_iters=2),
+                      P.OuterConfig(max_outer=1), np.zeros(6), np.array([10.0, 5.0, 0, 0, 0, 0]), dt=5.0 / 300,
+                      num_steps=300, q_c=0.5, sigma_b=1e-3, device=True, robust=True)
+    except Exception:  # noqa: BLE001 (the timed run below reports any failure)
+        pass
     t0 = time.perf_counter()
     try:
         r4, log4 = P.run_ipgvimp(P.planar_quadrotor(), env4, cfg4, P.OuterConfig(max_outer=3), np.zeros(6),
