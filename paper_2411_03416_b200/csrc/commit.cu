@@ -88,6 +88,10 @@ GVP_DEV double symv(const double (&A)[T_<N>], int r, int c) {
   return r >= c ? A[tri_idx(r, c)] : A[tri_idx(c, r)];
 }
 
+#ifdef GVP_COMMIT_PROFILE
+__device__ unsigned long long g_commit_prof[3];  // diagnostic build (tools/commit_profile.py)
+#endif
+
 template <int N, bool KS>
 __global__ void __launch_bounds__(128, 1) commit_kernel(const __grid_constant__ Args a) {
   using LO = Lay<N, KS>;
@@ -146,6 +150,9 @@ __global__ void __launch_bounds__(128, 1) commit_kernel(const __grid_constant__ 
   auto wait = [&](int s) { v3::mbar_wait(&bars[(unsigned)s % LO::NS], ((unsigned)s / LO::NS) & 1u); };
   auto rg = [&](int st, int e) -> double* { return ring + ((int)(st & 1) * LO::ENT + e) * 32 + p; };
 
+#ifdef GVP_COMMIT_PROFILE
+  const long long pc0 = clock64();
+#endif
   // =============================== pass B: knots K-1 .. 0 (warps 0, 1)
   int res = 0, fail_knot = -1;
   double pm = 1.0;
@@ -261,6 +268,9 @@ __global__ void __launch_bounds__(128, 1) commit_kernel(const __grid_constant__ 
   __syncthreads();
   const bool passF = ok && res == 0;
 
+#ifdef GVP_COMMIT_PROFILE
+  const long long pc1 = clock64();
+#endif
   // =============================== pass F: knots 0 .. K-1 (+1 step for the side warps)
   double acc0 = 0.0, acc1 = 0.0;  // chain A: -; chain B: mahal, |delta|^2; side A: trace, tr(K Sigma); side B: pq
   {
@@ -482,6 +492,14 @@ __global__ void __launch_bounds__(128, 1) commit_kernel(const __grid_constant__ 
     }
   }
   // ---------------- KL and the records (optimizer.py:164-177, 238-256)
+#ifdef GVP_COMMIT_PROFILE
+  if (tid == 0) {  // diagnostic build: cycles of pass B / pass F, summed over CTAs
+    const long long pc2 = clock64();
+    atomicAdd(&g_commit_prof[0], (unsigned long long)(pc1 - pc0));
+    atomicAdd(&g_commit_prof[1], (unsigned long long)(pc2 - pc1));
+    atomicAdd(&g_commit_prof[2], 1ull);
+  }
+#endif
   xch[(2 * warp) * 32 + p] = acc0;
   xch[(2 * warp + 1) * 32 + p] = acc1;
   __syncthreads();
@@ -561,3 +579,15 @@ int launch_commit_split(const V2Launch& q, cudaStream_t s) {
 }
 
 }  // namespace gvp
+
+#ifdef GVP_COMMIT_PROFILE
+// (diagnostic build) out = {pass B cycles, pass F cycles, CTAs} since the last call
+extern "C" int gvp_commit_profile(double* out) {
+  unsigned long long h[3];
+  GVP_CUDA(cudaMemcpyFromSymbol(h, gvp::v5::g_commit_prof, sizeof(h)));
+  const unsigned long long z[3] = {0, 0, 0};
+  GVP_CUDA(cudaMemcpyToSymbol(gvp::v5::g_commit_prof, z, sizeof(z)));
+  for (int i = 0; i < 3; ++i) out[i] = (double)h[i];
+  return GVP_OK;
+}
+#endif
