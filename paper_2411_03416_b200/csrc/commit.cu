@@ -90,6 +90,7 @@ GVP_DEV double symv(const double (&A)[T_<N>], int r, int c) {
 
 #ifdef GVP_COMMIT_PROFILE
 __device__ unsigned long long g_commit_prof[3];  // diagnostic build (tools/commit_profile.py)
+__device__ unsigned long long g_commit_role[2][4][2];  // [pass B / F][warp][work, wait] cycles
 #endif
 
 template <int N, bool KS>
@@ -161,9 +162,21 @@ __global__ void __launch_bounds__(128, 1) commit_kernel(const __grid_constant__ 
     double LiN[T], yN[N];
     if (tid == 0)
       for (int s = 0; s < LO::AH + 1 && s < K; ++s) issue(s, K - 1 - s, true);
+#ifdef GVP_COMMIT_PROFILE
+    long long rp_prev = clock64(), rp_work = 0, rp_wait = 0;
+#endif
     for (int s = 0; s < K; ++s) {
+#ifdef GVP_COMMIT_PROFILE
+      const long long rp0 = clock64();
+#endif
       wait(s);
       __syncthreads();
+#ifdef GVP_COMMIT_PROFILE
+      const long long rp1 = clock64();
+      rp_work += rp0 - rp_prev;
+      rp_wait += rp1 - rp0;
+      rp_prev = rp1;
+#endif
       if (tid == 0 && s + LO::AH + 1 < K) issue(s + LO::AH + 1, K - 1 - (s + LO::AH + 1), true);
       const int i = K - 1 - s;
       if (side || !ok || res != 0) continue;
@@ -252,6 +265,12 @@ __global__ void __launch_bounds__(128, 1) commit_kernel(const __grid_constant__ 
 #pragma unroll
       for (int q = 0; q < T; ++q) LiN[q] = Li[q];
     }
+#ifdef GVP_COMMIT_PROFILE
+    if ((tid & 31) == 0) {  // per warp: pass B work / wait cycles
+      atomicAdd(&g_commit_role[0][warp][0], (unsigned long long)rp_work);
+      atomicAdd(&g_commit_role[0][warp][1], (unsigned long long)rp_wait);
+    }
+#endif
   }
   v3::fence_proxy_async();  // scratch stores (generic proxy) -> TMA reads (async proxy)
   int* xi = reinterpret_cast<int*>(xch);
@@ -282,10 +301,26 @@ __global__ void __launch_bounds__(128, 1) commit_kernel(const __grid_constant__ 
     const int sbase = K;
     if (tid == 0)
       for (int s = 0; s < LO::AH && s < K; ++s) issue(sbase + s, s, false);
+#ifdef GVP_COMMIT_PROFILE
+    long long rf_prev = clock64(), rf_work = 0, rf_wait = 0;
+#endif
     for (int st_ = 0; st_ <= K; ++st_) {
       const int s = sbase + st_;
+#ifdef GVP_COMMIT_PROFILE
+      const long long rf0 = clock64();
+#endif
       if (st_ < K) wait(s);
       __syncthreads();
+#ifdef GVP_COMMIT_PROFILE
+      const long long rf1 = clock64();
+      rf_work += rf0 - rf_prev;
+      rf_wait += rf1 - rf0;
+      rf_prev = rf1;
+      if (st_ == K && (tid & 31) == 0) {  // per warp: pass F work / wait cycles
+        atomicAdd(&g_commit_role[1][warp][0], (unsigned long long)rf_work);
+        atomicAdd(&g_commit_role[1][warp][1], (unsigned long long)rf_wait);
+      }
+#endif
       if (tid == 0 && st_ + LO::AH < K) issue(s + LO::AH, st_ + LO::AH, false);
       if (!passF) continue;
       if (!side) {
@@ -581,13 +616,17 @@ int launch_commit_split(const V2Launch& q, cudaStream_t s) {
 }  // namespace gvp
 
 #ifdef GVP_COMMIT_PROFILE
-// (diagnostic build) out = {pass B cycles, pass F cycles, CTAs} since the last call
+// (diagnostic build) out = {pass B cycles, pass F cycles, CTAs, then [pass][warp][work, wait]
+// (16)} since the last call
 extern "C" int gvp_commit_profile(double* out) {
-  unsigned long long h[3];
+  unsigned long long h[3], r[16];
   GVP_CUDA(cudaMemcpyFromSymbol(h, gvp::v5::g_commit_prof, sizeof(h)));
-  const unsigned long long z[3] = {0, 0, 0};
-  GVP_CUDA(cudaMemcpyToSymbol(gvp::v5::g_commit_prof, z, sizeof(z)));
+  GVP_CUDA(cudaMemcpyFromSymbol(r, gvp::v5::g_commit_role, sizeof(r)));
+  const unsigned long long z[16] = {};
+  GVP_CUDA(cudaMemcpyToSymbol(gvp::v5::g_commit_prof, z, sizeof(h)));
+  GVP_CUDA(cudaMemcpyToSymbol(gvp::v5::g_commit_role, z, sizeof(r)));
   for (int i = 0; i < 3; ++i) out[i] = (double)h[i];
+  for (int i = 0; i < 16; ++i) out[3 + i] = (double)r[i];
   return GVP_OK;
 }
 #endif
