@@ -180,3 +180,37 @@ def test_c5_bench_plan_matches_reference(P):
                 break  # inside the reference's own noise band: the searches may part here
     else:
         assert len(got) == len(ref)
+
+
+def test_profiled_iterations_match_graphed_ones(P):
+    """gvp_engine_step_profiled_ex (the bench's per-kernel timing) runs the
+    same iteration kernel by kernel: records identical to the CUDA-graph
+    path's, six non-negative buckets, and the 4-bucket form folds them."""
+    env = c1_env(P)
+    sys_ltv = P.point_robot_lti(2)(50, 3.0 / 50)
+    goal = np.array([2.0, 1.5, 0.0, 0.0])
+    prior = P.assemble_prior(sys_ltv, np.zeros(4), goal, 1.0, 1e-3)
+    cfg = P.OptimizerConfig(k_q=3, kl_bound=10.0, beta_max=0.5, max_iters=12)
+    K = 51
+    init = np.linspace(0, 1, K)[None, :, None] * goal[None, None, :]
+    recs = []
+    for mode in ("graph", "ex", "four"):
+        eng = P.PlanBatch(1, K, 4, env.sdf, env.model, P.smolyak_rule(3, 4), cfg)
+        eng.load(prior.prec.diag_stack, prior.prec.off_stack, prior.info.reshape(1, K, 4),
+                 prior.mean.reshape(1, K, 4), init)
+        if mode == "graph":
+            eng.step(6, sync=True)
+        elif mode == "ex":
+            ms = np.zeros(6)
+            for _ in range(6):
+                ms += eng.step_profiled_ex(1)
+            assert ms.shape == (6,) and np.all(ms >= 0.0) and ms[1] > 0.0 and ms[2] > 0.0
+        else:
+            ms4 = np.zeros(4)
+            for _ in range(6):
+                ms4 += eng.step_profiled(1)
+            assert np.all(ms4 >= 0.0) and ms4[0] > 0.0
+        recs.append(eng.records()[0][:6])
+        eng.close()
+    assert np.array_equal(recs[0], recs[1], equal_nan=True)
+    assert np.array_equal(recs[0], recs[2], equal_nan=True)
