@@ -565,21 +565,28 @@ def main():
         probes += int(sum(c for c, m in zip(counts, moved) if m))
         it_prev = it_now
     # ---------------- e2e: through the C ABI from pinned host buffers
+    # the caller's inputs of a shared-system batch: the system's prior blocks and
+    # anchored-mean responses (optimizer.batch_parts, once per system) and every
+    # plan's start and goal; the per-plan information / prior mean / initial mean
+    # are expanded on the device (gvp_engine_load_boundary, run_pgvimp_batch's path)
+    from paper_2411_03416_b200.optimizer import batch_parts
+
     pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()  # noqa: E731
-    h_kd, h_ko = pin(prior.prec.diag_stack), pin(prior.prec.off_stack)
-    h_info, h_pm, h_m0 = pin(to_plan_minor(info)), pin(to_plan_minor(pmean)), pin(to_plan_minor(init))
+    base, resp0, respg, anchor, x0a, goala = batch_parts(
+        P.point_robot_lti(2)(N_INTERVALS, T_TOTAL / N_INTERVALS), np.zeros(4), goals, 1.0, 1e-3)
+    h_in = [pin(a) for a in (base.prec.diag_stack, base.prec.off_stack, base.info, base.mean, resp0, respg,
+                             anchor, x0a, goala)]
     h_rec = torch.empty((max_iters, B, 8), dtype=torch.float64).pin_memory().numpy()
     # the results a caller needs: records, final means and marginal covariances (packed)
     h_mean = torch.empty((K, n, B), dtype=torch.float64).pin_memory().numpy()
     h_cov = torch.empty((K, n * (n + 1) // 2, B), dtype=torch.float64).pin_memory().numpy()
-    h2d = h_kd.nbytes + h_ko.nbytes + h_info.nbytes + h_pm.nbytes + h_m0.nbytes
+    h2d = sum(a.nbytes for a in h_in)
     barrier()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     t_wall = time.perf_counter()
     e0.record(stream)
-    eng.lib.gvp_engine_load(eng.handle, _native.ptr(h_kd), _native.ptr(h_ko), _native.ptr(h_info),
-                            _native.ptr(h_pm), _native.ptr(h_m0))
+    eng.lib.gvp_engine_load_boundary(eng.handle, *[_native.ptr(a) for a in h_in])
     eng.step(args.steps)
     eng.lib.gvp_engine_get_records(eng.handle, _native.ptr(h_rec))
     eng.packed_into(mean=h_mean, covs=h_cov)
@@ -659,7 +666,7 @@ def main():
                                           "traffic_unit": "bytes/launch (ncu dram read+write, C5 mid-run)"}},
             "e2e": {"value": e2e_value, "unit": "factor-evals/s", "h2d_bytes_per_step": h2d // max(args.steps, 1),
                     "d2h_bytes_per_step": d2h // max(args.steps, 1),
-                    "what": "gvp_engine_load from pinned host + steps + D2H of the records, final means and packed marginal covariances, one C-ABI call chain"},
+                    "what": "gvp_engine_load_boundary from pinned host (the system's prior blocks and anchored-mean responses, every plan's start and goal; per-plan arrays expanded on the device) + steps + D2H of the records, final means and packed marginal covariances, one C-ABI call chain"},
             "clocks": clk.summary(),
         }
     eng.close()  # release the timed batch

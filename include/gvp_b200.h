@@ -196,6 +196,15 @@ int gvp_engine_load(gvp_engine* e, const double* kdiag, const double* koff, cons
 /* Same, from device pointers (no host traffic). */
 int gvp_engine_load_dev(gvp_engine* e, const double* kdiag, const double* koff,
                         const double* info, const double* prior_mean, const double* init_mean);
+/* A shared-prior batch by its boundary states (optimizer.batch_problem's
+ * affine construction, expanded on the device): kdiag/koff as above, plan 0's
+ * info and prior mean (nknots, n), the anchored-mean responses to unit start /
+ * goal offsets resp0/respg (n, nknots, n), the anchor block (n, n), and every
+ * plan's start and goal (nplans, n). Initial mean: initial_mean's straight
+ * line (OptimizerConfig.init default). */
+int gvp_engine_load_boundary(gvp_engine* e, const double* kdiag, const double* koff, const double* base_info,
+                             const double* base_mean, const double* resp0, const double* respg,
+                             const double* anchor, const double* x0s, const double* goals);
 
 /* Run up to `iters` more iterations of Algorithm 1 for every active plan
  * (asynchronous on the engine stream unless sync != 0). */

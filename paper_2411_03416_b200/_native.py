@@ -77,6 +77,7 @@ _SIGS = {
                                     C.c_double, _dp, _dp, C.c_int64, C.POINTER(PlanConfig)]),
     "gvp_engine_destroy": (None, [C.c_void_p]),
     "gvp_engine_load": (C.c_int, [C.c_void_p, _dp, _dp, _dp, _dp, _dp]),
+    "gvp_engine_load_boundary": (C.c_int, [C.c_void_p, _dp, _dp, _dp, _dp, _dp, _dp, _dp, _dp, _dp]),
     "gvp_engine_load_dev": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                                       C.c_void_p]),
     "gvp_engine_step": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32]),

@@ -212,6 +212,51 @@ __global__ void count_active_kernel(int B, const int* active, int* out) {
 }
 
 inline unsigned nblk(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
+// The per-plan problem of a batch sharing one system (optimizer.batch_problem,
+// SURVEY §8e): information and anchored prior mean are affine in each plan's
+// start / goal offset from plan 0's, the initial mean is initial_mean's
+// straight line (optimizer.py:280-296). One thread per (knot, coordinate,
+// plan), plan-minor outputs; plans >= nreal (padding) copy plan 0.
+__global__ void expand_boundary_kernel(int B, int nreal, int64_t K, int n, const double* __restrict__ bnd,
+                                       double* __restrict__ info, double* __restrict__ pmean,
+                                       double* __restrict__ mean) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= K * n * B) return;
+  const int b = (int)(t % B);
+  const int64_t kr = t / B, k = kr / n;
+  const int r = (int)(kr - k * n);
+  const double* base_info = bnd;
+  const double* base_mean = bnd + K * n;
+  const double* resp0 = base_mean + K * n;           // (n, K, n)
+  const double* respg = resp0 + (int64_t)n * K * n;  // (n, K, n)
+  const double* anchor = respg + (int64_t)n * K * n; // (n, n)
+  const double* x0s = anchor + n * n;                // (nreal, n) [B rows reserved]
+  const double* goals = x0s + (int64_t)B * n;
+  const int bs = b < nreal ? b : 0;
+  const double* x0 = x0s + (int64_t)bs * n;
+  const double* g = goals + (int64_t)bs * n;
+  double inf = base_info[k * n + r];
+  if (k == 0) {
+    double t0 = 0.0;  // (d0 @ anchor.T)[r]
+    for (int j = 0; j < n; ++j) t0 += (x0[j] - x0s[j]) * anchor[r * n + j];
+    inf += t0;
+  }
+  if (k == K - 1) {
+    double tg = 0.0;
+    for (int j = 0; j < n; ++j) tg += (g[j] - goals[j]) * anchor[r * n + j];
+    inf += tg;
+  }
+  double m0 = 0.0, mg = 0.0;  // sum_j d0_j resp0[j], sum_j dg_j respg[j]
+  for (int j = 0; j < n; ++j) {
+    m0 += (x0[j] - x0s[j]) * resp0[((int64_t)j * K + k) * n + r];
+    mg += (g[j] - goals[j]) * respg[((int64_t)j * K + k) * n + r];
+  }
+  const double a = (double)k * (1.0 / (double)(K - 1 > 0 ? K - 1 : 1));  // np.linspace(0, 1, K)
+  info[t] = inf;
+  pmean[t] = (base_mean[k * n + r] + m0) + mg;
+  mean[t] = (1.0 - a) * x0[r] + a * g[r];
+}
+
 }  // namespace
 
 struct gvp_engine {
@@ -232,6 +277,8 @@ struct gvp_engine {
   double *kdiag = nullptr, *koff = nullptr, *info = nullptr, *pmean = nullptr;
   double *gmu = nullptr, *gdiag = nullptr, *v = nullptr, *epsi = nullptr, *scratch = nullptr;
   double *kfull_d = nullptr;  // staging for full-block prior uploads
+  double* bnd = nullptr;       // gvp_engine_load_boundary staging (bnd_doubles())
+  int64_t bnd_doubles() const { return 2 * K * n + 2 * (int64_t)n * K * n + (int64_t)n * n + 2 * (int64_t)B * n; }
   double* records = nullptr;
   double* scal = nullptr;
   int* ints = nullptr;
@@ -406,7 +453,7 @@ extern "C" int gvp_engine_create(gvp_engine** out, int32_t nplans, int64_t nknot
       (r = e->alloc(&e->kfull_d, K * N2 * kb)) || (r = e->alloc(&e->scratch, (size_t)scr)) ||
       (r = e->alloc(&e->records, (size_t)cfg->max_iters * B * GVP_NREC)) ||
       (r = e->alloc(&e->scal, 10 * B)) || (r = e->alloc(&e->ints, 10 * B + 1)) ||
-      (r = e->alloc(&e->oob, B)) ||
+      (r = e->alloc(&e->oob, B)) || (r = e->alloc(&e->bnd, (size_t)e->bnd_doubles())) ||
       (r = e->alloc(&e->eigh_list, (size_t)(1 + B * std::max<int64_t>(K - 2, 1)))))
     return fail(r);
   if (cudaMemset(e->eigh_list, 0, sizeof(int)) != cudaSuccess) return fail(GVP_ERR_CUDA);
@@ -504,6 +551,42 @@ extern "C" int gvp_engine_load(gvp_engine* e, const double* kdiag, const double*
                                const double* info, const double* prior_mean,
                                const double* init_mean) {
   return engine_upload(e, kdiag, koff, info, prior_mean, init_mean, cudaMemcpyHostToDevice);
+}
+
+// Upload a shared-system batch by its boundary states (see expand_boundary_kernel):
+// host pointers; kdiag / koff as for gvp_engine_load (one plan's blocks),
+// base_info / base_mean (K, n) of plan 0's prior, resp0 / respg (n, K, n) the
+// anchored-mean responses to unit start / goal offsets, anchor (n, n), x0s /
+// goals (nplans, n). The initial mean is initial_mean's straight line.
+extern "C" int gvp_engine_load_boundary(gvp_engine* e, const double* kdiag, const double* koff,
+                                        const double* base_info, const double* base_mean, const double* resp0,
+                                        const double* respg, const double* anchor, const double* x0s,
+                                        const double* goals) {
+  if (!e || !kdiag || !koff || !base_info || !base_mean || !resp0 || !respg || !anchor || !x0s || !goals)
+    return GVP_ERR_ARG;
+  if (!e->shared_prior) {
+    set_error("gvp_engine_load_boundary needs a shared-prior engine");
+    return GVP_ERR_ARG;
+  }
+  const int64_t K = e->K, n = e->n, N2 = n * n, Kn = K * n;
+  cudaStream_t s = e->stream;
+  GVP_CUDA(cudaMemcpyAsync(e->kfull_d, kdiag, K * N2 * 8, cudaMemcpyHostToDevice, s));
+  for (int col = 0; col < 2; ++col)  // 2-wide copy of the shared off blocks
+    GVP_CUDA(cudaMemcpy2DAsync(e->koff + col, 16, koff, 8, 8, (K - 1) * N2, cudaMemcpyHostToDevice, s));
+  double* d = e->bnd;
+  GVP_CUDA(cudaMemcpyAsync(d, base_info, Kn * 8, cudaMemcpyHostToDevice, s));
+  GVP_CUDA(cudaMemcpyAsync(d + Kn, base_mean, Kn * 8, cudaMemcpyHostToDevice, s));
+  GVP_CUDA(cudaMemcpyAsync(d + 2 * Kn, resp0, n * Kn * 8, cudaMemcpyHostToDevice, s));
+  GVP_CUDA(cudaMemcpyAsync(d + 2 * Kn + n * Kn, respg, n * Kn * 8, cudaMemcpyHostToDevice, s));
+  double* da = d + 2 * Kn + 2 * n * Kn;
+  GVP_CUDA(cudaMemcpyAsync(da, anchor, N2 * 8, cudaMemcpyHostToDevice, s));
+  GVP_CUDA(cudaMemcpyAsync(da + N2, x0s, (size_t)e->nreal * n * 8, cudaMemcpyHostToDevice, s));
+  GVP_CUDA(cudaMemcpyAsync(da + N2 + (int64_t)e->B * n, goals, (size_t)e->nreal * n * 8, cudaMemcpyHostToDevice, s));
+  const int64_t tot = K * n * e->B;
+  expand_boundary_kernel<<<nblk(tot, 256), 256, 0, s>>>(e->B, e->nreal, K, (int)n, d, e->info, e->pmean, e->mean);
+  GVP_CUDA(cudaGetLastError());
+  ++e->launches;
+  return engine_reset(e);
 }
 
 extern "C" int gvp_engine_load_dev(gvp_engine* e, const double* kdiag, const double* koff,

@@ -99,6 +99,15 @@ class PlanBatch:
         self._ok(self.lib.gvp_engine_load(self.handle, N.ptr(kd), N.ptr(ko), N.ptr(inf), N.ptr(pm),
                                           N.ptr(m0)), "gvp_engine_load")
 
+    def load_boundary(self, kdiag, koff, base_info, base_mean, resp0, respg, anchor, x0s, goals):
+        """A shared-prior batch by its boundary states (optimizer.batch_parts):
+        plan 0's prior blocks / info / mean, the responses (n, K, n) and anchor
+        (n, n), every plan's start and goal (B, n); the per-plan information,
+        prior mean and straight-line initial mean are formed on the device."""
+        a = [N.f64(x) for x in (kdiag, koff, base_info, base_mean, resp0, respg, anchor, x0s, goals)]
+        self._ok(self.lib.gvp_engine_load_boundary(self.handle, *[N.ptr(x) for x in a]),
+                 "gvp_engine_load_boundary")
+
     def load_device(self, kdiag_ptr, koff_ptr, info_ptr, pmean_ptr, mean_ptr):
         """Device pointers already in the plan-minor layout (no host traffic)."""
         self._ok(self.lib.gvp_engine_load_dev(self.handle, kdiag_ptr, koff_ptr, info_ptr,

@@ -397,27 +397,18 @@ class BatchResult:
     wall_time_ms: float
 
 
-def batch_problem(sys_ltv: LTVSystem, x0s, goals, q_c: float, sigma_b: float, cfg: OptimizerConfig):
-    """The priors of B plans that share the system, q_c and sigma_b (SURVEY §8e
-    batch axis) without B prior assemblies: the anchored precision does not
-    depend on the boundary states, the information vector only at the two
-    anchor knots (prior.py:140-150), and the anchored mean / flow are affine in
-    them — so one prior (plan 0's) plus 2n unit responses of the mean solve
-    (on the device) give every plan's. Returns (prior of plan 0, info (B,K,n),
-    prior mean (B,K,n), initial mean (B,K,n))."""
+def batch_parts(sys_ltv: LTVSystem, x0s, goals, q_c: float, sigma_b: float):
+    """The shared part of a batch's priors (see batch_problem): plan 0's prior,
+    the anchored-mean responses to unit start / goal offsets resp0 / respg
+    (n, K, n), the anchor block, and the (B, n) starts and goals."""
     x0s = np.atleast_2d(np.asarray(x0s, dtype=np.float64))
     goals = np.atleast_2d(np.asarray(goals, dtype=np.float64))
     B = max(len(x0s), len(goals))
-    x0s = np.broadcast_to(x0s, (B, x0s.shape[1]))
-    goals = np.broadcast_to(goals, (B, goals.shape[1]))
+    x0s = np.ascontiguousarray(np.broadcast_to(x0s, (B, x0s.shape[1])))
+    goals = np.ascontiguousarray(np.broadcast_to(goals, (B, goals.shape[1])))
     base = assemble_prior(sys_ltv, x0s[0], goals[0], q_c, sigma_b)
     K, n = base.nsteps + 1, base.n
     anchor = np.eye(n) / sigma_b ** 2
-    d0, dg = x0s - x0s[0], goals - goals[0]
-    info = np.repeat(base.info.reshape(1, K, n), B, axis=0)
-    info[:, 0, :] += d0 @ anchor.T
-    info[:, -1, :] += dg @ anchor.T
-    # anchored-mean responses to a unit change of each start / goal coordinate
     from .prior import anchored_mean
 
     resp0, respg = np.zeros((n, K, n)), np.zeros((n, K, n))
@@ -427,6 +418,23 @@ def batch_problem(sys_ltv: LTVSystem, x0s, goals, q_c: float, sigma_b: float, cf
         resp0[j] = anchored_mean(base.prec, e.reshape(-1)).reshape(K, n)
         e[0], e[-1] = 0.0, anchor[:, j]
         respg[j] = anchored_mean(base.prec, e.reshape(-1)).reshape(K, n)
+    return base, resp0, respg, anchor, x0s, goals
+
+
+def batch_problem(sys_ltv: LTVSystem, x0s, goals, q_c: float, sigma_b: float, cfg: OptimizerConfig):
+    """The priors of B plans that share the system, q_c and sigma_b (SURVEY §8e
+    batch axis) without B prior assemblies: the anchored precision does not
+    depend on the boundary states, the information vector only at the two
+    anchor knots (prior.py:140-150), and the anchored mean / flow are affine in
+    them — so one prior (plan 0's) plus 2n unit responses of the mean solve
+    (on the device) give every plan's. Returns (prior of plan 0, info (B,K,n),
+    prior mean (B,K,n), initial mean (B,K,n))."""
+    base, resp0, respg, anchor, x0s, goals = batch_parts(sys_ltv, x0s, goals, q_c, sigma_b)
+    B, K, n = len(x0s), base.nsteps + 1, base.n
+    d0, dg = x0s - x0s[0], goals - goals[0]
+    info = np.repeat(base.info.reshape(1, K, n), B, axis=0)
+    info[:, 0, :] += d0 @ anchor.T
+    info[:, -1, :] += dg @ anchor.T
     pmean = (base.mean.reshape(1, K, n) + np.einsum("bj,jkn->bkn", d0, resp0)
              + np.einsum("bj,jkn->bkn", dg, respg))
     if cfg.init_mean is not None:
@@ -454,14 +462,23 @@ def run_pgvimp_batch(sys_ltv: LTVSystem, env: Environment | None, cfg: Optimizer
     out with their status; the batch never aborts."""
     cfg.validate()
     t0 = time.perf_counter()
-    base, info, pmean, init = batch_problem(sys_ltv, x0s, goals, q_c, sigma_b, cfg)
-    B, K, n = info.shape
+    line_init = cfg.init_mean is None and cfg.init not in ("flow", "prior")
+    if line_init:  # the per-plan arrays are expanded on the device from the boundary states
+        base, resp0, respg, anchor, x0a, goala = batch_parts(sys_ltv, x0s, goals, q_c, sigma_b)
+        B, K, n = len(x0a), base.nsteps + 1, base.n
+    else:
+        base, info, pmean, init = batch_problem(sys_ltv, x0s, goals, q_c, sigma_b, cfg)
+        B, K, n = info.shape
     rule = smolyak_rule(cfg.k_q, n)
     sdf = env.sdf if env is not None else far_field()
     model = env.model if env is not None else CollisionModel(0.0, 1.0)
     eng = PlanBatch(B, K, n, sdf, model, rule, cfg, shared_prior=True, spec_lanes=spec_lanes)
     try:
-        eng.load(base.prec.diag_stack, base.prec.off_stack, info, pmean, init)
+        if line_init:
+            eng.load_boundary(base.prec.diag_stack, base.prec.off_stack, base.info, base.mean, resp0, respg,
+                              anchor, x0a, goala)
+        else:
+            eng.load(base.prec.diag_stack, base.prec.off_stack, info, pmean, init)
         eng.run()
         st = eng.state()
         sm = eng.summary()

@@ -214,3 +214,40 @@ def test_profiled_iterations_match_graphed_ones(P):
         eng.close()
     assert np.array_equal(recs[0], recs[1], equal_nan=True)
     assert np.array_equal(recs[0], recs[2], equal_nan=True)
+
+
+def test_boundary_load_matches_host_batch_problem(P):
+    """gvp_engine_load_boundary (the per-plan info / prior mean / initial mean
+    expanded on the device from the boundary states) solves the same batch
+    as gvp_engine_load of optimizer.batch_problem's host arrays."""
+    from paper_2411_03416_b200.optimizer import batch_parts, batch_problem
+
+    env = c1_env(P)
+    sys_ltv = P.point_robot_lti(2)(50, 3.0 / 50)
+    rng = np.random.default_rng(7)
+    B = 9  # odd: the engine pads a copy of plan 0
+    x0s = np.zeros((B, 4))
+    x0s[:, :2] = rng.uniform(-0.2, 0.2, (B, 2))
+    goals = np.tile(np.array([2.0, 1.5, 0.0, 0.0]), (B, 1))
+    goals[:, :2] += rng.uniform(-0.3, 0.3, (B, 2))
+    cfg = P.OptimizerConfig(k_q=3, kl_bound=10.0, beta_max=0.5, max_iters=8)
+    K = 51
+    base, info, pmean, init = batch_problem(sys_ltv, x0s, goals, 1.0, 1e-3, cfg)
+    parts = batch_parts(sys_ltv, x0s, goals, 1.0, 1e-3)
+    out = []
+    for mode in ("host", "boundary"):
+        eng = P.PlanBatch(B, K, 4, env.sdf, env.model, P.smolyak_rule(3, 4), cfg, shared_prior=True)
+        if mode == "host":
+            eng.load(base.prec.diag_stack, base.prec.off_stack, info, pmean, init)
+        else:
+            b0, r0, rg, an, xa, ga = parts
+            eng.load_boundary(b0.prec.diag_stack, b0.prec.off_stack, b0.info, b0.mean, r0, rg, an, xa, ga)
+        m0 = eng.mean().copy()
+        eng.step(8, sync=True)
+        out.append((m0, eng.records(), eng.mean()))
+        eng.close()
+    assert rel_err(out[1][0], out[0][0]) <= 1e-14  # the straight-line initial means
+    assert np.array_equal(out[1][1][:, :, 0], out[0][1][:, :, 0], equal_nan=True)  # beta sequences
+    fin = np.isfinite(out[0][1][:, :, 2])
+    assert rel_err(out[1][1][:, :, 2:6][fin], out[0][1][:, :, 2:6][fin]) <= 1e-9
+    assert rel_err(out[1][2], out[0][2]) <= 1e-9
