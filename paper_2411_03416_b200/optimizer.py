@@ -219,7 +219,10 @@ def cost_breakdown(cur: JointGaussian, prior: DiscretePrior, temp: float,
                 raise ValueError("rule required to evaluate collision cost")
             factor_values = evaluate_all_factors(cur.mean, cur.prec, env.sdf, env.model, rule,
                                                  threads=threads, marginals=marginals)
-    collision = float(sum(f.e_psi for f in factor_values))
+    if isinstance(factor_values, _StageArrays):  # same left-to-right float sum, no per-factor objects
+        collision = float(sum(factor_values.e_psi.tolist()))
+    else:
+        collision = float(sum(f.e_psi for f in factor_values))
     return CostBreakdown(prior_cost=prior_cost, collision_cost=collision,
                          entropy_cost=-temp * (entropy_of(cur.prec) if logdet is None else
                                                0.5 * (cur.prec.dim * (_LOG_2PI + 1.0) - logdet)))
@@ -271,6 +274,34 @@ def _raise_plan_status(status: int, where: int, cfg: OptimizerConfig):
         raise RuntimeError(f"plan failed with status {status}")
 
 
+class _StageArrays:
+    """A device factor stage as arrays (e_psi (F,), g_mu (F, n), g_sigma (F, n, n))
+    for the interior unary collision factors (factors.py:159-164): the host loop
+    scatters them with block writes and cost_breakdown sums e_psi in factor
+    order, without one FactorGradient object per factor."""
+
+    __slots__ = ("e_psi", "g_mu", "g_sigma")
+
+    def __init__(self, e_psi, g_mu, g_sigma):
+        self.e_psi, self.g_mu, self.g_sigma = e_psi, g_mu, g_sigma
+
+    def __len__(self):
+        return len(self.e_psi)
+
+    def __iter__(self):
+        return (FactorGradient(e_psi=float(e), g_mu=gm, g_sigma=gs)
+                for e, gm, gs in zip(self.e_psi, self.g_mu, self.g_sigma))
+
+    def joint(self, K: int, n: int):
+        """assemble_joint_gradients (factors.py:228-255) for factors 1..K-2: each
+        block receives exactly one addend, added to the zero block in one sweep."""
+        g_mu = np.zeros((K, n))
+        g_mu[1:K - 1] += self.g_mu
+        g_s = BlockTridiagonalMatrix.zeros(K, n)
+        g_s.diag_stack[1:K - 1] += self.g_sigma
+        return g_mu.reshape(-1), g_s
+
+
 def _run_pgvimp_host(prior: DiscretePrior, env, cfg: OptimizerConfig, t0: float) -> RunResult:
     """Algorithm 1 (optimizer.py:299-401) as the reference's host loop, every
     kernel on the GPU: for block sizes the fused engine does not cover (the
@@ -288,7 +319,7 @@ def _run_pgvimp_host(prior: DiscretePrior, env, cfg: OptimizerConfig, t0: float)
     def factors(joint: JointGaussian, marg: ChainMarginals):
         if isinstance(env, ArmEnvironment):
             e_psi, g_mu, g_s = env.factor_gradients(joint.mean, np.stack(marg.covs), rule)
-            return [FactorGradient(e_psi=float(e), g_mu=gm, g_sigma=gs) for e, gm, gs in zip(e_psi, g_mu, g_s)]
+            return _StageArrays(e_psi, g_mu, g_s)
         return evaluate_all_factors(joint.mean, joint.prec, env.sdf, env.model, rule, threads=cfg.threads,
                                     marginals=marg)
 
@@ -303,7 +334,10 @@ def _run_pgvimp_host(prior: DiscretePrior, env, cfg: OptimizerConfig, t0: float)
         t_iter = time.perf_counter()
         if env is not None:
             fv = cached if cached is not None else factors(cur, result.marginals)
-            g_mu, g_sigma = assemble_joint_gradients(fv, maps, K, n)
+            if isinstance(fv, _StageArrays):
+                g_mu, g_sigma = fv.joint(K, n)
+            else:
+                g_mu, g_sigma = assemble_joint_gradients(fv, maps, K, n)
         else:
             g_mu, g_sigma = np.zeros(K * n), BlockTridiagonalMatrix.zeros(K, n)
         step = select_step_size(cur, prior, g_mu, g_sigma, cfg, temp, logdet_cur=ld_cur)
