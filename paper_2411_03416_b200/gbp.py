@@ -38,14 +38,20 @@ class ChainMarginals:
 
     @classmethod
     def from_stacks(cls, covs: np.ndarray, crosses: np.ndarray) -> "ChainMarginals":
-        return cls(covs=tuple(covs), crosses=tuple(crosses))
+        m = cls(covs=tuple(covs), crosses=tuple(crosses))
+        object.__setattr__(m, "_stacks", (covs, crosses))  # the kernels' arrays, reused as is
+        return m
 
     @property
     def covs_stack(self) -> np.ndarray:
-        return np.stack(self.covs)
+        st = getattr(self, "_stacks", None)
+        return st[0] if st is not None else np.stack(self.covs)
 
     @property
     def crosses_stack(self) -> np.ndarray:
+        st = getattr(self, "_stacks", None)
+        if st is not None:
+            return st[1]
         n = self.covs[0].shape[0]
         return np.stack(self.crosses) if len(self.crosses) else np.zeros((0, n, n))
 
@@ -85,8 +91,8 @@ def gbp_mean_solve(prec: BlockTridiagonalMatrix, info: np.ndarray) -> np.ndarray
 
 def trace_product(a: BlockTridiagonalMatrix, marg: ChainMarginals) -> float:
     """tr(A Sigma) over A's block-tridiagonal sparsity (gbp.py:109-120)."""
-    covs = np.stack(marg.covs)
+    covs = marg.covs_stack
     total = float(np.einsum("kij,kji->", a.diag_stack, covs))
     if a.nblocks > 1:
-        total += 2.0 * float(np.einsum("kij,kij->", a.off_stack, np.stack(marg.crosses)))
+        total += 2.0 * float(np.einsum("kij,kij->", a.off_stack, marg.crosses_stack))
     return total

@@ -318,7 +318,7 @@ def _run_pgvimp_host(prior: DiscretePrior, env, cfg: OptimizerConfig, t0: float)
 
     def factors(joint: JointGaussian, marg: ChainMarginals):
         if isinstance(env, ArmEnvironment):
-            e_psi, g_mu, g_s = env.factor_gradients(joint.mean, np.stack(marg.covs), rule)
+            e_psi, g_mu, g_s = env.factor_gradients(joint.mean, marg.covs_stack, rule)
             return _StageArrays(e_psi, g_mu, g_s)
         return evaluate_all_factors(joint.mean, joint.prec, env.sdf, env.model, rule, threads=cfg.threads,
                                     marginals=marg)
