@@ -505,11 +505,14 @@ int upload_step(Context& C, const double* mean, const double* diag, const double
   GVP_TRY(h2d(b.info, info, K * n, s));
   GVP_TRY(h2d(b.gmu, g_mu, K * n, s));
   GVP_TRY(h2d(b.gdiag, gdiag, K * B2, s));
-  if (goff) GVP_TRY(h2d(b.goff, goff, (K - 1) * B2, s));
+  // unary factors leave the gradient's off blocks zero (factors.py:228-255): an
+  // all-zero goff is neither uploaded nor read (the same bits: 0 * 2/T + x = x)
+  const bool has_goff = goff && !all_zero(goff, (K - 1) * B2);
+  if (has_goff) GVP_TRY(h2d(b.goff, goff, (K - 1) * B2, s));
   pb = StepProblem{pview(b.mean, n, 1),  pview(b.diag, B2, 1), pview(b.off, B2, 1),
                    pview(b.kdiag, B2, 1), pview(b.koff, B2, 1), pview(b.info, n, 1),
                    pview(b.gmu, n, 1),   pview(b.gdiag, B2, 1), pview(b.goff, B2, 1),
-                   goff != nullptr,      pview(b.mean, n, 1),   false};
+                   has_goff,             pview(b.mean, n, 1),   false};
   return GVP_OK;
 }
 }  // namespace
